@@ -1,0 +1,214 @@
+/*
+ * sparsemlp_b200.h -- C ABI of the B200 (sm_100a) static-sparse MLP training path.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `sparsemlp` (arxiv 2407.17437, "Nerva"): the four CSR kernels of
+ * pkg/src/sparsemlp/_kernels.py, the validated operators of tensor_core.py that
+ * wrap them, and the per-step glue of nn.py / train.py that runs between them
+ * (bias, ReLU, softmax cross-entropy, optimizer arithmetic, batch gather,
+ * Xavier init).  The reference binds its kernels by name from Python
+ * (nn.py:16-23 imports spmm/spmm_transposed/sddmm/sparse_combine from
+ * tensor_core); a maintainer would bind these symbols with ctypes instead
+ * (see INTEGRATION.md).
+ *
+ * Conventions (all entry points):
+ *   - every pointer is a DEVICE pointer unless documented otherwise; the caller
+ *     owns all buffers (the library never allocates on the hot path);
+ *   - dense operands are row-major [rows x ld] with the logical width `n`
+ *     (the reference's feature-major [features, batch] layout, nn.py:3-8);
+ *   - `dtype` is SMB_F32 or SMB_F64 (CsrMatrix accepts both,
+ *     tensor_core.py:170-171); engine-only ops are float32;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *   - calls are stream-ordered, never synchronise, and are reentrant on
+ *     disjoint outputs;
+ *   - return value: SMB_OK, or an SMB_ERR_* code with a message available from
+ *     smb_last_error() (thread-local).  The Python layer maps
+ *     SMB_ERR_INVALID -> InvalidArgumentError and SMB_ERR_STATE -> StateError
+ *     (errors.py:4-9).
+ *
+ * Rounding contract ("exact" kernels): every output element is accumulated in
+ * ascending source index with multiply and add rounded separately (no FMA
+ * contraction), exactly as the numba kernels do with fastmath off
+ * (_kernels.py:1-6).  spmm, spmm_t, sddmm, axpby, the fused optimizer update,
+ * row_sums (numpy pairwise order) and relu/relu_backward are therefore
+ * bit-identical to the reference given identical inputs.
+ */
+#ifndef SPARSEMLP_B200_H
+#define SPARSEMLP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SMB_API __attribute__((visibility("default")))
+#else
+#define SMB_API
+#endif
+
+#define SMB_ABI_VERSION 1
+
+/* status codes */
+#define SMB_OK 0
+#define SMB_ERR_INVALID 1 /* InvalidArgumentError (errors.py:4) */
+#define SMB_ERR_STATE 2   /* StateError (errors.py:8) */
+#define SMB_ERR_CUDA 3    /* CUDA launch / runtime failure */
+
+/* value dtypes */
+#define SMB_F32 0
+#define SMB_F64 1
+
+/* epilogues of smb_spmm */
+#define SMB_EPI_NONE 0
+#define SMB_EPI_RELU 1 /* y = max(y, 0) as np.maximum (nn.py:86-87) */
+
+/* optimizer kinds (nn.py:42-72, SparseLinearLayer.optimize nn.py:187-198) */
+#define SMB_OPT_NONE 0     /* gradient only, no update */
+#define SMB_OPT_GD 1       /* w += f(-eta) * g                                   nn.py:196-197 */
+#define SMB_OPT_MOMENTUM 2 /* v = f(mu) v + g;  w += f(-eta) * v                 nn.py:190,194-195 */
+#define SMB_OPT_NESTEROV 3 /* v = f(mu) v + g;  w += f(-eta*mu) v;  w += f(-eta) g  nn.py:190-193 */
+
+/* ---- library info -------------------------------------------------------- */
+
+SMB_API int smb_abi_version(void);
+/* Thread-local message of the last failing call on this thread ("" if none). */
+SMB_API const char* smb_last_error(void);
+/* Number of kernels this library has launched in this process (all threads). */
+SMB_API uint64_t smb_launch_count(void);
+
+/* ---- the four reference kernels ------------------------------------------ */
+
+/* out[i,:] = sum_{p in row i, ascending} values[p] * dense[col_idx[p], :]
+ *            (+ bias[i]) (then ReLU if epilogue == SMB_EPI_RELU).
+ * Replaces _kernels.spmm_kernel (_kernels.py:25-37) via tensor_core.spmm
+ * (tensor_core.py:227-240), fused with the bias add of
+ * SparseLinearLayer.forward (nn.py:173) and ReLU.forward (nn.py:86-87).
+ * Rows without nonzeros produce bias (or 0). m x k CSR, dense k x n, out m x n. */
+SMB_API int smb_spmm(int dtype, const int32_t* row_ptr, const int32_t* col_idx, const void* values,
+             int64_t m, int64_t k, const void* dense, int64_t ld_dense, int64_t n,
+             const void* bias, int epilogue, void* out, int64_t ld_out, void* stream);
+
+/* ---- SparsityPattern handle (tensor_core.py:97-152) -------------------------
+ * The static CSR structure shared by a layer's weights, gradient and velocity
+ * (nn.py:148-158), plus the indices derived from it once per layer:
+ * a CSC transpose index (col_ptr[k+1], row_idx[nnz] ascending inside each
+ * column, perm[nnz] = CSC slot -> CSR value index), which replaces the
+ * O(nblocks*nnz) rescan of _kernels.spmm_t_kernel (_kernels.py:40-59), and the
+ * SDDMM tile index.  row_ptr / col_idx are BORROWED device arrays and must
+ * outlive the handle; the pattern is immutable (tensor_core.py:128-133).
+ * With validate != 0 the structure is checked on the device like
+ * tensor_core._validate_structure (tensor_core.py:78-94) and a violation
+ * returns SMB_ERR_INVALID with the reference's message.  Setup-time call: it
+ * allocates and synchronises `stream`. */
+typedef struct smb_pattern smb_pattern;
+SMB_API int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx, int64_t m, int64_t k,
+                       int64_t nnz, int validate, void* stream, smb_pattern** out);
+SMB_API int smb_pattern_destroy(smb_pattern* pattern);
+/* copy the CSC index into caller-owned device buffers (col_ptr[k+1],
+ * row_idx[nnz], perm[nnz]; any may be NULL), stream-ordered. */
+SMB_API int smb_pattern_csc(const smb_pattern* pattern, int32_t* col_ptr, int32_t* row_idx,
+                            int32_t* perm, void* stream);
+
+/* out[c,:] = sum_{i ascending} values[perm[q]] * dense[i,:] over the column-c
+ * slots q of the CSC index, then out *= (mask[c,:] > 0) when mask != NULL.
+ * Replaces _kernels.spmm_t_kernel (_kernels.py:40-59) via
+ * tensor_core.spmm_transposed (tensor_core.py:243-255), fused with
+ * ReLU.backward of the layer below (nn.py:89-91: d * (x_cached > 0); the
+ * post-activation A satisfies A > 0 <=> x_cached > 0).  `values` are in CSR
+ * order.  dense m x n, out k x n. */
+SMB_API int smb_spmm_t(int dtype, const smb_pattern* pattern, const void* values, const void* dense,
+               int64_t ld_dense, int64_t n, const void* mask, int64_t ld_mask, void* out,
+               int64_t ld_out, void* stream);
+
+/* out_values[p] = a[i,0]*b[j,0] + a[i,1]*b[j,1] + ... (sequential over the
+ * n columns) for the p-th stored (i, j).  n == 0 gives zeros.
+ * Replaces _kernels.sddmm_kernel (_kernels.py:62-75) via tensor_core.sddmm
+ * (tensor_core.py:258-288).  a m x n, b k x n. */
+SMB_API int smb_sddmm(int dtype, const smb_pattern* pattern, const void* a, int64_t lda, const void* b,
+              int64_t ldb, int64_t n, void* out_values, void* stream);
+
+/* s[p] = T(alpha) * s[p] + T(beta) * t[p]   (alpha/beta pre-cast to the value
+ * dtype as tensor_core.py:304-305).  Replaces _kernels.axpby_kernel
+ * (_kernels.py:78-83) via tensor_core.sparse_combine (tensor_core.py:291-306). */
+SMB_API int smb_axpby(int dtype, double alpha, void* s, double beta, const void* t, int64_t count,
+              void* stream);
+
+/* ---- fused training-step ops ---------------------------------------------- */
+
+/* One launch for the whole weight side of SparseLinearLayer.backward+optimize
+ * (nn.py:178-198): grad = sddmm(pattern, d_out, x) (nn.py:183),
+ * grad_bias = row_sums(d_out) (nn.py:184, numpy pairwise order), then the
+ * optimizer update of values/velocity (the sparse_combine sequence
+ * nn.py:189-197) and of bias/velocity_bias (_step_vector, nn.py:118-131).
+ * With opt_kind == SMB_OPT_NONE nothing is updated and grad_out /
+ * grad_bias_out receive the gradients (data-parallel path: allreduce, then
+ * smb_optimizer_step).  grad_out / grad_bias_out may be NULL otherwise.
+ * velocity / velocity_bias may be NULL for SMB_OPT_GD and SMB_OPT_NONE.
+ * bias / velocity_bias / grad_bias_out may all be NULL (no bias).
+ * NOTE: spmm_t of this layer must run BEFORE this call (it reads pre-update
+ * values, train.py:400-401). */
+SMB_API int smb_sddmm_update(int dtype, const smb_pattern* pattern, const void* d_out, int64_t ld_dout,
+                     const void* x, int64_t ld_x, int64_t n, void* values, void* velocity,
+                     void* grad_out, void* bias, void* velocity_bias, void* grad_bias_out,
+                     int opt_kind, double mu, double eta, void* stream);
+
+/* param/velocity update from a gradient segment with the exact
+ * sparse_combine / _step_vector rounding (nn.py:118-131, 187-198). */
+SMB_API int smb_optimizer_step(int dtype, void* param, void* velocity, const void* grad, int64_t count,
+                       int opt_kind, double mu, double eta, void* stream);
+
+/* out[i] = sum_t dense[i, t] in numpy's pairwise order (tensor_core.row_sums,
+ * tensor_core.py:353-356). */
+SMB_API int smb_row_sums(int dtype, const void* dense, int64_t m, int64_t n, int64_t ld, void* out,
+                 void* stream);
+
+/* d_y = (softmax_columns(y) - t) / divisor   (nn.py:385-389, 411-417 and the
+ * "/ batch_size" of train.py:399).  y, t, d_y are classes x n.  If loss_out
+ * (device double[1]) is not NULL it receives softmax_ce_loss(y, t)
+ * (nn.py:397-408, summed over the batch, not divided).  exp is evaluated in
+ * double and rounded (numpy's float32 exp is not correctly rounded, so this
+ * op is tolerance-exact, not bit-exact). */
+SMB_API int smb_softmax_ce_grad(int dtype, const void* y, int64_t ld_y, const void* t, int64_t ld_t,
+                        int64_t classes, int64_t n, double divisor, void* d_y, int64_t ld_dy,
+                        double* loss_out, void* stream);
+
+/* y = max(x, 0) (nn.py:86-87) and out = d_out * (x_cached > 0) (nn.py:89-91). */
+SMB_API int smb_relu(int dtype, const void* x, int64_t ld_x, int64_t m, int64_t n, void* y, int64_t ld_y,
+             void* stream);
+SMB_API int smb_relu_backward(int dtype, const void* d_out, int64_t ld_d, const void* x_cached,
+                      int64_t ld_x, int64_t m, int64_t n, void* out, int64_t ld_out,
+                      void* stream);
+
+/* dst[f, j] = src[perm[base + j], f] for f < features, j < batch, where
+ * base = (*step_counter) * batch when step_counter != NULL, else `base`.
+ * `src` is the device-resident training set stored sample-major
+ * [n_samples x features]; dst is feature-major [features x ld_dst].
+ * Replaces the host gather Xtrain[:, batch] of sgd_train (train.py:390-396). */
+SMB_API int smb_gather_columns(int dtype, const void* src, int64_t n_samples, int64_t features,
+                       const int32_t* perm, const int32_t* step_counter, int64_t base,
+                       int64_t batch, void* dst, int64_t ld_dst, void* stream);
+
+/* *counter = (*counter + 1) % modulo  (device-side step index for CUDA-graph
+ * replays of the training step). */
+SMB_API int smb_step_counter_advance(int32_t* counter, int32_t modulo, void* stream);
+
+/* ---- initialisation ------------------------------------------------------- */
+
+/* out[p] = T(-a + 2a * u_{offset+p}) for p < count, where u_i = (x_i >> 11) * 2^-53
+ * and x_i is the (i+1)-th 64-bit output of numpy's PCG64 (XSL-RR 128/64)
+ * started at (state, inc).  Bit-identical to xavier_init
+ * (sparsity.py:223-237: rng.uniform(-a, a, size).astype(dtype)) for the
+ * Generator whose bit_generator.state is (state, inc); every thread jumps
+ * ahead independently (O(log n) LCG jump). */
+SMB_API int smb_xavier_pcg64(int dtype, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                     uint64_t inc_lo, uint64_t offset, int64_t count, double limit, void* out,
+                     void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSEMLP_B200_H */

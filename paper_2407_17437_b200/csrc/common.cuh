@@ -1,0 +1,234 @@
+// Shared helpers for the sm_100a sparse-MLP kernels: exact (separately rounded)
+// arithmetic, vector types, error plumbing for the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/sparsemlp_b200.h"
+
+namespace smb {
+
+// ---------------------------------------------------------------------------
+// error state (thread-local message, process-wide launch counter)
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+void clear_error();
+void count_launches(uint64_t n);
+
+#define SMB_REQUIRE(cond, ...)            \
+  do {                                    \
+    if (!(cond)) {                        \
+      ::smb::set_error(__VA_ARGS__);      \
+      return SMB_ERR_INVALID;             \
+    }                                     \
+  } while (0)
+
+// Check the launch that just happened; counts it for smb_launch_count().
+int check_launch(const char* what, uint64_t launches = 1);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// exact arithmetic: multiply and add rounded separately, never contracted.
+// (The library is also compiled with --fmad=false as a second guard.)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// np.maximum(y, 0): NaN propagates, -0.0 -> +0.0 (verified against numpy 2.3)
+template <typename T>
+__device__ __forceinline__ T relu_np(T y) {
+  return (y > T(0) || y != y) ? y : T(0);
+}
+
+// d * (x > 0) with numpy's bool->float promotion: d*1 or d*0 (keeps -0 / NaN)
+template <typename T>
+__device__ __forceinline__ T mask_np(T d, T x) {
+  return mul_rn(d, x > T(0) ? T(1) : T(0));
+}
+
+// 16-byte vector of T
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int N = 4;
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int N = 2;
+};
+
+template <typename T>
+struct VecOps;
+template <>
+struct VecOps<float> {
+  using V = float4;
+  __device__ __forceinline__ static float get(const V& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+  }
+  __device__ __forceinline__ static void set(V& v, int i, float x) {
+    if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
+  }
+  __device__ __forceinline__ static V zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  // acc += s * v, lane-wise, separately rounded
+  __device__ __forceinline__ static void axpy(V& acc, float s, const V& v) {
+    acc.x = add_rn(acc.x, mul_rn(s, v.x));
+    acc.y = add_rn(acc.y, mul_rn(s, v.y));
+    acc.z = add_rn(acc.z, mul_rn(s, v.z));
+    acc.w = add_rn(acc.w, mul_rn(s, v.w));
+  }
+};
+template <>
+struct VecOps<double> {
+  using V = double2;
+  __device__ __forceinline__ static double get(const V& v, int i) { return i == 0 ? v.x : v.y; }
+  __device__ __forceinline__ static void set(V& v, int i, double x) {
+    if (i == 0) v.x = x; else v.y = x;
+  }
+  __device__ __forceinline__ static V zero() { return make_double2(0.0, 0.0); }
+  __device__ __forceinline__ static void axpy(V& acc, double s, const V& v) {
+    acc.x = add_rn(acc.x, mul_rn(s, v.x));
+    acc.y = add_rn(acc.y, mul_rn(s, v.y));
+  }
+};
+
+// read-only, L1-allocating load of a 16-byte vector
+template <typename V>
+__device__ __forceinline__ V ldg_vec(const V* p) {
+  return __ldg(p);
+}
+
+__host__ __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Optimizer constants exactly as the reference forms them:
+//   sparse_combine(opt.mu, V, 1.0, G)            -> alpha = T(mu), beta = T(1)
+//   sparse_combine(1.0, W, -eta * opt.mu, V)     -> T(-eta*mu) (float64 product)
+//   sparse_combine(1.0, W, -eta, G)              -> T(-eta)
+// (nn.py:189-197, tensor_core.py:304-305; _step_vector nn.py:121-131)
+template <typename T>
+struct OptConsts {
+  int kind;
+  T mu;
+  T c_v;  // T(-eta * mu)
+  T c_g;  // T(-eta)
+};
+
+template <typename T>
+inline OptConsts<T> make_opt(int kind, double mu, double eta) {
+  OptConsts<T> o;
+  o.kind = kind;
+  o.mu = static_cast<T>(mu);
+  o.c_v = static_cast<T>(-eta * mu);
+  o.c_g = static_cast<T>(-eta);
+  return o;
+}
+
+// One element of the update, in the reference's exact operation order.
+// 1*x is exact, so fl(1*w) + fl(c*v) == add_rn(w, mul_rn(c, v)).
+template <typename T>
+__device__ __forceinline__ void apply_update(const OptConsts<T>& o, T g, T* w, T* v) {
+  if (o.kind == SMB_OPT_GD) {
+    *w = add_rn(*w, mul_rn(o.c_g, g));
+  } else if (o.kind == SMB_OPT_MOMENTUM) {
+    T vv = add_rn(mul_rn(o.mu, *v), g);
+    *v = vv;
+    *w = add_rn(*w, mul_rn(o.c_g, vv));
+  } else if (o.kind == SMB_OPT_NESTEROV) {
+    T vv = add_rn(mul_rn(o.mu, *v), g);
+    *v = vv;
+    T ww = add_rn(*w, mul_rn(o.c_v, vv));
+    *w = add_rn(ww, mul_rn(o.c_g, g));
+  }
+}
+
+// numpy's pairwise summation (loops_utils.h pairwise_sum, PW_BLOCKSIZE=128)
+// of a[0..n) with unit stride, as used by ndarray.sum(axis=-1) on contiguous
+// rows (tensor_core.row_sums).  Sequential per thread; the leaves use the
+// 8-accumulator unrolled loop.  Verified bit-identical to numpy 2.3 for
+// n in [1, 5000].
+template <typename T>
+__device__ T pairwise_leaf(const T* a, int64_t n) {
+  if (n < 8) {
+    T res = T(0);
+    for (int64_t i = 0; i < n; ++i) res = add_rn(res, a[i]);
+    return res;
+  }
+  T r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int64_t i = 8;
+  const int64_t lim = n - (n % 8);
+  for (; i < lim; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], a[i + j]);
+  }
+  T res = add_rn(add_rn(add_rn(r[0], r[1]), add_rn(r[2], r[3])),
+                 add_rn(add_rn(r[4], r[5]), add_rn(r[6], r[7])));
+  for (; i < n; ++i) res = add_rn(res, a[i]);
+  return res;
+}
+
+template <typename T>
+__device__ T pairwise_sum(const T* a, int64_t n) {
+  // explicit-stack version of:
+  //   n <= 128: leaf;  else n2 = n/2 - (n/2)%8; return ps(a, n2) + ps(a+n2, n-n2)
+  // Depth is log2(n/128) + 1 <= 40 for 64-bit n; 48 frames is plenty.
+  struct Frame {
+    int64_t off, n;
+    int state;  // 0: expand, 1: left done
+    T left;
+  };
+  Frame st[48];
+  int sp = 0;
+  st[0] = {0, n, 0, T(0)};
+  T ret = T(0);
+  while (sp >= 0) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      ret = pairwise_leaf(a + f.off, f.n);
+      --sp;
+      // propagate
+      while (sp >= 0) {
+        Frame& p = st[sp];
+        if (p.state == 0) {
+          p.left = ret;
+          p.state = 1;
+          int64_t n2 = p.n / 2;
+          n2 -= n2 % 8;
+          st[++sp] = {p.off + n2, p.n - n2, 0, T(0)};
+          break;
+        } else {
+          ret = add_rn(p.left, ret);
+          --sp;
+        }
+      }
+    } else {
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      st[sp + 1] = {f.off, n2, 0, T(0)};
+      ++sp;
+    }
+  }
+  return ret;
+}
+
+}  // namespace smb
