@@ -1,0 +1,449 @@
+"""Benchmark: sparse-MLP training throughput (samples/s) on B200.
+
+Workload (BASELINE.json configs[1], the density-sweep config, at its
+headline point): MLP 3072-1024-512-10, ReLU, softmax cross-entropy, fp32,
+Erdos-Renyi CSR sparsity at global density 0.01, Xavier init, SGD lr 0.01 with
+Nesterov momentum 0.9, batch 1024 per GPU, seeded synthetic N(0,1) data of
+50,000 x 3072 standardised features with uniform labels over 10 classes
+(SURVEY.md 8(d) stands in for CIFAR-10).  One "step" = one full training step
+(batch gather, forward, loss gradient, backward, update) of the fused,
+CUDA-graph-captured path.  Multi-GPU (torchrun): data parallel, weak scaling
+(batch 1024 per GPU, loss scaled by 1/B_global, one NCCL all-reduce of the
+flat value/bias gradient buffer per step).
+
+Our arm prints one JSON line with: value (device-resident throughput, per-step
+CUDA events on the launching stream, L2 flushed before every timed step, max
+over ranks), e2e (the public FusedTrainStep.train_batch API fed from pinned
+host buffers, H2D + step + D2H of the loss inside the timed region), roofline
+(dominant kernel, algorithmic bytes / CUDA-event duration vs the measured HBM
+peak), cpu_baseline (the oracle port timed on this host's cores), clocks and
+gpu_launches.  `--impl reference` times the reference algorithm's CPU
+implementation (the C/numpy oracle port, all host threads) on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "sparse-MLP train samples/sec vs density; SpMM/SDDMM GB/s vs B200 HBM peak"
+UNIT = "samples/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", default="3072,1024,512,10")
+    ap.add_argument("--density", type=float, default=0.01)
+    ap.add_argument("--batch", type=int, default=1024, help="per-GPU batch")
+    ap.add_argument("--samples", type=int, default=50_000)
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="budget of the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also report the config-2 density sweep (B=100 and 1024)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes per kernel launch (SURVEY.md 8(d), 4-byte words)
+# ---------------------------------------------------------------------------
+def kernel_bytes(kind: str, m: int, k: int, z: int, B: int, mask: bool = True) -> int:
+    if kind == "spmm":          # fwd SpMM + bias + ReLU
+        return 4 * (m + 1) + 8 * z + 4 * k * B + 4 * m + 4 * m * B
+    if kind == "spmm_t":        # transposed SpMM (+ ReLU mask of the layer below)
+        return 4 * (k + 1) + 8 * z + 4 * m * B + (4 * k * B if mask else 0) + 4 * k * B
+    if kind == "sddmm_update":  # SDDMM + Nesterov update of values/velocity
+        return 4 * (m + 1) + 4 * z + 4 * m * B + 4 * k * B + 16 * z
+    raise ValueError(kind)
+
+
+def measured_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def config_dict(args, ws):
+    return {"workload": f"configs[1] point: MLP {args.layers.replace(',', '-')} ER d={args.density} "
+                        f"B={args.batch}/GPU fp32 Nesterov lr={args.lr}",
+            "layers": [int(x) for x in args.layers.split(",")], "density": args.density,
+            "batch_per_gpu": args.batch, "global_batch": args.batch * ws,
+            "train_samples": args.samples, "parallelism": f"dp{ws}",
+            "l2": "flushed (512 MB write) before every timed step; dataset 614 MB > L2"}
+
+
+def cpu_step_sample(args, global_batch, budget_s, min_steps=3, max_steps=200):
+    """Time the oracle port's training step (C kernels on all host threads +
+    numpy glue) on a bounded sample; returns (samples/s, steps, threads)."""
+    from oracle import oracle as O
+
+    O.build()
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    chain = [int(x) for x in args.layers.split(",")]
+    ref = O.OracleMLP.build(chain, args.density, seed=args.seed)
+    rng = np.random.default_rng(args.seed + 17)
+    x = rng.standard_normal((chain[0], global_batch), dtype=np.float32)
+    lab = rng.integers(0, chain[-1], global_batch)
+    t = np.zeros((chain[-1], global_batch), np.float32)
+    t[lab, np.arange(global_batch)] = 1
+    ref.step(x, t, args.lr)  # warm (thread pool, page faults)
+    steps, t0 = 0, time.perf_counter()
+    while steps < max_steps and (steps < min_steps or time.perf_counter() - t0 < budget_s):
+        ref.step(x, t, args.lr)
+        steps += 1
+    dt = time.perf_counter() - t0
+    return global_batch * steps / dt, steps, threads, dt
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    gb = args.batch * ws
+    # warmup + K timed steps of the CPU implementation, each one full step
+    from oracle import oracle as O
+
+    O.build()
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    chain = [int(x) for x in args.layers.split(",")]
+    ref = O.OracleMLP.build(chain, args.density, seed=args.seed)
+    rng = np.random.default_rng(args.seed + 17)
+    x = rng.standard_normal((chain[0], gb), dtype=np.float32)
+    lab = rng.integers(0, chain[-1], gb)
+    t = np.zeros((chain[-1], gb), np.float32)
+    t[lab, np.arange(gb)] = 1
+    for _ in range(args.warmup):
+        ref.step(x, t, args.lr)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref.step(x, t, args.lr)
+    dt = time.perf_counter() - t0
+    value = gb * args.steps / dt
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_dict(args, ws),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} timed training steps at global batch {gb} "
+                                   f"(oracle/: C kernels on {threads} pthreads + numpy glue)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    import paper_2407_17437_b200 as smb
+    from paper_2407_17437_b200 import _lib
+    from paper_2407_17437_b200.engine import KernelTimer
+
+    chain = [int(x) for x in args.layers.split(",")]
+    B, gb = args.batch, args.batch * ws
+    cfg = smb.ExperimentConfig(layer_dims=chain, density=args.density, batch_size=B, lr=args.lr,
+                               seed=args.seed)
+    model, plan = smb.build_model(cfg)
+    data = smb.synthetic_dataset(seed=args.seed, n_samples=args.samples, features=chain[0],
+                                 classes=chain[-1])
+    ddata = smb.DeviceDataset(data)
+    step = smb.FusedTrainStep(model, B, global_batch=gb, process_group=pg)
+    step.attach_dataset(ddata)
+    perm = np.random.default_rng(args.seed).permutation(args.samples)
+    step.set_epoch(perm, rank_offset=rank * B)
+    eta = args.lr
+    dev = torch.device("cuda", local)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if pg is not None:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if pg is None:
+            return v
+        import torch.distributed as dist
+
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (graph capture on the first steps) ----
+    for _ in range(max(3, args.warmup)):
+        step.step(eta)
+    barrier()
+
+    # ---- launches per step (our kernels) from one eager step ----
+    step.use_graph = False
+    c0 = _lib.launch_count()
+    step.step(eta)
+    launches_per_step = _lib.launch_count() - c0
+    step.use_graph = True
+    barrier()
+
+    # ---- timed region: K steps, L2 flushed before each, per-step events ----
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            starts[i].record()
+            step.step(eta)
+            ends[i].record()
+        barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = max_over_ranks(float(np.sum(step_ms)))
+    value = gb * args.steps / (total_ms / 1e3)
+
+    # back-to-back graph replays (no flush) for context
+    barrier()
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s_ev.record()
+    for _ in range(args.steps):
+        step.step(eta)
+    e_ev.record()
+    barrier()
+    b2b_ms = max_over_ranks(s_ev.elapsed_time(e_ev))
+
+    # ---- per-kernel spans (eager, GPU held while the step is enqueued) ----
+    timer = KernelTimer()
+    step.timer, step.use_graph = timer, False
+    nk = min(10, args.steps)
+    for i in range(nk):
+        flush.fill_(float(i))
+        KernelTimer.hold_gpu()
+        step.step(eta)
+    summ = timer.summary()
+    step.timer, step.use_graph = None, True
+    units = step.units
+    best = None
+    kernels = {}
+    for tag, (cnt, ms) in summ.items():
+        kernels[tag] = round(1e3 * ms / cnt, 2)
+        name, _, idx = tag.partition("[")
+        if name not in ("spmm", "spmm_t", "sddmm_update") or not idx:
+            continue
+        u = units[int(idx.rstrip("]"))]
+        if not u.sparse:
+            continue
+        mask = name == "spmm_t" and units[int(idx.rstrip("]")) - 1].relu
+        b = kernel_bytes(name, u.m, u.k, u.nvals, B, mask)
+        us = 1e3 * ms / cnt
+        if best is None or us > best[2]:
+            best = (tag, b, us, u)
+    hbm, peak_src = measured_peaks()
+    roofline = None
+    if best:
+        tag, b, us, u = best
+        ach = b / (us * 1e-6) / 1e9
+        traffic = None
+        prof = REPO / "profiles" / "ncu_traffic.json"
+        if prof.exists():
+            try:
+                traffic = json.loads(prof.read_text()).get(
+                    f"{args.layers}|{args.density}|{B}|{tag}")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach / hbm, 4), "traffic": traffic, "kernel": tag,
+                    "kernel_us": round(us, 2), "algorithmic_bytes": b,
+                    "peak_source": peak_src,
+                    "pairs_per_s": round(u.nvals * B / (us * 1e-6), 1)}
+
+    # ---- end to end through the public API: pinned host batches ----
+    R = 4
+    rng = np.random.default_rng(args.seed + 1)
+    xs, ts = [], []
+    for r in range(R):
+        cols = perm[(r * gb + rank * B):(r * gb + rank * B + B)]
+        xs.append(torch.from_numpy(np.ascontiguousarray(data.Xtrain[:, cols])).pin_memory())
+        ts.append(torch.from_numpy(np.ascontiguousarray(data.Ttrain[:, cols])).pin_memory())
+    loss_host = torch.empty(1, dtype=torch.float64).pin_memory()
+    for r in range(2):
+        step.train_batch(xs[r], ts[r], eta, loss_host)
+    barrier()
+    s_ev.record()
+    for i in range(args.steps):
+        step.train_batch(xs[i % R], ts[i % R], eta, loss_host)
+    e_ev.record()
+    barrier()
+    e2e_ms = max_over_ranks(s_ev.elapsed_time(e_ev))
+    e2e = {"value": gb * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(xs[0].numel() * 4 + ts[0].numel() * 4),
+           "d2h_bytes_per_step": 8, "per": "rank", "api": "FusedTrainStep.train_batch"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(args, ws), "e2e": e2e, "roofline": roofline,
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clk.summary(),
+        "back_to_back": {"value": gb * args.steps / (b2b_ms / 1e3), "unit": UNIT,
+                         "note": "graph replays without L2 flush"},
+        "kernel_us": kernels,
+        "plan_nnz": plan.layer_nnz,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        sps, nsteps, threads, dt = cpu_step_sample(args, gb, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": sps, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{nsteps} training steps at batch {gb} "
+                                          f"({dt:.1f} s, oracle/ C kernels + numpy glue)"}
+    if args.sweep and ws == 1:
+        line["sweep"] = density_sweep(args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def density_sweep(args, steps=20):
+    """Config-2 sweep: samples/s (back-to-back graph replays, L2 flushed
+    before each step) for every density at B=100 and B=1024."""
+    import torch
+
+    import paper_2407_17437_b200 as smb
+
+    chain = [int(x) for x in args.layers.split(",")]
+    data = smb.synthetic_dataset(seed=args.seed, n_samples=20_480, features=chain[0],
+                                 classes=chain[-1])
+    ddata = smb.DeviceDataset(data)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    out = []
+    for B in (100, 1024):
+        for d in (0.001, 0.005, 0.01, 0.05, 0.1, 0.2, 0.5):
+            model, plan = smb.build_model(smb.ExperimentConfig(
+                layer_dims=chain, density=d, batch_size=B, lr=args.lr, seed=args.seed))
+            st = smb.FusedTrainStep(model, B)
+            st.attach_dataset(ddata)
+            st.set_epoch(np.random.default_rng(0).permutation(20_480))
+            for _ in range(3):
+                st.step(args.lr)
+            tot = 0.0
+            for i in range(steps):
+                flush.fill_(float(i))
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                st.step(args.lr)
+                e.record()
+                e.synchronize()
+                tot += s.elapsed_time(e)
+            out.append({"density": d, "batch": B, "nnz": sum(plan.layer_nnz),
+                        "ms_per_step": round(tot / steps, 4),
+                        "samples_per_s": round(B * steps / (tot / 1e3), 1)})
+    return out
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

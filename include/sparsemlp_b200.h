@@ -123,6 +123,18 @@ SMB_API int smb_spmm_t(int dtype, const smb_pattern* pattern, const void* values
                int64_t ld_dense, int64_t n, const void* mask, int64_t ld_mask, void* out,
                int64_t ld_out, void* stream);
 
+/* smb_spmm_t plus the bias side of the layer BELOW, fused into the epilogue:
+ * grad_bias[c] = row_sums(out[c, :]) in numpy's pairwise order (nn.py:184,
+ * tensor_core.py:353-356) and the optimizer update of bias / velocity_bias
+ * (_step_vector, nn.py:118-131) -- out is that layer's output gradient
+ * d_out, so this is the exact bias arithmetic of its backward + optimize.
+ * opt_kind == SMB_OPT_NONE only writes grad_bias_out (data-parallel path). */
+SMB_API int smb_spmm_t_bias(int dtype, const smb_pattern* pattern, const void* values,
+                            const void* dense, int64_t ld_dense, int64_t n, const void* mask,
+                            int64_t ld_mask, void* out, int64_t ld_out, void* bias,
+                            void* velocity_bias, void* grad_bias_out, int opt_kind, double mu,
+                            double eta, void* stream);
+
 /* out_values[p] = a[i,0]*b[j,0] + a[i,1]*b[j,1] + ... (sequential over the
  * n columns) for the p-th stored (i, j).  n == 0 gives zeros.
  * Replaces _kernels.sddmm_kernel (_kernels.py:62-75) via tensor_core.sddmm
@@ -155,6 +167,13 @@ SMB_API int smb_sddmm_update(int dtype, const smb_pattern* pattern, const void* 
                      void* grad_out, void* bias, void* velocity_bias, void* grad_bias_out,
                      int opt_kind, double mu, double eta, void* stream);
 
+/* grad_bias = row_sums(d_out) (numpy pairwise order) and the bias optimizer
+ * update; one warp per row (nn.py:184, 118-131).  Dense layers and any
+ * layer whose output gradient was not produced by smb_spmm_t_bias. */
+SMB_API int smb_bias_grad_update(int dtype, const void* d_out, int64_t ld, int64_t m, int64_t n,
+                                 void* bias, void* velocity_bias, void* grad_bias_out,
+                                 int opt_kind, double mu, double eta, void* stream);
+
 /* param/velocity update from a gradient segment with the exact
  * sparse_combine / _step_vector rounding (nn.py:118-131, 187-198). */
 SMB_API int smb_optimizer_step(int dtype, void* param, void* velocity, const void* grad, int64_t count,
@@ -174,6 +193,22 @@ SMB_API int smb_row_sums(int dtype, const void* dense, int64_t m, int64_t n, int
 SMB_API int smb_softmax_ce_grad(int dtype, const void* y, int64_t ld_y, const void* t, int64_t ld_t,
                         int64_t classes, int64_t n, double divisor, void* d_y, int64_t ld_dy,
                         double* loss_out, void* stream);
+
+/* The loss step of the fused training step: smb_softmax_ce_grad over
+ * ceil(n/256) CTAs, whose last CTA additionally (a) reduces the batch loss in
+ * a fixed order into loss_out, (b) applies the last layer's bias side
+ * (row sums of d_y + update, as smb_bias_grad_update) and (c) advances
+ * *step_counter modulo `modulo` (CUDA-graph replays of the step).  Any of
+ * loss_out / bias / grad_bias_out / step_counter may be NULL.  `workspace`
+ * (device, smb_softmax_ce_workspace_bytes(n) bytes, zeroed once before first
+ * use) holds the CTA ticket and the per-CTA loss partials. */
+SMB_API size_t smb_softmax_ce_workspace_bytes(int64_t n);
+SMB_API int smb_softmax_ce_step(int dtype, const void* y, int64_t ld_y, const void* t,
+                                int64_t ld_t, int64_t classes, int64_t n, double divisor,
+                                void* d_y, int64_t ld_dy, double* loss_out, void* bias,
+                                void* velocity_bias, void* grad_bias_out, int opt_kind, double mu,
+                                double eta, int32_t* step_counter, int32_t modulo,
+                                void* workspace, void* stream);
 
 /* y = max(x, 0) (nn.py:86-87) and out = d_out * (x_cached > 0) (nn.py:89-91). */
 SMB_API int smb_relu(int dtype, const void* x, int64_t ld_x, int64_t m, int64_t n, void* y, int64_t ld_y,

@@ -158,6 +158,7 @@ def er_plan(chain, density):
     """(densities, nnz) of the ER solve with round-half-even + drift fix."""
     pairs = list(zip(chain[:-1], chain[1:]))
     sizes = [a * b for a, b in pairs]
+    ratio = [(a + b) / (a * b) for a, b in pairs]  # sparsity.py:127
     target = density * sum(sizes)
     sat = [False] * len(pairs)
     dens = [0.0] * len(pairs)
@@ -166,14 +167,14 @@ def er_plan(chain, density):
         if denom == 0:
             break
         eps = (target - sum(sz for sz, s in zip(sizes, sat) if s)) / denom
-        new = [i for i, (a, b) in enumerate(pairs) if not sat[i] and eps * (a + b) / (a * b) >= 1.0]
+        new = [i for i in range(len(pairs)) if not sat[i] and eps * ratio[i] >= 1.0]
         for i in new:
             sat[i], dens[i] = True, 1.0
         if new:
             continue
-        for i, (a, b) in enumerate(pairs):
+        for i in range(len(pairs)):
             if not sat[i]:
-                dens[i] = eps * (a + b) / (a * b)
+                dens[i] = eps * ratio[i]
         break
     nnz = [sz if s else int(round(d * sz)) for d, sz, s in zip(dens, sizes, sat)]
     drift = int(round(target)) - sum(nnz)

@@ -45,6 +45,17 @@ SIGNATURES = {
         _i32,
         [_i32, _p, _p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _i32, _f64, _f64, _p],
     ),
+    "smb_spmm_t_bias": (
+        _i32,
+        [_i32, _p, _p, _p, _i64, _i64, _p, _i64, _p, _i64, _p, _p, _p, _i32, _f64, _f64, _p],
+    ),
+    "smb_bias_grad_update": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p, _p, _i32, _f64, _f64, _p]),
+    "smb_softmax_ce_workspace_bytes": (C.c_size_t, [_i64]),
+    "smb_softmax_ce_step": (
+        _i32,
+        [_i32, _p, _i64, _p, _i64, _i64, _i64, _f64, _p, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
+         _p, _i32, _p, _p],
+    ),
     "smb_optimizer_step": (_i32, [_i32, _p, _p, _p, _i64, _i32, _f64, _f64, _p]),
     "smb_row_sums": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p]),
     "smb_softmax_ce_grad": (

@@ -1,4 +1,8 @@
 // C-ABI plumbing: thread-local error messages, launch accounting, version.
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace smb {
@@ -17,6 +21,16 @@ void set_error(const char* fmt, ...) {
 void clear_error() { g_err[0] = 0; }
 
 void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void ensure_dynamic_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : done)
+    if (e.first == kernel && e.second >= bytes) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  done.emplace_back(kernel, bytes);
+}
 
 int check_launch(const char* what, uint64_t launches) {
   const cudaError_t e = cudaGetLastError();

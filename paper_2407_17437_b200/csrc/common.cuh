@@ -33,6 +33,14 @@ int check_launch(const char* what, uint64_t launches = 1);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Opt a kernel into `bytes` of dynamic shared memory, once per kernel per
+// process (device-wide attribute; cheap registry keyed by the entry point).
+void ensure_dynamic_smem(const void* kernel, size_t bytes);
+template <typename K>
+inline void ensure_smem(K* kernel, size_t bytes) {
+  ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 // ---------------------------------------------------------------------------
 // exact arithmetic: multiply and add rounded separately, never contracted.
 // (The library is also compiled with --fmad=false as a second guard.)
@@ -106,9 +114,14 @@ struct VecOps<double> {
   }
 };
 
-// read-only, L1-allocating load of a 16-byte vector
+// Gather loads through the read-only path (L1-allocating: measured 1.5x
+// faster on B200 than ld.global.nc.L1::no_allocate for the SpMM gathers).
 template <typename V>
 __device__ __forceinline__ V ldg_vec(const V* p) {
+  return __ldg(p);
+}
+template <typename T>
+__device__ __forceinline__ T ldg_stream(const T* p) {
   return __ldg(p);
 }
 
@@ -228,6 +241,123 @@ __device__ T pairwise_sum(const T* a, int64_t n) {
       ++sp;
     }
   }
+  return ret;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative numpy pairwise sum (same tree, same roundings as
+// pairwise_sum above).  The leaves of the split tree are computed 4 at a time
+// by 8-lane groups (lane j of a group owns accumulator r[j]); lane 0 then
+// combines the leaf values in the recursion order.  `leaf_buf` is per-warp
+// scratch (shared memory) of at least warp_pairwise_leaves(n) elements.  All
+// 32 lanes must call; the result is returned on every lane.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int warp_pairwise_leaves(int n) { return n / 64 + 2; }
+
+template <typename T>
+__device__ T warp_pairwise_sum(const T* a, int n, T* leaf_buf) {
+  const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
+  if (n <= 0) return T(0);
+  int st_off[32], st_len[32];
+  int sp = 0, leaf = 0;
+  int cur_off = 0, cur_len = n;
+  bool done = false;
+  while (!done) {
+    // gather up to 4 leaves in DFS (left-to-right) order
+    int b_off[4] = {0, 0, 0, 0}, b_len[4] = {0, 0, 0, 0};
+    int nb = 0;
+    while (nb < 4 && !done) {
+      while (cur_len > 128) {
+        int n2 = cur_len / 2;
+        n2 -= n2 % 8;
+        st_off[sp] = cur_off + n2;
+        st_len[sp] = cur_len - n2;
+        ++sp;
+        cur_len = n2;
+      }
+      b_off[nb] = cur_off;
+      b_len[nb] = cur_len;
+      ++nb;
+      if (sp == 0) {
+        done = true;
+      } else {
+        --sp;
+        cur_off = st_off[sp];
+        cur_len = st_len[sp];
+      }
+    }
+    const int off = grp == 0 ? b_off[0] : grp == 1 ? b_off[1] : grp == 2 ? b_off[2] : b_off[3];
+    const int len = grp < nb ? (grp == 0 ? b_len[0] : grp == 1 ? b_len[1] : grp == 2 ? b_len[2] : b_len[3]) : 0;
+    const T* p = a + off;
+    const int lim = len - (len % 8);
+    // the whole leaf (<= 128 elements, <= 16 per lane) is loaded up front so
+    // a batch of 4 leaves costs one memory round trip, then summed in order
+    T v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = (8 * k + j < lim) ? p[8 * k + j] : T(0);
+    T tail[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const int i = (len >= 8 ? lim : 0) + k;
+      tail[k] = (j == 0 && i < len) ? p[i] : T(0);
+    }
+    T r = v[0];
+#pragma unroll
+    for (int k = 1; k < 16; ++k)
+      if (8 * k < lim) r = add_rn(r, v[k]);
+    T t = __shfl_down_sync(0xffffffffu, r, 1);
+    if ((j & 1) == 0) r = add_rn(r, t);
+    t = __shfl_down_sync(0xffffffffu, r, 2);
+    if ((j & 3) == 0) r = add_rn(r, t);
+    t = __shfl_down_sync(0xffffffffu, r, 4);
+    if (j == 0 && grp < nb) {
+      T res;
+      const int rest = len >= 8 ? len - lim : len;
+      res = len >= 8 ? add_rn(r, t) : T(0);
+#pragma unroll
+      for (int k = 0; k < 7; ++k)
+        if (k < rest) res = add_rn(res, tail[k]);
+      if (n <= 128) leaf_buf[0] = res; else leaf_buf[leaf + grp] = res;
+    }
+    leaf += nb;
+  }
+  __syncwarp();
+  T ret = leaf_buf[0];
+  if (n > 128 && lane == 0) {
+    // combine in recursion order: value(node) = value(left) + value(right)
+    int st_n[32], st_state[32];
+    T st_left[32];
+    int k = 0, idx = 0, cur = n;
+    for (;;) {
+      while (cur > 128) {
+        st_n[k] = cur;
+        st_state[k] = 0;
+        ++k;
+        int n2 = cur / 2;
+        n2 -= n2 % 8;
+        cur = n2;
+      }
+      ret = leaf_buf[idx++];
+      bool next = false;
+      while (!next) {
+        if (k == 0) break;
+        if (st_state[k - 1] == 0) {
+          st_left[k - 1] = ret;
+          st_state[k - 1] = 1;
+          int n2 = st_n[k - 1] / 2;
+          n2 -= n2 % 8;
+          cur = st_n[k - 1] - n2;
+          next = true;
+        } else {
+          ret = add_rn(st_left[k - 1], ret);
+          --k;
+        }
+      }
+      if (!next) break;
+    }
+  }
+  ret = __shfl_sync(0xffffffffu, ret, 0);
+  __syncwarp();
   return ret;
 }
 

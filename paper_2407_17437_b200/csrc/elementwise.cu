@@ -1,7 +1,7 @@
 // Memory-bound glue of the training step: sparse_combine (axpby), the
-// optimizer update of flat segments, numpy-order row sums, softmax
-// cross-entropy gradient, ReLU forward/backward, the device batch gather and
-// the CUDA-graph step counter.
+// optimizer update of flat segments, numpy-order row sums (+ bias update),
+// the softmax cross-entropy step, ReLU forward/backward and the device batch
+// gather.
 #include "common.cuh"
 
 namespace smb {
@@ -34,55 +34,112 @@ __global__ void optimizer_kernel(T* __restrict__ w, T* __restrict__ v, const T* 
   }
 }
 
-// ---- numpy pairwise row sums (tensor_core.py:353-356) ----------------------
+// ---- warp per row: pairwise row sum (tensor_core.py:353-356) and the bias
+// optimizer update (_step_vector, nn.py:118-131) --------------------------
+constexpr int kRowWarps = 8;
+constexpr int kWarpLeafCap = 260;  // warp_pairwise_leaves(n) for n <= 16384
+
 template <typename T>
-__global__ void row_sums_kernel(const T* __restrict__ a, int64_t m, int64_t n, int64_t ld,
-                                T* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) out[i] = pairwise_sum(a + i * ld, n);
+__global__ void __launch_bounds__(kRowWarps * 32)
+    bias_rows_kernel(const T* __restrict__ d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias,
+                     T* grad, OptConsts<T> opt) {
+  __shared__ T leaf[kRowWarps][kWarpLeafCap];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + warp;
+  if (row >= m) return;
+  T g;
+  if (n <= 16384) {
+    g = warp_pairwise_sum(d + row * ld, (int)n, leaf[warp]);
+  } else {
+    g = pairwise_sum(d + row * ld, n);  // sequential fallback for very wide batches
+  }
+  if (lane != 0) return;
+  if (grad) grad[row] = g;
+  if (opt.kind != SMB_OPT_NONE && bias) {
+    T dummy = T(0);
+    apply_update(opt, g, bias + row, vbias ? vbias + row : &dummy);
+  }
 }
 
-// ---- softmax cross-entropy gradient (nn.py:385-417, train.py:399) ---------
-// One thread per sample column; a single CTA so the optional batch loss is
-// reduced in a fixed order.
+// ---- softmax cross-entropy step (nn.py:385-417, train.py:399) -------------
+// One thread per sample column: z = y - max, e = exp(z) (double, rounded),
+// s = sum_c e (sequential, numpy's axis-0 order), d = (e/s - t) / divisor.
+// The per-column loss log(s) - sum_c z*t is reduced per CTA in a fixed tree
+// and across CTAs by the last CTA to finish (ticket), which then also runs
+// the last layer's bias row sums / update and advances the step counter.
 template <typename T>
-__global__ void softmax_ce_kernel(const T* __restrict__ y, int64_t ld_y, const T* __restrict__ t,
-                                  int64_t ld_t, int64_t classes, int64_t n, T divisor,
-                                  T* __restrict__ dy, int64_t ld_dy, double* loss_out) {
-  __shared__ double part[1024];
+__global__ void __launch_bounds__(256)
+    softmax_step_kernel(const T* __restrict__ y, int64_t ld_y, const T* __restrict__ t,
+                        int64_t ld_t, int64_t classes, int64_t n, T divisor, T* dy, int64_t ld_dy,
+                        double* loss_out, double* loss_parts, unsigned* ticket, T* bias, T* vbias,
+                        T* grad_bias, OptConsts<T> opt, int32_t* counter, int32_t modulo) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double s_warp[8];
+  __shared__ bool s_last;
   double local = 0.0;
   for (int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; col < n;
        col += (int64_t)gridDim.x * blockDim.x) {
-    // z = y - y.max(axis=0)
     T mx = y[col];
     for (int64_t c = 1; c < classes; ++c) {
       const T v = y[c * ld_y + col];
       mx = (v > mx || v != v) ? v : mx;
     }
-    // e.sum(axis=0): sequential over classes (numpy axis-0 reduce order)
     T s = T(0);
     double zt = 0.0;
     for (int64_t c = 0; c < classes; ++c) {
       const T z = sub_rn(y[c * ld_y + col], mx);
       const T e = static_cast<T>(exp(static_cast<double>(z)));
+      dy[c * ld_dy + col] = e;
       s = add_rn(s, e);
       zt += static_cast<double>(z) * static_cast<double>(t[c * ld_t + col]);
     }
     for (int64_t c = 0; c < classes; ++c) {
-      const T z = sub_rn(y[c * ld_y + col], mx);
-      const T e = static_cast<T>(exp(static_cast<double>(z)));
-      const T pr = div_rn(e, s);
+      const T pr = div_rn(dy[c * ld_dy + col], s);
       dy[c * ld_dy + col] = div_rn(sub_rn(pr, t[c * ld_t + col]), divisor);
     }
     local += log(static_cast<double>(s)) - zt;
   }
-  if (loss_out == nullptr) return;
-  part[threadIdx.x] = local;
+  // fixed-order block reduction of the loss
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+  if (lane == 0) s_warp[warp] = local;
   __syncthreads();
   if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b += s_warp[w];
+    if (gridDim.x == 1) {
+      s_last = true;
+      if (loss_out) *loss_out = b;
+    } else {
+      loss_parts[blockIdx.x] = b;
+      __threadfence();
+      s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0 && gridDim.x > 1) {
     double tot = 0.0;
-    for (int i = 0; i < (int)blockDim.x; ++i) tot += part[i];
-    *loss_out = tot;
+    for (unsigned b = 0; b < gridDim.x; ++b) tot += loss_parts[b];
+    if (loss_out) *loss_out = tot;
+    *ticket = 0u;  // ready for the next launch / graph replay
+  }
+  if (counter && threadIdx.x == 0) {
+    const int32_t v = *counter + 1;
+    *counter = (modulo > 0 && v >= modulo) ? 0 : v;
+  }
+  if (grad_bias == nullptr && !(opt.kind != SMB_OPT_NONE && bias)) return;
+  T* leaf = reinterpret_cast<T*>(smem_raw) + warp * warp_pairwise_leaves((int)n);
+  for (int64_t c = warp; c < classes; c += (blockDim.x >> 5)) {
+    const T g = warp_pairwise_sum(dy + c * ld_dy, (int)n, leaf);
+    if (lane == 0) {
+      if (grad_bias) grad_bias[c] = g;
+      if (opt.kind != SMB_OPT_NONE && bias) {
+        T dummy = T(0);
+        apply_update(opt, g, bias + c, vbias ? vbias + c : &dummy);
+      }
+    }
   }
 }
 
@@ -109,40 +166,57 @@ __global__ void relu_backward_kernel(const T* __restrict__ d, int64_t ld_d,
 }
 
 // ---- device batch gather (train.py:390-396) ----------------------------------
-// dst[f, j] = src[perm[base + j], f]: 32 samples x 32 features per tile,
-// coalesced on both sides through a padded shared-memory transpose.
-template <typename T>
-__global__ void gather_columns_kernel(const T* __restrict__ src, int64_t features,
-                                      const int32_t* __restrict__ perm,
-                                      const int32_t* __restrict__ step_counter, int64_t base,
-                                      int64_t batch, T* __restrict__ dst, int64_t ld_dst) {
-  __shared__ T tile[32][33];
+// dst[f, j] = src[perm[base + j], f]: a CTA moves 32 samples x 128 features,
+// reading whole 512-byte sample segments (16-byte vectors) and writing
+// 128-byte batch rows, transposing through padded shared memory.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256)
+    gather_columns_kernel(const T* __restrict__ src, int64_t features,
+                          const int32_t* __restrict__ perm, const int32_t* __restrict__ step_counter,
+                          int64_t base, int64_t batch, T* __restrict__ dst, int64_t ld_dst) {
+  constexpr int FT = 128;  // features per tile
+  __shared__ T tile[32][FT + 1];
   __shared__ int32_t s_idx[32];
   const int64_t b0 = step_counter ? (int64_t)(*step_counter) * batch : base;
   const int64_t j0 = (int64_t)blockIdx.x * 32;
-  const int64_t f0 = (int64_t)blockIdx.y * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const int64_t f0 = (int64_t)blockIdx.y * FT;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   if (ty == 0) s_idx[tx] = (j0 + tx < batch) ? perm[b0 + j0 + tx] : -1;
   __syncthreads();
+  if (VEC) {
+    constexpr int VW = 16 / sizeof(T);
+    using V = typename Vec16<T>::type;
+    // each sample row segment: FT/VW vectors; 256 threads cover 32 rows
+    for (int e = threadIdx.x; e < 32 * (FT / VW); e += 256) {
+      const int r = e / (FT / VW), v = e % (FT / VW);
+      const int32_t sidx = s_idx[r];
+      const int64_t f = f0 + (int64_t)v * VW;
+      if (sidx < 0 || f >= features) continue;
+      const T* p = src + (int64_t)sidx * features + f;
+      if (f + VW <= features) {
+        const V x = __ldg(reinterpret_cast<const V*>(p));
 #pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    const int32_t sidx = s_idx[r];
-    if (sidx >= 0 && f0 + tx < features) tile[r][tx] = src[(int64_t)sidx * features + f0 + tx];
+        for (int j = 0; j < VW; ++j) tile[r][v * VW + j] = VecOps<T>::get(x, j);
+      } else {
+        for (int j = 0; f + j < features; ++j) tile[r][v * VW + j] = p[j];
+      }
+    }
+  } else {
+    for (int r = ty; r < 32; r += 8) {
+      const int32_t sidx = s_idx[r];
+      if (sidx < 0) continue;
+      for (int c = tx; c < FT && f0 + c < features; c += 32)
+        tile[r][c] = src[(int64_t)sidx * features + f0 + c];
+    }
   }
   __syncthreads();
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    if (f0 + r < features && j0 + tx < batch) dst[(f0 + r) * ld_dst + j0 + tx] = tile[tx][r];
-  }
+  if (j0 + tx >= batch) return;
+  for (int c = ty; c < FT && f0 + c < features; c += 8)
+    dst[(f0 + c) * ld_dst + j0 + tx] = tile[tx][c];
 }
 
-__global__ void step_counter_kernel(int32_t* counter, int32_t modulo) {
-  const int32_t v = *counter + 1;
-  *counter = (modulo > 0 && v >= modulo) ? 0 : v;
-}
-
-template <typename T>
-int dispatch_dtype(int dtype, const char* name, T&& fn) {
+template <typename F>
+int dispatch_dtype(int dtype, const char* name, F&& fn) {
   if (dtype == SMB_F32) return fn(float{});
   if (dtype == SMB_F64) return fn(double{});
   set_error("%s: unsupported dtype %d", name, dtype);
@@ -150,6 +224,20 @@ int dispatch_dtype(int dtype, const char* name, T&& fn) {
 }
 
 }  // namespace
+
+template <typename T>
+int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias, T* grad,
+                     const OptConsts<T>& opt, cudaStream_t st) {
+  if (m == 0) return SMB_OK;
+  bias_rows_kernel<T><<<(unsigned)ceil_div(m, kRowWarps), kRowWarps * 32, 0, st>>>(
+      d, ld, m, n, bias, vbias, grad, opt);
+  return check_launch("bias_rows");
+}
+template int launch_bias_rows<float>(const float*, int64_t, int64_t, int64_t, float*, float*,
+                                     float*, const OptConsts<float>&, cudaStream_t);
+template int launch_bias_rows<double>(const double*, int64_t, int64_t, int64_t, double*, double*,
+                                      double*, const OptConsts<double>&, cudaStream_t);
+
 }  // namespace smb
 
 using namespace smb;
@@ -192,12 +280,64 @@ extern "C" int smb_row_sums(int dtype, const void* dense, int64_t m, int64_t n, 
                             void* out, void* stream) {
   clear_error();
   SMB_REQUIRE(m >= 0 && n >= 0 && ld >= n, "smb_row_sums: bad shape");
-  if (m == 0) return SMB_OK;
+  SMB_REQUIRE(m == 0 || out != nullptr, "smb_row_sums: null output");
   return dispatch_dtype(dtype, "smb_row_sums", [&](auto tag) {
     using T = decltype(tag);
-    row_sums_kernel<T><<<(unsigned)ceil_div(m, 128), 128, 0, as_stream(stream)>>>(
-        static_cast<const T*>(dense), m, n, ld, static_cast<T*>(out));
-    return check_launch("smb_row_sums");
+    return launch_bias_rows<T>(static_cast<const T*>(dense), ld, m, n, nullptr, nullptr,
+                               static_cast<T*>(out), make_opt<T>(SMB_OPT_NONE, 0, 0),
+                               as_stream(stream));
+  });
+}
+
+extern "C" int smb_bias_grad_update(int dtype, const void* d_out, int64_t ld, int64_t m,
+                                    int64_t n, void* bias, void* velocity_bias,
+                                    void* grad_bias_out, int opt_kind, double mu, double eta,
+                                    void* stream) {
+  clear_error();
+  SMB_REQUIRE(m >= 0 && n >= 0 && ld >= n, "smb_bias_grad_update: bad shape");
+  SMB_REQUIRE(opt_kind >= SMB_OPT_NONE && opt_kind <= SMB_OPT_NESTEROV,
+              "smb_bias_grad_update: bad optimizer kind %d", opt_kind);
+  SMB_REQUIRE(!(opt_kind == SMB_OPT_MOMENTUM || opt_kind == SMB_OPT_NESTEROV) || bias == nullptr ||
+                  velocity_bias != nullptr,
+              "smb_bias_grad_update: momentum needs a bias velocity buffer");
+  return dispatch_dtype(dtype, "smb_bias_grad_update", [&](auto tag) {
+    using T = decltype(tag);
+    return launch_bias_rows<T>(static_cast<const T*>(d_out), ld, m, n, static_cast<T*>(bias),
+                               static_cast<T*>(velocity_bias), static_cast<T*>(grad_bias_out),
+                               make_opt<T>(opt_kind, mu, eta), as_stream(stream));
+  });
+}
+
+extern "C" size_t smb_softmax_ce_workspace_bytes(int64_t n) {
+  return 256 + sizeof(double) * (size_t)ceil_div(n > 0 ? n : 1, 256);
+}
+
+static int softmax_launch(int dtype, const void* y, int64_t ld_y, const void* t, int64_t ld_t,
+                          int64_t classes, int64_t n, double divisor, void* d_y, int64_t ld_dy,
+                          double* loss_out, void* bias, void* vbias, void* grad_bias,
+                          int opt_kind, double mu, double eta, int32_t* counter, int32_t modulo,
+                          void* workspace, void* stream) {
+  SMB_REQUIRE(classes >= 1 && n >= 0, "softmax: bad shape");
+  SMB_REQUIRE(ld_y >= n && ld_t >= n && ld_dy >= n, "softmax: leading dimension");
+  SMB_REQUIRE(divisor != 0.0, "softmax: zero divisor");
+  SMB_REQUIRE(n <= (int64_t(1) << 30), "softmax: batch too wide");
+  return dispatch_dtype(dtype, "smb_softmax_ce", [&](auto tag) {
+    using T = decltype(tag);
+    // multi-CTA needs the workspace (ticket + per-CTA loss partials)
+    const unsigned grid = workspace ? (unsigned)ceil_div(n > 0 ? n : 1, 256) : 1u;
+    unsigned* ticket = workspace ? static_cast<unsigned*>(workspace) : nullptr;
+    double* parts = workspace ? reinterpret_cast<double*>(static_cast<char*>(workspace) + 256)
+                              : nullptr;
+    const size_t dyn = sizeof(T) * 8 * (size_t)warp_pairwise_leaves((int)n);
+    auto kern = softmax_step_kernel<T>;
+    if (dyn > 40 * 1024)
+      ensure_smem(kern, dyn);
+    kern<<<grid, 256, dyn, as_stream(stream)>>>(
+        static_cast<const T*>(y), ld_y, static_cast<const T*>(t), ld_t, classes, n,
+        static_cast<T>(divisor), static_cast<T*>(d_y), ld_dy, loss_out, parts, ticket,
+        static_cast<T*>(bias), static_cast<T*>(vbias), static_cast<T*>(grad_bias),
+        make_opt<T>(opt_kind, mu, eta), counter, modulo);
+    return check_launch("smb_softmax_ce");
   });
 }
 
@@ -205,17 +345,26 @@ extern "C" int smb_softmax_ce_grad(int dtype, const void* y, int64_t ld_y, const
                                    int64_t ld_t, int64_t classes, int64_t n, double divisor,
                                    void* d_y, int64_t ld_dy, double* loss_out, void* stream) {
   clear_error();
-  SMB_REQUIRE(classes >= 1 && n >= 0, "smb_softmax_ce_grad: bad shape");
-  SMB_REQUIRE(ld_y >= n && ld_t >= n && ld_dy >= n, "smb_softmax_ce_grad: leading dimension");
-  SMB_REQUIRE(divisor != 0.0, "smb_softmax_ce_grad: zero divisor");
-  return dispatch_dtype(dtype, "smb_softmax_ce_grad", [&](auto tag) {
-    using T = decltype(tag);
-    // one CTA keeps the optional loss reduction in a fixed order
-    softmax_ce_kernel<T><<<1, 1024, 0, as_stream(stream)>>>(
-        static_cast<const T*>(y), ld_y, static_cast<const T*>(t), ld_t, classes, n,
-        static_cast<T>(divisor), static_cast<T*>(d_y), ld_dy, loss_out);
-    return check_launch("smb_softmax_ce_grad");
-  });
+  return softmax_launch(dtype, y, ld_y, t, ld_t, classes, n, divisor, d_y, ld_dy, loss_out,
+                        nullptr, nullptr, nullptr, SMB_OPT_NONE, 0, 0, nullptr, 0, nullptr,
+                        stream);
+}
+
+extern "C" int smb_softmax_ce_step(int dtype, const void* y, int64_t ld_y, const void* t,
+                                   int64_t ld_t, int64_t classes, int64_t n, double divisor,
+                                   void* d_y, int64_t ld_dy, double* loss_out, void* bias,
+                                   void* velocity_bias, void* grad_bias_out, int opt_kind,
+                                   double mu, double eta, int32_t* step_counter, int32_t modulo,
+                                   void* workspace, void* stream) {
+  clear_error();
+  SMB_REQUIRE(opt_kind >= SMB_OPT_NONE && opt_kind <= SMB_OPT_NESTEROV,
+              "smb_softmax_ce_step: bad optimizer kind %d", opt_kind);
+  SMB_REQUIRE(!(opt_kind == SMB_OPT_MOMENTUM || opt_kind == SMB_OPT_NESTEROV) || bias == nullptr ||
+                  velocity_bias != nullptr,
+              "smb_softmax_ce_step: momentum needs a bias velocity buffer");
+  return softmax_launch(dtype, y, ld_y, t, ld_t, classes, n, divisor, d_y, ld_dy, loss_out, bias,
+                        velocity_bias, grad_bias_out, opt_kind, mu, eta, step_counter, modulo,
+                        workspace, stream);
 }
 
 extern "C" int smb_relu(int dtype, const void* x, int64_t ld_x, int64_t m, int64_t n, void* y,
@@ -259,13 +408,26 @@ extern "C" int smb_gather_columns(int dtype, const void* src, int64_t n_samples,
   if (batch == 0 || features == 0) return SMB_OK;
   return dispatch_dtype(dtype, "smb_gather_columns", [&](auto tag) {
     using T = decltype(tag);
-    dim3 grid((unsigned)ceil_div(batch, 32), (unsigned)ceil_div(features, 32));
-    gather_columns_kernel<T><<<grid, dim3(32, 8), 0, as_stream(stream)>>>(
-        static_cast<const T*>(src), features, perm, step_counter, base, batch,
-        static_cast<T*>(dst), ld_dst);
+    dim3 grid((unsigned)ceil_div(batch, 32), (unsigned)ceil_div(features, 128));
+    const bool vec = aligned16(src) && (features * (int64_t)sizeof(T)) % 16 == 0;
+    if (vec)
+      gather_columns_kernel<T, true><<<grid, 256, 0, as_stream(stream)>>>(
+          static_cast<const T*>(src), features, perm, step_counter, base, batch,
+          static_cast<T*>(dst), ld_dst);
+    else
+      gather_columns_kernel<T, false><<<grid, 256, 0, as_stream(stream)>>>(
+          static_cast<const T*>(src), features, perm, step_counter, base, batch,
+          static_cast<T*>(dst), ld_dst);
     return check_launch("smb_gather_columns");
   });
 }
+
+namespace smb {
+__global__ void step_counter_kernel(int32_t* counter, int32_t modulo) {
+  const int32_t v = *counter + 1;
+  *counter = (modulo > 0 && v >= modulo) ? 0 : v;
+}
+}  // namespace smb
 
 extern "C" int smb_step_counter_advance(int32_t* counter, int32_t modulo, void* stream) {
   clear_error();

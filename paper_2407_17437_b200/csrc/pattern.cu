@@ -2,6 +2,8 @@
 // (tensor_core._validate_structure, tensor_core.py:78-94), a deterministic
 // CSR -> CSC transpose index (replaces the O(nblocks * nnz) rescan of
 // _kernels.spmm_t_kernel, _kernels.py:40-59) and the SDDMM tile index.
+#include <vector>
+
 #include "pattern.cuh"
 
 namespace smb {
@@ -226,6 +228,22 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
   cudaFree(tmp_perm);
   count_launches(launches);
   if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) return fail_cuda("index build");
+  if (nnz > 0) {
+    // row spans of 128- and 512-nonzero tiles: tile t covers rows
+    // tile_row0[t] .. row of its last nonzero <= tile_row0[t + 1] (or m - 1)
+    std::vector<int32_t> t0(p->ntiles);
+    if (cudaMemcpy(t0.data(), p->tile_row0, sizeof(int32_t) * p->ntiles,
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return fail_cuda("tile index readback");
+    for (int64_t t = 0; t < p->ntiles; ++t) {
+      const int64_t last128 = (t + 1 < p->ntiles) ? t0[t + 1] : m - 1;
+      p->span128 = imax(p->span128, last128 - t0[t] + 1);
+      if (t % 4 == 0) {
+        const int64_t last512 = (t + 4 < p->ntiles) ? t0[t + 4] : m - 1;
+        p->span512 = imax(p->span512, last512 - t0[t] + 1);
+      }
+    }
+  }
   *out = p;
   return SMB_OK;
 }

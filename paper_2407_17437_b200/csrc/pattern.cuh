@@ -13,6 +13,9 @@ struct smb_pattern {
   int32_t* perm = nullptr;           // owned, [nnz]   CSC slot -> CSR value index
   int32_t* tile_row0 = nullptr;      // owned, [ntiles] row of nonzero t*kSddmmTile
   int64_t ntiles = 0;
+  // most rows spanned by any tile of kSddmmTile (span128) / 4*kSddmmTile
+  // (span512) consecutive nonzeros (first row .. row of the last nonzero)
+  int64_t span128 = 0, span512 = 0;
 };
 
 namespace smb {

@@ -4,47 +4,58 @@
 // sequentially over t with separately rounded multiply/add exactly like
 // _kernels.sddmm_kernel (_kernels.py:62-75), then (optionally) the momentum /
 // Nesterov / GD update of values and velocity in the sparse_combine order of
-// SparseLinearLayer.optimize (nn.py:187-197).  Extra CTAs of the same launch
-// compute grad_bias = row_sums(d_out) in numpy's pairwise order (nn.py:184)
-// and update bias / velocity_bias (_step_vector, nn.py:118-131).  No dense
-// m x k gradient and no mask is ever formed.
+// SparseLinearLayer.optimize (nn.py:187-197).  No dense m x k gradient and no
+// mask is ever formed.  The bias side (grad_bias = row_sums(d_out), nn.py:184,
+// and its _step_vector update) runs in the warp-per-row kernel of
+// elementwise.cu -- or, on the fused training step, in the epilogue of the
+// transposed SpMM / softmax kernel that produced d_out.
 //
-// Mapping: one CTA = 128 consecutive nonzeros (one per thread) of the CSR
-// order; the batch is walked in 32-column chunks through a 3-stage cp.async
-// pipeline that stages, per chunk, the 128 gathered x rows and the (few)
-// d_out rows the tile touches.  Rows are padded to 32+16/sizeof(T) elements
-// so each thread's 16-byte LDS of its own x row and the broadcast LDS of its
-// d_out row are bank-conflict free.  Each thread runs one sequential
-// accumulation chain (required for bit-exactness), 4 (fp32) columns per LDS.
+// Mapping: one CTA = TILE (128 or 512) consecutive nonzeros of the CSR order,
+// one per thread, each running ONE sequential accumulation chain (required
+// for bit-exactness; the FADD latency is hidden by having 16 warps of
+// independent chains per SM).  The batch is walked in 16-column chunks
+// through a STAGES-deep ring in shared memory, filled with 16-byte cp.async
+// (LDGSTS) copies of the gathered x rows and of the few d_out rows the tile
+// touches; one barrier per chunk.  Every thread owns a fixed set of copy
+// slots (row base pointer + smem offset computed once), so a copy costs ~4
+// instructions.  Rows are padded to 16 + 16/sizeof(T) elements so each
+// thread's 16-byte LDS of its own x row and the (broadcast) LDS of its d_out
+// row are bank-conflict free.
+// (A TMA variant -- one cp.async.bulk per 128-byte row, producer warp +
+// mbarrier ring -- measured 4x slower on B200: 128-byte bulk copies are
+// request-rate bound at ~1.1 TB/s.  See DESIGN.md.)
 #include "pattern.cuh"
 
 namespace smb {
 namespace {
 
-constexpr int kTile = kSddmmTile;  // nonzeros per CTA == threads per CTA
-constexpr int kChunk = 32;         // batch columns per pipeline stage
-constexpr int kSlots = 32;         // staged d_out rows per tile
-constexpr int kStages = 3;
+constexpr int kChunk = 16;  // batch columns per pipeline stage
 
-template <typename T>
+template <typename T, int TILE>
 struct SddmmCfg {
-  static constexpr int VW = 16 / sizeof(T);   // elements per 16 B
-  static constexpr int LDS = kChunk + VW;     // padded smem row (elements)
-  static constexpr int VPR = kChunk / VW;     // 16 B vectors per staged row
-  static constexpr size_t stage_elems = size_t(kTile + kSlots) * LDS;
-  static constexpr size_t smem_bytes = kStages * stage_elems * sizeof(T);
+  static constexpr int VW = 16 / sizeof(T);  // elements per 16 B
+  static constexpr int LDS = kChunk + VW;    // padded smem row (elements)
+  static constexpr int VPR = kChunk / VW;    // 16 B vectors per staged row
+  static constexpr int SLOTS = TILE / 4;  // staged d_out rows per tile
+  // fp32: 512-tile x 4 stages = 200 KB (1 CTA, 16 warps / SM),
+  //       128-tile x 6 stages = 77 KB (2 CTAs / SM)
+  static constexpr int STAGES = TILE >= 512 ? 4 : 6;
+  static constexpr size_t stage_elems = size_t(TILE + SLOTS) * LDS;
+  static constexpr size_t smem_bytes = STAGES * stage_elems * sizeof(T);
+  static_assert(TILE % VPR == 0, "tile / vector split");
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gmem),
                "r"(src_bytes));
 }
 template <int BYTES>
-__device__ __forceinline__ void cp_async_small(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem), "n"(BYTES),
-               "r"(src_bytes));
+__device__ __forceinline__ void cp_async_small(unsigned dst, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(gmem),
+               "n"(BYTES), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
@@ -52,149 +63,156 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Stage one 32-column chunk of a row (x row of a nonzero, or a d_out row).
-template <typename T, bool VEC>
-__device__ __forceinline__ void stage_row_part(T* dst_row, const T* src_row, int64_t t0, int64_t n,
-                                               int v, bool row_valid) {
-  using C = SddmmCfg<T>;
-  if constexpr (VEC) {
-    const int64_t c0 = t0 + (int64_t)v * C::VW;
-    int valid = row_valid ? (int)imax(0, imin(C::VW, n - c0)) : 0;
-    const T* src = valid > 0 ? src_row + c0 : src_row;
-    cp_async16(dst_row + v * C::VW, src, valid * (int)sizeof(T));
-  } else {
-#pragma unroll
-    for (int j = 0; j < C::VW; ++j) {
-      const int64_t c = t0 + (int64_t)v * C::VW + j;
-      const bool ok = row_valid && c < n;
-      cp_async_small<sizeof(T)>(dst_row + v * C::VW + j, ok ? src_row + c : src_row,
-                                ok ? (int)sizeof(T) : 0);
-    }
-  }
-}
-
-template <typename T>
-__device__ void bias_rows(int64_t row0, int64_t m, const T* __restrict__ d_out, int64_t ld_d,
-                          int64_t n, T* bias, T* vbias, T* grad_bias_out,
-                          const OptConsts<T>& opt) {
-  const int64_t row = row0 + threadIdx.x;
-  if (row >= m) return;
-  const T g = pairwise_sum(d_out + row * ld_d, n);
-  if (grad_bias_out) grad_bias_out[row] = g;
-  if (opt.kind != SMB_OPT_NONE && bias) {
-    T dummy = T(0);
-    apply_update(opt, g, bias + row, vbias ? vbias + row : &dummy);
-  }
-}
-
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(kTile)
-    sddmm_update_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                        const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
-                        int64_t nz_tiles, const T* __restrict__ d_out, int64_t ld_d,
-                        const T* __restrict__ x, int64_t ld_x, int64_t n, T* values, T* velocity,
-                        T* grad_out, T* bias, T* vbias, T* grad_bias_out, OptConsts<T> opt) {
-  using C = SddmmCfg<T>;
-  if ((int64_t)blockIdx.x >= nz_tiles) {
-    bias_rows<T>(((int64_t)blockIdx.x - nz_tiles) * kTile, m, d_out, ld_d, n, bias, vbias,
-                 grad_bias_out, opt);
-    return;
-  }
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* smem = reinterpret_cast<T*>(smem_raw);
-  __shared__ int32_t s_col[kTile];
-  __shared__ int32_t s_rp[kTile + 1];
-
-  const int tid = threadIdx.x;
-  const int64_t p0 = (int64_t)blockIdx.x * kTile;
-  const int64_t p = p0 + tid;
-  const bool active = p < nnz;
-  const int32_t r0 = tile_row0[blockIdx.x];
-
-  // row of p: binary search in a shared window of row_ptr[r0 .. r0+kTile]
-  s_col[tid] = active ? col_idx[p] : 0;
-  s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
-  if (tid == 0) s_rp[kTile] = (r0 + kTile <= m) ? row_ptr[r0 + kTile] : INT32_MAX;
-  __syncthreads();
-  int64_t row;
-  if (p < (int64_t)s_rp[kTile]) {
-    int lo = 0, hi = kTile;  // s_rp[lo] <= p < s_rp[hi]
+// Row of nonzero p inside a tile starting at row r0, through a shared window
+// s_rp[0..W] = row_ptr[r0 .. r0+W]; global binary search when the tile spans
+// more than W rows (long runs of empty rows).
+template <int W>
+__device__ __forceinline__ int64_t tile_row_of(int64_t p, int32_t r0, const int32_t* s_rp,
+                                               const int32_t* row_ptr, int64_t m) {
+  if (p < (int64_t)s_rp[W]) {
+    int lo = 0, hi = W;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if ((int64_t)s_rp[mid] <= p) lo = mid; else hi = mid;
     }
-    row = r0 + lo;
-  } else {  // tile spans more than kTile rows (empty rows): global search
-    int64_t lo = r0 + kTile, hi = m;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)row_ptr[mid] <= p) lo = mid; else hi = mid;
-    }
-    row = lo;
+    return r0 + lo;
   }
-  const int slot = (int)imin(row - r0, kSlots);  // kSlots == "not staged"
-  const int n_staged = (int)imin(kSlots, m - r0);
+  int64_t lo = r0 + W, hi = m;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)row_ptr[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 
-  const int64_t n_chunks = (n + kChunk - 1) / kChunk;
-  auto issue = [&](int64_t ch) {
-    T* xs = smem + (ch % kStages) * C::stage_elems;
-    T* ds = xs + kTile * C::LDS;
-    const int64_t t0 = ch * kChunk;
-    for (int e = tid; e < kTile * C::VPR; e += kTile) {
-      const int r = e / C::VPR, v = e % C::VPR;
-      stage_row_part<T, VEC>(xs + r * C::LDS, x + (int64_t)s_col[r] * ld_x, t0, n, v,
-                             p0 + r < nnz);
-    }
-    for (int e = tid; e < n_staged * C::VPR; e += kTile) {
-      const int r = e / C::VPR, v = e % C::VPR;
-      stage_row_part<T, VEC>(ds + r * C::LDS, d_out + (int64_t)(r0 + r) * ld_d, t0, n, v, true);
-    }
-  };
-
+// Copy `bytes` (<= 16) of a 16-byte vector; VEC: one cp.async with zero fill,
+// else element-wise (unaligned operands).
+template <typename T, bool VEC>
+__device__ __forceinline__ void copy_vec(unsigned dst, const T* src, int valid_elems) {
+  constexpr int VW = 16 / sizeof(T);
+  if constexpr (VEC) {
+    cp_async16(dst, src, valid_elems * (int)sizeof(T));
+  } else {
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+    for (int j = 0; j < VW; ++j)
+      cp_async_small<sizeof(T)>(dst + j * sizeof(T), j < valid_elems ? src + j : src,
+                                j < valid_elems ? (int)sizeof(T) : 0);
+  }
+}
+
+// ALL: every tile's d_out rows fit the SLOTS staging rows (checked on the
+// host from the pattern's tile spans), so the hot loop has no fallback path.
+template <typename T, int TILE, bool VEC, bool ALL>
+__global__ void __launch_bounds__(TILE)
+    sddmm_pipe_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                      const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
+                      const T* __restrict__ d_out, int64_t ld_d, const T* __restrict__ x,
+                      int64_t ld_x, int64_t n, T* values, T* velocity, T* grad_out,
+                      OptConsts<T> opt) {
+  using C = SddmmCfg<T, TILE>;
+  constexpr int S = C::STAGES, VW = C::VW, VPR = C::VPR, LDS = C::LDS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  __shared__ int32_t s_col[TILE];
+  __shared__ int32_t s_rp[TILE + 1];
+  const int tid = threadIdx.x;
+  const int64_t p0 = (int64_t)blockIdx.x * TILE;
+  const int64_t p = p0 + tid;
+  const int n_active = (int)imin(TILE, nnz - p0);
+  const bool active = tid < n_active;
+  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (TILE / kSddmmTile)];
+  s_col[tid] = active ? col_idx[p] : 0;
+  s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
+  if (tid == 0) s_rp[TILE] = (r0 + TILE <= m) ? row_ptr[r0 + TILE] : INT32_MAX;
+  __syncthreads();
+  const int64_t row = tile_row_of<TILE>(p, r0, s_rp, row_ptr, m);
+  const int slot = (int)imin(row - r0, C::SLOTS);  // SLOTS == "not staged"
+  const int n_staged = (int)imin(C::SLOTS, m - r0);
+  const int64_t n_chunks = (n + kChunk - 1) / kChunk;
+
+  // ---- fixed copy slots of this thread (computed once) ----
+  // x rows: vector v = tid % VPR of rows tid/VPR + k*TILE/VPR, k < VPR
+  const int v = tid % VPR;
+  const T* xsrc[VPR];
+  unsigned xdst[VPR];
+  int xok[VPR];
+#pragma unroll
+  for (int k = 0; k < VPR; ++k) {
+    const int r = tid / VPR + k * (TILE / VPR);
+    xok[k] = r < n_active;
+    xsrc[k] = x + (int64_t)s_col[r] * ld_x + v * VW;
+    xdst[k] = (unsigned)((r * LDS + v * VW) * sizeof(T));
+  }
+  // d_out rows of the tile: SLOTS*VPR copies, DC per thread; copy e = tid +
+  // c*TILE stages vector v of slot row e/VPR (TILE % VPR == 0 keeps v fixed)
+  constexpr int DC = (C::SLOTS * VPR + TILE - 1) / TILE;
+  bool dcopy[DC];
+  const T* dsrc[DC];
+  unsigned ddst[DC];
+#pragma unroll
+  for (int c = 0; c < DC; ++c) {
+    const int e = tid + c * TILE;
+    dcopy[c] = e < n_staged * VPR;
+    dsrc[c] = d_out + (int64_t)(r0 + (dcopy[c] ? e / VPR : 0)) * ld_d + v * VW;
+    ddst[c] = (unsigned)(((TILE + e / VPR) * LDS + v * VW) * sizeof(T));
+  }
+  const unsigned sbase = smem_u32(smem);
+  constexpr unsigned kStageBytes = (unsigned)(C::stage_elems * sizeof(T));
+
+  auto issue = [&](int64_t ch) {
+    const unsigned st = sbase + (unsigned)(ch % S) * kStageBytes;
+    const int64_t t0 = ch * kChunk;
+    // elements of this thread's vector inside [0, n)
+    const int valid = (int)imax(0, imin(VW, n - (t0 + v * VW)));
+#pragma unroll
+    for (int k = 0; k < VPR; ++k) copy_vec<T, VEC>(st + xdst[k], xsrc[k] + t0, xok[k] ? valid : 0);
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+      if (dcopy[c]) copy_vec<T, VEC>(st + ddst[c], dsrc[c] + t0, valid);
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
     if (s < n_chunks) issue(s);
     cp_async_commit();
   }
-
   // -0.0 is the exact additive identity, so acc = -0 + a0*b0 == a0*b0 and the
   // chain below is the reference's  acc = a0*b0; acc += a_t*b_t  verbatim.
   T acc = T(-0.0);
   const T* drow = d_out + row * ld_d;
+  using V = typename Vec16<T>::type;
   for (int64_t ch = 0; ch < n_chunks; ++ch) {
-    if (ch + kStages - 1 < n_chunks) issue(ch + kStages - 1);
+    cp_async_wait<S - 2>();
+    __syncthreads();  // chunk ch landed for everyone; stage (ch-1)%S is free
+    if (ch + S - 1 < n_chunks) issue(ch + S - 1);
     cp_async_commit();
-    cp_async_wait<kStages - 1>();
-    __syncthreads();
     if (active) {
-      const T* xs = smem + (ch % kStages) * C::stage_elems;
-      const T* xr = xs + tid * C::LDS;
-      const T* dr = xs + (kTile + slot) * C::LDS;
+      const T* xs = smem + (ch % S) * C::stage_elems;
+      const T* xr = xs + tid * LDS;
+      const T* dr = xs + (TILE + slot) * LDS;
       const int64_t t0 = ch * kChunk;
       const int cnt = (int)imin(kChunk, n - t0);
       if (cnt == kChunk) {
 #pragma unroll
-        for (int v = 0; v < C::VPR; ++v) {
-          using V = typename Vec16<T>::type;
-          const V xv = *reinterpret_cast<const V*>(xr + v * C::VW);
+        for (int u = 0; u < VPR; ++u) {
+          const V xv = *reinterpret_cast<const V*>(xr + u * VW);
           V dv;
-          if (slot < kSlots) dv = *reinterpret_cast<const V*>(dr + v * C::VW);
-          else {
+          if (ALL || slot < C::SLOTS) {
+            dv = *reinterpret_cast<const V*>(dr + u * VW);
+          } else {
 #pragma unroll
-            for (int j = 0; j < C::VW; ++j) VecOps<T>::set(dv, j, drow[t0 + v * C::VW + j]);
+            for (int j = 0; j < VW; ++j) VecOps<T>::set(dv, j, drow[t0 + u * VW + j]);
           }
 #pragma unroll
-          for (int j = 0; j < C::VW; ++j)
+          for (int j = 0; j < VW; ++j)
             acc = add_rn(acc, mul_rn(VecOps<T>::get(dv, j), VecOps<T>::get(xv, j)));
         }
       } else {
         for (int j = 0; j < cnt; ++j) {
-          const T dv = slot < kSlots ? dr[j] : drow[t0 + j];
+          const T dv = (ALL || slot < C::SLOTS) ? dr[j] : drow[t0 + j];
           acc = add_rn(acc, mul_rn(dv, xr[j]));
         }
       }
     }
-    __syncthreads();
   }
   cp_async_wait<0>();
   if (!active) return;
@@ -206,38 +224,52 @@ __global__ void __launch_bounds__(kTile)
   }
 }
 
+}  // namespace
+
+template <typename T>
+int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias, T* grad,
+                     const OptConsts<T>& opt, cudaStream_t st);
+
 template <typename T>
 int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, const void* x,
                       int64_t ld_x, int64_t n, void* values, void* velocity, void* grad_out,
                       void* bias, void* vbias, void* grad_bias_out, int opt_kind, double mu,
                       double eta, void* stream, const char* name) {
-  using C = SddmmCfg<T>;
   const OptConsts<T> opt = make_opt<T>(opt_kind, mu, eta);
-  const bool want_bias = (grad_bias_out != nullptr) || (opt_kind != SMB_OPT_NONE && bias);
-  const int64_t bias_tiles = want_bias ? ceil_div(pat->m, kTile) : 0;
-  const int64_t grid = pat->ntiles + bias_tiles;
-  if (grid == 0) return SMB_OK;
-  const bool vec = aligned16(x) && aligned16(d_out) && ld_x % C::VW == 0 && ld_d % C::VW == 0;
   cudaStream_t st = as_stream(stream);
-  auto run = [&](auto kernel) {
-    static thread_local bool configured = false;  // per (T, VEC) instantiation
-    if (!configured) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)C::smem_bytes);
-      configured = true;
+  if (pat->ntiles > 0) {
+    constexpr int VW = 16 / sizeof(T);
+    const bool vec = aligned16(x) && aligned16(d_out) && ld_x % VW == 0 && ld_d % VW == 0;
+    // 512-nonzero tiles (16 warps of chains per SM) when there are enough of
+    // them to fill the GPU; 128-nonzero tiles for small layers and fp64
+    const bool big = sizeof(T) == 4 && ceil_div(pat->nnz, 512) >= 148;
+    auto go = [&](auto kernel, int tile, size_t bytes) {
+      ensure_smem(kernel, bytes);
+      kernel<<<(unsigned)ceil_div(pat->nnz, tile), tile, bytes, st>>>(
+          pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz,
+          static_cast<const T*>(d_out), ld_d, static_cast<const T*>(x), ld_x, n,
+          static_cast<T*>(values), static_cast<T*>(velocity), static_cast<T*>(grad_out), opt);
+    };
+    // every tile's d_out rows staged -> fallback-free kernel
+    const bool all = (big ? pat->span512 : pat->span128) <= (big ? 512 : 128) / 4;
+    if (big) {
+      if (vec && all) go(sddmm_pipe_kernel<T, 512, true, true>, 512, SddmmCfg<T, 512>::smem_bytes);
+      else if (vec) go(sddmm_pipe_kernel<T, 512, true, false>, 512, SddmmCfg<T, 512>::smem_bytes);
+      else go(sddmm_pipe_kernel<T, 512, false, false>, 512, SddmmCfg<T, 512>::smem_bytes);
+    } else {
+      if (vec && all) go(sddmm_pipe_kernel<T, 128, true, true>, 128, SddmmCfg<T, 128>::smem_bytes);
+      else if (vec) go(sddmm_pipe_kernel<T, 128, true, false>, 128, SddmmCfg<T, 128>::smem_bytes);
+      else go(sddmm_pipe_kernel<T, 128, false, false>, 128, SddmmCfg<T, 128>::smem_bytes);
     }
-    kernel<<<(unsigned)grid, kTile, C::smem_bytes, st>>>(
-        pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz, pat->ntiles,
-        static_cast<const T*>(d_out), ld_d, static_cast<const T*>(x), ld_x, n,
-        static_cast<T*>(values), static_cast<T*>(velocity), static_cast<T*>(grad_out),
-        static_cast<T*>(bias), static_cast<T*>(vbias), static_cast<T*>(grad_bias_out), opt);
-  };
-  if (vec) run(sddmm_update_kernel<T, true>);
-  else run(sddmm_update_kernel<T, false>);
-  return check_launch(name);
+    const int rc = check_launch(name);
+    if (rc != SMB_OK) return rc;
+  }
+  const bool want_bias = (grad_bias_out != nullptr) || (opt_kind != SMB_OPT_NONE && bias);
+  if (!want_bias) return SMB_OK;
+  return launch_bias_rows<T>(static_cast<const T*>(d_out), ld_d, pat->m, n, static_cast<T*>(bias),
+                             static_cast<T*>(vbias), static_cast<T*>(grad_bias_out), opt, st);
 }
 
-}  // namespace
 }  // namespace smb
 
 using namespace smb;

@@ -6,37 +6,54 @@
 // (_kernels.py:25-37) and (CSC column, row_idx, values[perm]) for dX = W^T dY
 // (_kernels.py:40-59; ascending source row == the reference's row-order scan).
 //
-// Mapping: one warp owns (output row, 32*W-column chunk of the batch); each
-// lane owns W consecutive batch columns and keeps them in registers for the
-// whole segment, so accumulation order per element is exactly the
-// reference's (ascending s, mul and add rounded separately).  The warp reads
-// 32 (idx, val) pairs with one coalesced load and broadcasts them with
-// shuffles; the dense rows are gathered as 512-byte coalesced vectors
-// through the read-only path, U rows in flight per warp.
+// Mapping: one CTA owns one output row (gridDim.y splits very wide batches);
+// its warps own consecutive 32*W-column chunks of the batch and each lane
+// keeps W consecutive columns in registers for the whole segment, so the
+// accumulation order per element is exactly the reference's (ascending s,
+// multiply and add rounded separately).  Each warp reads 32 (idx, val) pairs
+// with one coalesced load and broadcasts them with shuffles; the dense rows
+// are gathered as 128/512-byte coalesced vectors through the read-only path
+// with a U-deep refill-on-consume register ring per warp.
+//
+// Epilogues (fused, one pass over the output row):
+//   forward   + bias[r], np.maximum(., 0)                     nn.py:173, 86-87
+//   backward  * (mask > 0)  (ReLU.backward of the layer below)  nn.py:89-91
+//             and, when one CTA covers the whole row, grad_bias[r] =
+//             row_sums(out[r, :]) in numpy's pairwise order (nn.py:184) with
+//             the bias optimizer update (_step_vector, nn.py:118-131).
 #include "pattern.cuh"
 
 namespace smb {
 namespace {
-
-constexpr int kWarpsPerBlock = 8;
-constexpr int kUnroll = 8;
 
 template <typename T, int W>
 struct Frag {
   T v[W];
 };
 
+// W consecutive elements as 16-byte vectors (W a multiple of the vector width)
+template <typename T, int W>
+__device__ __forceinline__ void load_frag_full(Frag<T, W>& f, const T* p) {
+  if constexpr (W == 1) {
+    f.v[0] = ldg_stream(p);
+  } else {
+    using V = typename Vec16<T>::type;
+    constexpr int VW = Vec16<T>::N;
+    static_assert(W % VW == 0, "vector width");
+#pragma unroll
+    for (int h = 0; h < W / VW; ++h) {
+      const V v = ldg_vec(reinterpret_cast<const V*>(p) + h);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) f.v[h * VW + j] = VecOps<T>::get(v, j);
+    }
+  }
+}
+
 template <typename T, int W>
 __device__ __forceinline__ void load_frag(Frag<T, W>& f, const T* p, int valid) {
-  if constexpr (W > 1) {
-    using V = typename Vec16<T>::type;
-    static_assert(sizeof(V) == W * sizeof(T), "vector width");
-    if (valid == W) {
-      V v = ldg_vec(reinterpret_cast<const V*>(p));
-#pragma unroll
-      for (int j = 0; j < W; ++j) f.v[j] = VecOps<T>::get(v, j);
-      return;
-    }
+  if (valid == W) {
+    load_frag_full<T, W>(f, p);
+    return;
   }
 #pragma unroll
   for (int j = 0; j < W; ++j) f.v[j] = (j < valid) ? __ldg(p + j) : T(0);
@@ -46,11 +63,15 @@ template <typename T, int W>
 __device__ __forceinline__ void store_frag(const Frag<T, W>& f, T* p, int valid) {
   if constexpr (W > 1) {
     using V = typename Vec16<T>::type;
+    constexpr int VW = Vec16<T>::N;
     if (valid == W) {
-      V v;
 #pragma unroll
-      for (int j = 0; j < W; ++j) VecOps<T>::set(v, j, f.v[j]);
-      *reinterpret_cast<V*>(p) = v;
+      for (int h = 0; h < W / VW; ++h) {
+        V v;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) VecOps<T>::set(v, j, f.v[h * VW + j]);
+        reinterpret_cast<V*>(p)[h] = v;
+      }
       return;
     }
   }
@@ -63,24 +84,35 @@ enum EpiKind { kEpiBiasAct = 0, kEpiMask = 1 };
 
 template <typename T>
 struct EpiArgs {
-  const T* bias;   // kEpiBiasAct: per-row bias or null
-  int relu;        // kEpiBiasAct: apply np.maximum(y, 0)
-  const T* mask;   // kEpiMask: out *= (mask > 0), or null
+  const T* bias;  // forward: per-row bias or null
+  int relu;       // forward: apply np.maximum(y, 0)
+  const T* mask;  // backward: out *= (mask > 0), or null
   int64_t ld_mask;
+  // backward row-sum stage (only when the CTA covers the whole row)
+  int rowsum;
+  T* rb_bias;   // bias of the layer whose output gradient this is (updated)
+  T* rb_vbias;  // its velocity
+  T* rb_grad;   // grad_bias out (may be null)
+  OptConsts<T> opt;
 };
 
-template <typename T, int W, int EPI, bool PERM>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    segment_spmm_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
-                        const int32_t* __restrict__ perm, const T* __restrict__ vals,
-                        int64_t n_rows, const T* __restrict__ dense, int64_t ld_dense,
-                        int64_t n, int64_t n_chunks, T* __restrict__ out, int64_t ld_out,
-                        EpiArgs<T> epi) {
+// widest CTA per row: 32 warps with scalar lanes, 16 warps with 16-byte
+// lanes, 8 warps with 32-byte lanes (keeps the U-deep ring in registers)
+template <int W>
+constexpr int max_threads_for() { return W * 4 > 16 ? 256 : (W > 1 ? 512 : 1024); }
+
+template <typename T, int W, int U, int EPI, bool PERM>
+__global__ void __launch_bounds__(max_threads_for<W>())
+    row_spmm_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
+                    const int32_t* __restrict__ perm, const T* __restrict__ vals,
+                    const T* __restrict__ dense, int64_t ld_dense, int64_t n,
+                    T* __restrict__ out, int64_t ld_out, EpiArgs<T> epi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (gw >= n_rows * n_chunks) return;
-  const int64_t row = gw / n_chunks;
-  const int64_t chunk = gw - row * n_chunks;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int64_t row = blockIdx.x;
+  const int64_t chunk = (int64_t)blockIdx.y * nwarps + warp;
   const int64_t col0 = chunk * (32 * W) + (int64_t)lane * W;
   const int valid = (int)imax(0, imin(W, n - col0));
 
@@ -91,7 +123,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int32_t s_begin = seg_ptr[row];
   const int32_t s_end = seg_ptr[row + 1];
   const T* dcol = dense + col0;
+  const uint32_t ldu = (uint32_t)ld_dense;  // row offsets as one IMAD.WIDE.U32
+  // warp-uniform: every lane of this warp owns W valid columns
+  const bool full_chunk = (chunk + 1) * (32 * W) <= n;
 
+  // 32 (idx, val) pairs per coalesced load, broadcast by shuffles; a U-deep
+  // ring of dense-row fragments, each slot refilled as soon as it is consumed
   for (int32_t s0 = s_begin; s0 < s_end; s0 += 32) {
     const int cnt = min(32, s_end - s0);
     int my_idx = 0;
@@ -100,26 +137,48 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       my_idx = idx[s0 + lane];
       my_val = PERM ? vals[perm[s0 + lane]] : vals[s0 + lane];
     }
-    for (int q = 0; q < cnt; q += kUnroll) {
-      Frag<T, W> xs[kUnroll];
+    Frag<T, W> xs[U];
+    if (cnt == 32 && full_chunk) {
+      // fast path: fully unrolled, no runtime predicates
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int src = __shfl_sync(0xffffffffu, my_idx, (q + u) & 31);
-        if (q + u < cnt && valid > 0) load_frag<T, W>(xs[u], dcol + (int64_t)src * ld_dense, valid);
+      for (int u = 0; u < U; ++u) {
+        const uint32_t src = (uint32_t)__shfl_sync(0xffffffffu, my_idx, u);
+        load_frag_full<T, W>(xs[u], dcol + (size_t)src * ldu);
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int q = 0; q < 32; ++q) {
+        const T v = __shfl_sync(0xffffffffu, my_val, q);
+#pragma unroll
+        for (int j = 0; j < W; ++j) acc.v[j] = add_rn(acc.v[j], mul_rn(v, xs[q % U].v[j]));
+        if (q + U < 32) {
+          const uint32_t nxt = (uint32_t)__shfl_sync(0xffffffffu, my_idx, q + U);
+          load_frag_full<T, W>(xs[q % U], dcol + (size_t)nxt * ldu);
+        }
+      }
+      continue;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int src = __shfl_sync(0xffffffffu, my_idx, u & 31);
+      if (u < cnt && valid > 0) load_frag<T, W>(xs[u], dcol + (int64_t)src * ld_dense, valid);
+    }
+    for (int q = 0; q < cnt; q += U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         const T v = __shfl_sync(0xffffffffu, my_val, (q + u) & 31);
+        const int nxt = __shfl_sync(0xffffffffu, my_idx, (q + u + U) & 31);
         if (q + u < cnt) {
 #pragma unroll
           for (int j = 0; j < W; ++j) acc.v[j] = add_rn(acc.v[j], mul_rn(v, xs[u].v[j]));
+          if (q + u + U < cnt && valid > 0)
+            load_frag<T, W>(xs[u], dcol + (int64_t)nxt * ld_dense, valid);
         }
       }
     }
   }
-  if (valid == 0) return;
 
   if constexpr (EPI == kEpiBiasAct) {
+    if (valid == 0) return;
     if (epi.bias != nullptr) {
       const T b = epi.bias[row];
 #pragma unroll
@@ -129,90 +188,173 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 #pragma unroll
       for (int j = 0; j < W; ++j) acc.v[j] = relu_np(acc.v[j]);
     }
+    store_frag<T, W>(acc, out + row * ld_out + col0, valid);
   } else {
-    if (epi.mask != nullptr) {
-      Frag<T, W> mk;
-      load_frag<T, W>(mk, epi.mask + row * epi.ld_mask + col0, valid);
+    if (valid > 0) {
+      if (epi.mask != nullptr) {
+        Frag<T, W> mk;
+        load_frag<T, W>(mk, epi.mask + row * epi.ld_mask + col0, valid);
 #pragma unroll
-      for (int j = 0; j < W; ++j) acc.v[j] = mask_np(acc.v[j], mk.v[j]);
+        for (int j = 0; j < W; ++j) acc.v[j] = mask_np(acc.v[j], mk.v[j]);
+      }
+      store_frag<T, W>(acc, out + row * ld_out + col0, valid);
+    }
+    if (!epi.rowsum) return;
+    // whole row in this CTA: stage it, pairwise-sum it, update this row's bias
+    T* s_row = reinterpret_cast<T*>(smem_raw);
+    T* leaf_buf = s_row + ((n + 3) & ~int64_t(3));
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+      if (j < valid) s_row[col0 + j] = acc.v[j];
+    __syncthreads();
+    if (warp == 0) {
+      const T g = warp_pairwise_sum(s_row, (int)n, leaf_buf);
+      if (lane == 0) {
+        if (epi.rb_grad) epi.rb_grad[row] = g;
+        if (epi.opt.kind != SMB_OPT_NONE && epi.rb_bias) {
+          T dummy = T(0);
+          apply_update(epi.opt, g, epi.rb_bias + row, epi.rb_vbias ? epi.rb_vbias + row : &dummy);
+        }
+      }
     }
   }
-  store_frag<T, W>(acc, out + row * ld_out + col0, valid);
 }
 
+template <typename T, int W, int U, int EPI, bool PERM>
+bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm, const T* vals,
+                 int64_t n_rows, const T* dense, int64_t ld_dense, int64_t n, T* out,
+                 int64_t ld_out, EpiArgs<T> epi, cudaStream_t st) {
+  const int64_t chunks = ceil_div(n, 32 * W);
+  // The fused row-sum needs the whole row in one CTA; take that shape when
+  // there are enough rows to fill the GPU, else narrow CTAs (<= 8 warps) and
+  // the separate warp-per-row bias kernel.
+  const bool fuse = EPI == kEpiMask && epi.rowsum && n_rows >= 2 * 148 &&
+                    chunks <= max_threads_for<W>() / 32;
+  const int warps = fuse ? (int)chunks : (int)imin(8, chunks);
+  const int64_t gy = ceil_div(chunks, warps);
+  size_t dyn = 0;
+  if (fuse) dyn = sizeof(T) * (size_t)(((n + 3) & ~int64_t(3)) + warp_pairwise_leaves((int)n));
+  epi.rowsum = fuse ? 1 : 0;
+  auto kern = row_spmm_kernel<T, W, U, EPI, PERM>;
+  if (dyn > 40 * 1024)
+    ensure_smem(kern, dyn);
+  kern<<<dim3((unsigned)n_rows, (unsigned)gy), warps * 32, dyn, st>>>(
+      seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out, epi);
+  return epi.rowsum != 0;
+}
+
+// n_rows x n outputs; *rowsum_done tells whether the fused row-sum ran
 template <typename T, int EPI, bool PERM>
 int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm,
                         const T* vals, int64_t n_rows, const T* dense, int64_t ld_dense,
                         int64_t n, T* out, int64_t ld_out, EpiArgs<T> epi, cudaStream_t st,
-                        const char* name) {
+                        const char* name, bool* rowsum_done) {
+  if (rowsum_done) *rowsum_done = false;
   if (n_rows == 0 || n == 0) return SMB_OK;
   constexpr int VW = Vec16<T>::N;
   const bool vec_ok = aligned16(dense) && aligned16(out) && ld_dense % VW == 0 &&
                       ld_out % VW == 0 &&
                       (EPI != kEpiMask || epi.mask == nullptr ||
                        (aligned16(epi.mask) && epi.ld_mask % VW == 0));
-  // Wide vectors need enough warps to fill 148 SMs; with few rows or a
-  // narrow batch use one column per lane so the work spreads over more warps.
-  const bool wide = vec_ok && n_rows * ceil_div(n, 32 * VW) >= 148 * 16;
-  if (wide) {
-    const int64_t n_chunks = ceil_div(n, 32 * VW);
-    const int64_t warps = n_rows * n_chunks;
-    const int64_t blocks = ceil_div(warps, kWarpsPerBlock);
-    segment_spmm_kernel<T, VW, EPI, PERM><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, st>>>(
-        seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n, n_chunks, out, ld_out, epi);
-  } else {
-    const int64_t n_chunks = ceil_div(n, 32);
-    const int64_t warps = n_rows * n_chunks;
-    const int64_t blocks = ceil_div(warps, kWarpsPerBlock);
-    segment_spmm_kernel<T, 1, EPI, PERM><<<(unsigned)blocks, kWarpsPerBlock * 32, 0, st>>>(
-        seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n, n_chunks, out, ld_out, epi);
-  }
+  // The widest lanes (2 x 16 B, then 16 B) whose warp count still fills 148
+  // SMs: wider lanes amortise the per-nonzero index / shuffle / address work
+  // over more columns.  With few rows one column per lane spreads each row
+  // over many more warps.
+  auto enough = [&](int w) { return n >= 32 * w && n_rows * ceil_div(n, 32 * w) >= 148 * 8; };
+  bool done;
+  if (vec_ok && enough(2 * VW))
+    done = launch_rows<T, 2 * VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
+                                                n, out, ld_out, epi, st);
+  else if (vec_ok && enough(VW))
+    done = launch_rows<T, VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                            out, ld_out, epi, st);
+  else
+    done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                            out, ld_out, epi, st);
+  if (rowsum_done) *rowsum_done = done;
   return check_launch(name);
 }
 
-template <typename T>
-int spmm_impl(const int32_t* row_ptr, const int32_t* col_idx, const void* values, int64_t m,
-              int64_t k, const void* dense, int64_t ld_dense, int64_t n, const void* bias,
-              int epilogue, void* out, int64_t ld_out, void* stream) {
-  (void)k;
-  EpiArgs<T> epi{static_cast<const T*>(bias), epilogue == SMB_EPI_RELU, nullptr, 0};
-  return launch_segment_spmm<T, kEpiBiasAct, false>(
-      row_ptr, col_idx, nullptr, static_cast<const T*>(values), m, static_cast<const T*>(dense),
-      ld_dense, n, static_cast<T*>(out), ld_out, epi, as_stream(stream), "smb_spmm");
-}
-
-template <typename T>
-int spmm_t_impl(const int32_t* col_ptr, const int32_t* row_idx, const int32_t* perm,
-                const void* values, int64_t m, int64_t k, const void* dense, int64_t ld_dense,
-                int64_t n, const void* mask, int64_t ld_mask, void* out, int64_t ld_out,
-                void* stream) {
-  (void)m;
-  EpiArgs<T> epi{nullptr, 0, static_cast<const T*>(mask), ld_mask};
-  return launch_segment_spmm<T, kEpiMask, true>(
-      col_ptr, row_idx, perm, static_cast<const T*>(values), k, static_cast<const T*>(dense),
-      ld_dense, n, static_cast<T*>(out), ld_out, epi, as_stream(stream), "smb_spmm_t");
-}
-
 }  // namespace
+
+// warp-per-row reduction + bias update (elementwise.cu), used when the fused
+// epilogue cannot cover a row (batches wider than 32 warps x 32 x W columns)
+template <typename T>
+int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias, T* grad,
+                     const OptConsts<T>& opt, cudaStream_t st);
+
+template <typename T>
+int spmm_t_fused_impl(const smb_pattern* pat, const void* values, const void* dense,
+                      int64_t ld_dense, int64_t n, const void* mask, int64_t ld_mask, void* out,
+                      int64_t ld_out, void* bias, void* vbias, void* grad_bias_out, int opt_kind,
+                      double mu, double eta, void* stream) {
+  const bool want_rows =
+      grad_bias_out != nullptr || (opt_kind != SMB_OPT_NONE && bias != nullptr);
+  EpiArgs<T> epi{};
+  epi.mask = static_cast<const T*>(mask);
+  epi.ld_mask = ld_mask;
+  epi.rowsum = want_rows ? 1 : 0;
+  epi.rb_bias = static_cast<T*>(bias);
+  epi.rb_vbias = static_cast<T*>(vbias);
+  epi.rb_grad = static_cast<T*>(grad_bias_out);
+  epi.opt = make_opt<T>(opt_kind, mu, eta);
+  bool done = false;
+  cudaStream_t st = as_stream(stream);
+  int rc = launch_segment_spmm<T, kEpiMask, true>(
+      pat->col_ptr, pat->row_idx, pat->perm, static_cast<const T*>(values), pat->k,
+      static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi, st,
+      "smb_spmm_t", &done);
+  if (rc != SMB_OK || !want_rows || done) return rc;
+  return launch_bias_rows<T>(static_cast<const T*>(out), ld_out, pat->k, n, epi.rb_bias,
+                             epi.rb_vbias, epi.rb_grad, epi.opt, st);
+}
+
 }  // namespace smb
 
 using namespace smb;
+
+namespace {
+template <typename T>
+int spmm_impl(const int32_t* row_ptr, const int32_t* col_idx, const void* values, int64_t m,
+              const void* dense, int64_t ld_dense, int64_t n, const void* bias, int epilogue,
+              void* out, int64_t ld_out, void* stream) {
+  EpiArgs<T> epi{};
+  epi.bias = static_cast<const T*>(bias);
+  epi.relu = epilogue == SMB_EPI_RELU;
+  return launch_segment_spmm<T, kEpiBiasAct, false>(
+      row_ptr, col_idx, nullptr, static_cast<const T*>(values), m, static_cast<const T*>(dense),
+      ld_dense, n, static_cast<T*>(out), ld_out, epi, as_stream(stream), "smb_spmm", nullptr);
+}
+
+int spmm_t_checks(const smb_pattern* pat, int64_t ld_dense, int64_t n, const void* mask,
+                  int64_t ld_mask, void* out, int64_t ld_out) {
+  SMB_REQUIRE(pat != nullptr, "smb_spmm_t: null pattern");
+  SMB_REQUIRE(n >= 0, "smb_spmm_t: negative dimension");
+  SMB_REQUIRE(ld_dense >= n && ld_out >= n, "smb_spmm_t: leading dimension smaller than n");
+  SMB_REQUIRE(mask == nullptr || ld_mask >= n, "smb_spmm_t: mask leading dimension");
+  SMB_REQUIRE(pat->k == 0 || out != nullptr, "smb_spmm_t: null output");
+  SMB_REQUIRE(pat->k < (int64_t(1) << 31), "smb_spmm_t: too many columns");
+  return SMB_OK;
+}
+}  // namespace
 
 extern "C" int smb_spmm(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
                         const void* values, int64_t m, int64_t k, const void* dense,
                         int64_t ld_dense, int64_t n, const void* bias, int epilogue, void* out,
                         int64_t ld_out, void* stream) {
   clear_error();
+  (void)k;
   SMB_REQUIRE(m >= 0 && k >= 0 && n >= 0, "smb_spmm: negative dimension");
   SMB_REQUIRE(ld_dense >= n && ld_out >= n, "smb_spmm: leading dimension smaller than n");
   SMB_REQUIRE(epilogue == SMB_EPI_NONE || epilogue == SMB_EPI_RELU, "smb_spmm: bad epilogue %d",
               epilogue);
   SMB_REQUIRE(m == 0 || (row_ptr && out), "smb_spmm: null pointer");
+  SMB_REQUIRE(m < (int64_t(1) << 31), "smb_spmm: too many rows");
   if (dtype == SMB_F32)
-    return spmm_impl<float>(row_ptr, col_idx, values, m, k, dense, ld_dense, n, bias, epilogue,
-                            out, ld_out, stream);
+    return spmm_impl<float>(row_ptr, col_idx, values, m, dense, ld_dense, n, bias, epilogue, out,
+                            ld_out, stream);
   if (dtype == SMB_F64)
-    return spmm_impl<double>(row_ptr, col_idx, values, m, k, dense, ld_dense, n, bias, epilogue,
+    return spmm_impl<double>(row_ptr, col_idx, values, m, dense, ld_dense, n, bias, epilogue,
                              out, ld_out, stream);
   set_error("smb_spmm: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
@@ -222,17 +364,39 @@ extern "C" int smb_spmm_t(int dtype, const smb_pattern* pat, const void* values,
                           const void* dense, int64_t ld_dense, int64_t n, const void* mask,
                           int64_t ld_mask, void* out, int64_t ld_out, void* stream) {
   clear_error();
-  SMB_REQUIRE(pat != nullptr, "smb_spmm_t: null pattern");
-  SMB_REQUIRE(n >= 0, "smb_spmm_t: negative dimension");
-  SMB_REQUIRE(ld_dense >= n && ld_out >= n, "smb_spmm_t: leading dimension smaller than n");
-  SMB_REQUIRE(mask == nullptr || ld_mask >= n, "smb_spmm_t: mask leading dimension");
-  SMB_REQUIRE(pat->k == 0 || out != nullptr, "smb_spmm_t: null output");
+  const int rc = spmm_t_checks(pat, ld_dense, n, mask, ld_mask, out, ld_out);
+  if (rc != SMB_OK) return rc;
   if (dtype == SMB_F32)
-    return spmm_t_impl<float>(pat->col_ptr, pat->row_idx, pat->perm, values, pat->m, pat->k,
-                              dense, ld_dense, n, mask, ld_mask, out, ld_out, stream);
+    return spmm_t_fused_impl<float>(pat, values, dense, ld_dense, n, mask, ld_mask, out, ld_out,
+                                    nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0, stream);
   if (dtype == SMB_F64)
-    return spmm_t_impl<double>(pat->col_ptr, pat->row_idx, pat->perm, values, pat->m, pat->k,
-                               dense, ld_dense, n, mask, ld_mask, out, ld_out, stream);
+    return spmm_t_fused_impl<double>(pat, values, dense, ld_dense, n, mask, ld_mask, out, ld_out,
+                                     nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0, stream);
   set_error("smb_spmm_t: unsupported dtype %d", dtype);
+  return SMB_ERR_INVALID;
+}
+
+extern "C" int smb_spmm_t_bias(int dtype, const smb_pattern* pat, const void* values,
+                               const void* dense, int64_t ld_dense, int64_t n, const void* mask,
+                               int64_t ld_mask, void* out, int64_t ld_out, void* bias,
+                               void* velocity_bias, void* grad_bias_out, int opt_kind, double mu,
+                               double eta, void* stream) {
+  clear_error();
+  const int rc = spmm_t_checks(pat, ld_dense, n, mask, ld_mask, out, ld_out);
+  if (rc != SMB_OK) return rc;
+  SMB_REQUIRE(opt_kind >= SMB_OPT_NONE && opt_kind <= SMB_OPT_NESTEROV,
+              "smb_spmm_t_bias: bad optimizer kind %d", opt_kind);
+  SMB_REQUIRE(!(opt_kind == SMB_OPT_MOMENTUM || opt_kind == SMB_OPT_NESTEROV) ||
+                  bias == nullptr || velocity_bias != nullptr,
+              "smb_spmm_t_bias: momentum needs a bias velocity buffer");
+  if (dtype == SMB_F32)
+    return spmm_t_fused_impl<float>(pat, values, dense, ld_dense, n, mask, ld_mask, out, ld_out,
+                                    bias, velocity_bias, grad_bias_out, opt_kind, mu, eta,
+                                    stream);
+  if (dtype == SMB_F64)
+    return spmm_t_fused_impl<double>(pat, values, dense, ld_dense, n, mask, ld_mask, out, ld_out,
+                                     bias, velocity_bias, grad_bias_out, opt_kind, mu, eta,
+                                     stream);
+  set_error("smb_spmm_t_bias: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
 }

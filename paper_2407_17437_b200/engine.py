@@ -6,9 +6,10 @@ of the reference's per-batch loop (train.py:389-402):
     gather      xb = Xtrain[:, batch], tb = Ttrain[:, batch]    smb_gather_columns
     forward     a_l = relu(W_l a_{l-1} + b_l)                   smb_spmm (bias+ReLU fused)
     loss grad   d_L = (softmax(y) - t) / B                      smb_softmax_ce_grad
-    backward    d_{l-1} = (W_l^T d_l) * (a_{l-1} > 0)           smb_spmm_t (mask fused)
-                grad_l = sddmm(d_l, a_{l-1}); update W_l, b_l   smb_sddmm_update (fused)
-    next batch  step counter += 1                               smb_step_counter_advance
+    backward    d_{l-1} = (W_l^T d_l) * (a_{l-1} > 0)           smb_spmm_t_bias (mask fused,
+                + row_sums(d_{l-1}), update b_{l-1}              + bias side of layer l-1)
+                grad_l = sddmm(d_l, a_{l-1}); update W_l        smb_sddmm_update (fused)
+    next batch  step counter += 1                               (softmax kernel's last CTA)
 
 spmm_t of layer l runs before the update of layer l (pre-update weights,
 train.py:400-401).  The layer-1 input gradient is never computed: the
@@ -35,17 +36,78 @@ from .errors import ConfigurationError, InvalidArgumentError
 from .nn import ActivationLayer, DenseLinearLayer, ReLU, SparseLinearLayer, optimizer_kind
 from .tensor_core import _no_tf32, ptr, stream_ptr
 
-__all__ = ["FusedTrainStep"]
+__all__ = ["FusedTrainStep", "KernelTimer"]
+
+
+class KernelTimer:
+    """CUDA-event spans around individual launches on the launching stream."""
+
+    def __init__(self):
+        self.records = []  # (tag, start_event, end_event)
+
+    @staticmethod
+    def hold_gpu(cycles: int = 40_000_000) -> None:
+        """Enqueue a spin kernel so the host can enqueue a whole step before the
+        GPU reaches it: the spans then time kernels, not host launch gaps."""
+        torch.cuda._sleep(cycles)
+
+    def span(self, tag):
+        timer = self
+
+        class _Span:
+            def __enter__(self):
+                self.s = torch.cuda.Event(enable_timing=True)
+                self.e = torch.cuda.Event(enable_timing=True)
+                self.s.record()
+
+            def __exit__(self, *exc):
+                self.e.record()
+                timer.records.append((tag, self.s, self.e))
+
+        return _Span()
+
+    def summary(self):
+        """{tag: (count, total_ms)} after synchronising."""
+        torch.cuda.synchronize()
+        out = {}
+        for tag, s, e in self.records:
+            c, t = out.get(tag, (0, 0.0))
+            out[tag] = (c + 1, t + s.elapsed_time(e))
+        return out
 
 
 def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
 
-class _Unit:
-    __slots__ = ("layer", "relu", "sparse", "m", "k", "grad_off", "bias_off", "nvals")
+def shard_epoch(perm, global_batch: int, local_batch: int, rank_offset: int):
+    """This rank's sample order for one epoch, laid out so its batch k is
+    entries [k*local_batch, (k+1)*local_batch): the columns
+    [rank_offset, rank_offset + local_batch) of every global batch of the
+    shuffled order (K = N // global_batch batches; the partial batch is
+    dropped like train.py:389).  Returns (int32 indices, K)."""
+    p = np.ascontiguousarray(perm, dtype=np.int64)
+    if not 0 <= rank_offset <= global_batch - local_batch:
+        raise InvalidArgumentError("rank slice outside the global batch")
+    kb = p.shape[0] // global_batch
+    idx = p[: kb * global_batch].reshape(kb, global_batch)[:, rank_offset:rank_offset + local_batch]
+    return np.ascontiguousarray(idx.reshape(-1)).astype(np.int32), kb
 
-    def __init__(self, layer, relu):
+
+def flat_layout(units):
+    """Offsets of the data-parallel gradient buffer: per layer [values | bias]."""
+    off, layout = 0, []
+    for m, nvals in units:
+        layout.append((off, off + nvals))
+        off += nvals + m
+    return layout, off
+
+
+class _Unit:
+    __slots__ = ("layer", "relu", "sparse", "m", "k", "grad_off", "bias_off", "nvals", "index")
+
+    def __init__(self, layer, relu, index=0):
+        self.index = index
         self.layer = layer
         self.relu = relu
         self.sparse = isinstance(layer, SparseLinearLayer)
@@ -83,23 +145,28 @@ class FusedTrainStep:
         self.dys = [torch.zeros((u.m, ld), dtype=f32, device=dev) for u in self.units]
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws = int(_lib.load().smb_softmax_ce_workspace_bytes(self.B))
+        self._ce_ws = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self.perm = None
         self.data = None
         self.steps_per_epoch = 0
-        # scratch for dense layers' bias gradient
-        self._dense_gb = {id(u): torch.zeros(u.m, dtype=f32, device=dev)
-                          for u in self.units if not u.sparse}
         # data-parallel flat gradient buffer: [values | bias] per layer
         self.flat = None
         if self.world > 1:
-            off = 0
-            for u in self.units:
-                u.grad_off = off
-                off += u.nvals
-                u.bias_off = off
-                off += u.m
-            self.flat = torch.zeros(off, dtype=f32, device=dev)
+            layout, total = flat_layout([(u.m, u.nvals) for u in self.units])
+            for u, (g_off, b_off) in zip(self.units, layout):
+                u.grad_off, u.bias_off = g_off, b_off
+            self.flat = torch.zeros(total, dtype=f32, device=dev)
         self._graphs = {}
+        self.timer = None  # optional KernelTimer: per-launch CUDA events (eager only)
+
+    def _call(self, tag: str, name: str, *args) -> None:
+        t = self.timer
+        if t is None:
+            _lib.call(name, *args)
+            return
+        with t.span(tag):
+            _lib.call(name, *args)
 
     # ------------------------------------------------------------------
     @staticmethod
@@ -122,7 +189,7 @@ class FusedTrainStep:
                 i += 1
             if lay.weights.dtype not in (np.float32, torch.float32):
                 raise ConfigurationError("fused step runs float32 models")
-            units.append(_Unit(lay, relu))
+            units.append(_Unit(lay, relu, len(units)))
             i += 1
         if not units:
             raise ConfigurationError("model has no linear layers")
@@ -139,11 +206,8 @@ class FusedTrainStep:
     def set_epoch(self, perm: np.ndarray, rank_offset: int = 0) -> None:
         """Upload the epoch's sample order; this rank's batch k is
         perm[k*B_global + rank_offset : ... + B]."""
-        p = np.ascontiguousarray(perm, dtype=np.int64)
-        kb = p.shape[0] // self.B_global
-        # lay the rank's slices out contiguously so batch k starts at k*B
-        idx = p[: kb * self.B_global].reshape(kb, self.B_global)[:, rank_offset:rank_offset + self.B]
-        flat = torch.from_numpy(np.ascontiguousarray(idx.reshape(-1)).astype(np.int32))
+        idx, kb = shard_epoch(perm, self.B_global, self.B, rank_offset)
+        flat = torch.from_numpy(idx)
         if self.perm is None or self.perm.numel() != flat.numel():
             self.perm = torch.empty(flat.numel(), dtype=torch.int32, device=self.dev)
             self._graphs.clear()
@@ -152,34 +216,52 @@ class FusedTrainStep:
         self.steps_per_epoch = kb
 
     # ------------------------------------------------------------------
+    def _bias_target(self, u, fuse_update: bool):
+        """(bias, velocity_bias, grad_bias_out, opt_kind, mu) for unit u's bias side."""
+        lay = u.layer
+        opt = lay.optimizer
+        if fuse_update:
+            return (ptr(lay.bias), ptr(lay.velocity_bias), None, optimizer_kind(opt),
+                    float(opt.mu))
+        return (None, None, ptr(self.flat[u.bias_off:u.bias_off + u.m]), _lib.SMB_OPT_NONE,
+                float(opt.mu))
+
     def _launch_forward_backward(self, eta: float, fuse_update: bool, gather: bool) -> None:
         st = stream_ptr()
         B, ld = self.B, self.ld
         F32 = _lib.SMB_F32
         if gather:
             d = self.data
-            _lib.call("smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features, ptr(self.perm),
-                      ptr(self.counter), 0, B, ptr(self.x_in), ld, st)
-            _lib.call("smb_gather_columns", F32, ptr(d.T), d.n_samples, d.classes, ptr(self.perm),
-                      ptr(self.counter), 0, B, ptr(self.t_in), ld, st)
-        # forward
+            self._call("gather", "smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features,
+                       ptr(self.perm), ptr(self.counter), 0, B, ptr(self.x_in), ld, st)
+            self._call("gather", "smb_gather_columns", F32, ptr(d.T), d.n_samples, d.classes,
+                       ptr(self.perm), ptr(self.counter), 0, B, ptr(self.t_in), ld, st)
+        # forward: a_l = act(W_l a_{l-1} + b_l)
         x = self.x_in
-        for u, a in zip(self.units, self.acts):
+        for li, (u, a) in enumerate(zip(self.units, self.acts)):
             lay = u.layer
             if u.sparse:
-                _lib.call("smb_spmm", F32, ptr(lay.weights.row_ptr), ptr(lay.weights.col_idx),
-                          ptr(lay.weights.values), u.m, u.k, ptr(x), ld, B, ptr(lay.bias),
-                          _lib.SMB_EPI_RELU if u.relu else _lib.SMB_EPI_NONE, ptr(a), ld, st)
+                self._call(f"spmm[{li}]", "smb_spmm", F32, ptr(lay.weights.row_ptr),
+                           ptr(lay.weights.col_idx), ptr(lay.weights.values), u.m, u.k, ptr(x), ld,
+                           B, ptr(lay.bias), _lib.SMB_EPI_RELU if u.relu else _lib.SMB_EPI_NONE,
+                           ptr(a), ld, st)
             else:
                 with _no_tf32():
                     torch.addmm(lay.bias[:, None], lay.weights, x[:, :B], out=a[:, :B])
                 if u.relu:
-                    _lib.call("smb_relu", F32, ptr(a), ld, u.m, B, ptr(a), ld, st)
+                    self._call(f"relu[{li}]", "smb_relu", F32, ptr(a), ld, u.m, B, ptr(a), ld, st)
             x = a
-        # loss gradient (softmax CE), scaled by 1/B_global
-        _lib.call("smb_softmax_ce_grad", F32, ptr(self.acts[-1]), ld, ptr(self.t_in), ld,
-                  self.classes, B, float(self.B_global), ptr(self.dys[-1]), ld, ptr(self.loss), st)
-        # backward, last layer first
+        # loss gradient (softmax CE) scaled by 1/B_global; the same launch
+        # applies the last layer's bias side and advances the step counter
+        top = self.units[-1]
+        b, vb, gb, kind, mu = self._bias_target(top, fuse_update)
+        self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
+                   ptr(self.t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]), ld,
+                   ptr(self.loss), b, vb, gb, kind, mu, float(eta),
+                   ptr(self.counter) if gather else None, int(self.steps_per_epoch),
+                   ptr(self._ce_ws), st)
+        # backward, last layer first: d_{l-1} (+ bias side of layer l-1), then
+        # the weight side of layer l (spmm_t reads the pre-update W_l)
         for li in range(len(self.units) - 1, -1, -1):
             u = self.units[li]
             lay = u.layer
@@ -188,17 +270,21 @@ class FusedTrainStep:
             if li > 0:
                 below = self.units[li - 1]
                 mask = self.acts[li - 1] if below.relu else None
+                dst = self.dys[li - 1]
+                b, vb, gb, kind, mu = self._bias_target(below, fuse_update)
                 if u.sparse:
-                    _lib.call("smb_spmm_t", F32, lay.weights.pattern.handle, ptr(lay.weights.values),
-                              ptr(dy), ld, B, ptr(mask), ld if mask is not None else 0,
-                              ptr(self.dys[li - 1]), ld, st)
+                    self._call(f"spmm_t[{li}]", "smb_spmm_t_bias", F32, lay.weights.pattern.handle,
+                               ptr(lay.weights.values), ptr(dy), ld, B, ptr(mask),
+                               ld if mask is not None else 0, ptr(dst), ld, b, vb, gb, kind, mu,
+                               float(eta), st)
                 else:
-                    dst = self.dys[li - 1]
                     with _no_tf32():
                         torch.mm(lay.weights.T, dy[:, :B], out=dst[:, :B])
                     if mask is not None:
-                        _lib.call("smb_relu_backward", F32, ptr(dst), ld, ptr(mask), ld, u.k, B,
-                                  ptr(dst), ld, st)
+                        self._call(f"relu_bwd[{li}]", "smb_relu_backward", F32, ptr(dst), ld,
+                                   ptr(mask), ld, u.k, B, ptr(dst), ld, st)
+                    self._call(f"bias[{li - 1}]", "smb_bias_grad_update", F32, ptr(dst), ld, u.k,
+                               B, b, vb, gb, kind, mu, float(eta), st)
             self._weight_side(u, dy, x_prev, eta, fuse_update, st)
 
     def _weight_side(self, u, dy, x_prev, eta, fuse_update, st):
@@ -210,33 +296,20 @@ class FusedTrainStep:
         if u.sparse:
             vel = lay.velocity.values if lay.velocity is not None else None
             g_out = None if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals]
-            gb_out = None if fuse_update else self.flat[u.bias_off:u.bias_off + u.m]
-            _lib.call("smb_sddmm_update", F32, lay.weights.pattern.handle, ptr(dy), ld, ptr(x_prev),
-                      ld, B, ptr(lay.weights.values), ptr(vel), ptr(g_out), ptr(lay.bias),
-                      ptr(lay.velocity_bias), ptr(gb_out), kind, float(opt.mu), float(eta), st)
+            self._call(f"sddmm_update[{u.index}]", "smb_sddmm_update", F32,
+                       lay.weights.pattern.handle, ptr(dy), ld, ptr(x_prev), ld, B,
+                       ptr(lay.weights.values), ptr(vel), ptr(g_out), None, None, None, kind,
+                       float(opt.mu), float(eta), st)
             return
-        # dense layer: cuBLAS gradient, exact pairwise bias sum, exact update
-        if fuse_update:
-            gw = lay.grad
-            gb = self._dense_gb[id(u)]
-        else:
-            gw = self.flat[u.grad_off:u.grad_off + u.nvals].view(u.m, u.k)
-            gb = self.flat[u.bias_off:u.bias_off + u.m]
+        # dense layer: cuBLAS FP32 weight gradient + exact update
+        gw = lay.grad if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals].view(u.m, u.k)
         with _no_tf32():
             torch.mm(dy[:, :B], x_prev[:, :B].T, out=gw)
-        _lib.call("smb_row_sums", F32, ptr(dy), u.m, B, ld, ptr(gb), st)
         if fuse_update:
-            self._dense_update(u, gw, gb, eta, st)
-
-    def _dense_update(self, u, gw, gb, eta, st):
-        lay = u.layer
-        opt = lay.optimizer
-        kind = optimizer_kind(opt)
-        vel = lay.velocity.view(-1) if lay.velocity is not None else None
-        _lib.call("smb_optimizer_step", _lib.SMB_F32, ptr(lay.weights), ptr(vel), ptr(gw),
-                  u.nvals, kind, float(opt.mu), float(eta), st)
-        _lib.call("smb_optimizer_step", _lib.SMB_F32, ptr(lay.bias), ptr(lay.velocity_bias),
-                  ptr(gb), u.m, kind, float(opt.mu), float(eta), st)
+            vel = lay.velocity.view(-1) if lay.velocity is not None else None
+            self._call(f"update[{u.index}]", "smb_optimizer_step", F32, ptr(lay.weights),
+                       ptr(vel), ptr(gw), u.nvals, optimizer_kind(opt), float(opt.mu), float(eta),
+                       st)
 
     def _launch_updates_from_flat(self, eta: float) -> None:
         st = stream_ptr()
@@ -247,29 +320,25 @@ class FusedTrainStep:
             g = self.flat[u.grad_off:u.grad_off + u.nvals]
             gb = self.flat[u.bias_off:u.bias_off + u.m]
             if u.sparse:
+                vals = lay.weights.values
                 vel = lay.velocity.values if lay.velocity is not None else None
-                _lib.call("smb_optimizer_step", _lib.SMB_F32, ptr(lay.weights.values), ptr(vel),
-                          ptr(g), u.nvals, kind, float(opt.mu), float(eta), st)
-                _lib.call("smb_optimizer_step", _lib.SMB_F32, ptr(lay.bias), ptr(lay.velocity_bias),
-                          ptr(gb), u.m, kind, float(opt.mu), float(eta), st)
             else:
-                self._dense_update(u, g.view(u.m, u.k), gb, eta, st)
-
-    def _advance(self, gather: bool) -> None:
-        if gather:
-            _lib.call("smb_step_counter_advance", ptr(self.counter), int(self.steps_per_epoch),
-                      stream_ptr())
+                vals = lay.weights
+                vel = lay.velocity.view(-1) if lay.velocity is not None else None
+            self._call(f"update[{u.index}]", "smb_optimizer_step", _lib.SMB_F32, ptr(vals),
+                       ptr(vel), ptr(g), u.nvals, kind, float(opt.mu), float(eta), st)
+            self._call(f"update_bias[{u.index}]", "smb_optimizer_step", _lib.SMB_F32,
+                       ptr(lay.bias), ptr(lay.velocity_bias), ptr(gb), u.m, kind, float(opt.mu),
+                       float(eta), st)
 
     # ------------------------------------------------------------------
     def _run_eager(self, eta: float, gather: bool, part: str) -> None:
         if self.world == 1:
             self._launch_forward_backward(eta, True, gather)
-            self._advance(gather)
         elif part == "fb":
             self._launch_forward_backward(eta, False, gather)
         else:
             self._launch_updates_from_flat(eta)
-            self._advance(gather)
 
     def _graph(self, eta: float, gather: bool, part: str):
         key = (float(eta), gather, part)
@@ -313,6 +382,25 @@ class FusedTrainStep:
             self._graph(eta, gather, part)
             return
         self._graphs[key].replay()
+
+    def train_batch(self, xb, tb, eta: float, loss_out=None) -> None:
+        """One step on a host-supplied batch (the reference's per-batch call
+        sequence, train.py:398-401): xb [features, B] and tb [classes, B]
+        (ideally pinned host tensors) are copied into the device input
+        buffers on the current stream, the captured step runs, and the batch
+        loss is copied into `loss_out` (a pinned float64 host tensor) when
+        given.  Stream-ordered; nothing synchronises."""
+        B = self.B
+        x_dst = self.x_in[:, :B]
+        t_dst = self.t_in[:, :B]
+        if tuple(xb.shape) != tuple(x_dst.shape) or tuple(tb.shape) != tuple(t_dst.shape):
+            raise InvalidArgumentError(
+                f"expected batch shapes {tuple(x_dst.shape)} / {tuple(t_dst.shape)}")
+        x_dst.copy_(torch.as_tensor(xb), non_blocking=True)
+        t_dst.copy_(torch.as_tensor(tb), non_blocking=True)
+        self.step(eta, gather=False)
+        if loss_out is not None:
+            loss_out.copy_(self.loss, non_blocking=True)
 
     def loss_value(self) -> float:
         """Summed softmax-CE loss of the last step's local batch (syncs)."""

@@ -1,0 +1,80 @@
+"""Config-3 kernel microbenchmark (BASELINE.json configs[2]): W 8192x8192 CSR,
+uniform pattern (sample_pattern from Rng(seed).stream("pattern")), values and
+X / dY ~ N(0,1) fp32, B in {128, 512, 2048}.  Times forward SpMM, transposed
+SpMM and SDDMM + Nesterov update separately with CUDA events on the
+launching stream, flushing L2 (a 512 MB write) before every timed launch.
+Prints one JSON object per (density, B) with achieved algorithmic GB/s
+(SURVEY.md 8(d) byte model) and pair rates."""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+
+import paper_2407_17437_b200 as smb
+from paper_2407_17437_b200 import _lib
+from paper_2407_17437_b200.tensor_core import ptr, stream_ptr
+
+HBM = 6446.6  # GB/s, MEASURED_PEAKS.json hbm_gbs
+
+
+def bytes_model(m, k, z, B):
+    spmm = 4 * (m + 1) + 8 * z + 4 * k * B + 4 * m + 4 * m * B
+    spmm_t = 4 * (k + 1) + 8 * z + 4 * m * B + 4 * k * B + 4 * k * B
+    sddmm = 4 * (m + 1) + 4 * z + 4 * m * B + 4 * k * B + 16 * z + 16 * m
+    return spmm, spmm_t, sddmm
+
+
+def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
+    dev = torch.device("cuda")
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)
+    n = 8192
+    for d in densities:
+        nnz = int(round(d * n * n))
+        pat = smb.sample_pattern(n, n, nnz, smb.Rng(0).stream("pattern"))
+        rng = np.random.default_rng(1)
+        vals = torch.from_numpy(rng.standard_normal(nnz).astype(np.float32)).to(dev)
+        vel = torch.zeros_like(vals)
+        for B in batches:
+            X = torch.randn(n, B, device=dev)
+            dY = torch.randn(n, B, device=dev)
+            out = torch.empty(n, B, device=dev)
+            res = {}
+
+            def launch(kind):
+                st = stream_ptr()
+                if kind == "spmm":
+                    _lib.call("smb_spmm", 0, ptr(pat.row_ptr), ptr(pat.col_idx), ptr(vals), n, n,
+                              ptr(X), B, B, None, 0, ptr(out), B, st)
+                elif kind == "spmm_t":
+                    _lib.call("smb_spmm_t", 0, pat.handle, ptr(vals), ptr(dY), B, B, None, 0,
+                              ptr(out), B, st)
+                else:
+                    _lib.call("smb_sddmm_update", 0, pat.handle, ptr(dY), B, ptr(X), B, B,
+                              ptr(vals), ptr(vel), None, None, None, None, 3, 0.9, 1e-6, st)
+
+            for kind in ("spmm", "spmm_t", "sddmm_update"):
+                times = []
+                for it in range(iters + 2):
+                    flush.fill_(it)
+                    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s.record()
+                    launch(kind)
+                    e.record()
+                    e.synchronize()
+                    if it >= 2:
+                        times.append(s.elapsed_time(e) * 1e3)
+                res[kind] = float(np.median(times))
+            bs = bytes_model(n, n, nnz, B)
+            rec = {"density": d, "nnz": nnz, "B": B}
+            for (kind, us), b in zip(res.items(), bs):
+                rec[kind] = {"us": round(us, 2), "GB/s": round(b / us / 1e3, 1),
+                             "frac_hbm": round(b / us / 1e3 / HBM, 3),
+                             "Gpairs/s": round(nnz * B / us / 1e3, 1)}
+            print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,273 @@
+"""Kernel parity on the GPU: every exact kernel must be BIT-IDENTICAL to the
+CPU oracle (itself pinned to the reference in test_oracle_golden.py) on the
+same seeded inputs -- random instances in the reference tests' shapes
+(pkg/tests/test_tensor_core.py:96-182) plus the edge cases it covers (empty
+pattern, empty rows, single nonzero, n = 0/1, odd n, fp64)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bits_equal, random_csr, rel_err
+
+pytestmark = pytest.mark.gpu
+
+import paper_2407_17437_b200 as smb  # noqa: E402
+from paper_2407_17437_b200 import tensor_core as tc  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+SHAPES = [(1, 1, 1), (2, 3, 4), (17, 13, 5), (40, 33, 37), (64, 96, 100), (129, 257, 128),
+          (300, 200, 1), (512, 1024, 130), (1000, 700, 257)]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("density", [0.05, 0.3, 1.0])
+def test_spmm_bit_exact(oracle, dtype, shape, density):
+    m, k, n = shape
+    rng = np.random.default_rng(hash((m, k, n, density)) % 2**32)
+    rp, ci, v, dense = random_csr(rng, m, k, density, dtype, empty_rows=True)
+    x = rng.standard_normal((k, n)).astype(dtype)
+    s = smb.CsrMatrix(m, k, rp, ci, v)
+    got = smb.spmm(s, x)
+    want = oracle.spmm(rp, ci, v, x)
+    assert bits_equal(got, want)
+    # the reference's fp64-oracle tolerance holds for its own shape range (<= 40)
+    tol = (1e-5 if dtype == np.float32 else 1e-12) * (1 if max(m, k) <= 40 else 10)
+    assert rel_err(got, dense.astype(np.float64) @ x) <= tol
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("density", [0.05, 0.3, 1.0])
+def test_spmm_transposed_bit_exact(oracle, dtype, shape, density):
+    m, k, n = shape
+    rng = np.random.default_rng(1 + hash((m, k, n, density)) % 2**32)
+    rp, ci, v, dense = random_csr(rng, m, k, density, dtype, empty_rows=True)
+    d = rng.standard_normal((m, n)).astype(dtype)
+    s = smb.CsrMatrix(m, k, rp, ci, v)
+    got = smb.spmm_transposed(s, d)
+    want = oracle.spmm_t(rp, ci, v, k, d)
+    assert bits_equal(got, want)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("density", [0.05, 0.3, 1.0])
+def test_sddmm_bit_exact(oracle, dtype, shape, density):
+    m, k, n = shape
+    rng = np.random.default_rng(2 + hash((m, k, n, density)) % 2**32)
+    rp, ci, v, _ = random_csr(rng, m, k, density, dtype, empty_rows=True)
+    a = rng.standard_normal((m, n)).astype(dtype)
+    b = rng.standard_normal((k, n)).astype(dtype)
+    pat = smb.SparsityPattern(m, k, rp, ci)
+    got = host(smb.sddmm(pat, dev(a), dev(b)).values)
+    want = oracle.sddmm(rp, ci, a, b)
+    assert bits_equal(got, want)
+
+
+def test_sddmm_zero_batch_gives_zeros():
+    pat = smb.csr_from_dense(np.ones((3, 4), dtype=np.float32)).pattern
+    out = smb.sddmm(pat, torch.zeros((3, 0), device="cuda"), torch.zeros((4, 0), device="cuda"))
+    assert torch.count_nonzero(out.values) == 0
+
+
+def test_sddmm_many_empty_rows_window_fallback(oracle):
+    # > 128 rows inside one 128-nonzero tile exercises the global row search
+    m, k, n = 5000, 64, 9
+    rng = np.random.default_rng(7)
+    counts = np.zeros(m, dtype=np.int64)
+    counts[rng.choice(m, size=40, replace=False)] = rng.integers(1, 8, size=40)
+    rp = np.zeros(m + 1, dtype=np.int32)
+    np.cumsum(counts, out=rp[1:])
+    ci = np.concatenate([np.sort(rng.choice(k, size=c, replace=False)) for c in counts if c]).astype(np.int32)
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float32)
+    got = host(smb.sddmm(smb.SparsityPattern(m, k, rp, ci), dev(a), dev(b)).values)
+    assert bits_equal(got, oracle.sddmm(rp, ci, a, b))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_sparse_combine_bit_exact(oracle, dtype):
+    rng = np.random.default_rng(55)
+    rp, ci, v, _ = random_csr(rng, 90, 70, 0.4, dtype)
+    t = rng.standard_normal(v.shape[0]).astype(dtype)
+    for alpha, beta in [(0.9, 1.0), (1.0, -0.05 * 0.9), (1.0, -0.05), (0.3, 0.7)]:
+        s = smb.CsrMatrix(90, 70, rp, ci, v.copy())
+        smb.sparse_combine(alpha, s, beta, s.pattern.with_values(t))
+        want = v.copy()
+        oracle.axpby(alpha, want, beta, t)
+        assert bits_equal(host(s.values), want)
+
+
+def test_hand_values():
+    # pkg/tests/test_tensor_core.py:81-84, 113-120, 144-150
+    s = smb.CsrMatrix(2, 2, np.array([0, 1, 2]), np.array([0, 1]), np.array([1.0, 2.0], np.float32))
+    b = np.array([[1, 2], [3, 4]], dtype=np.float32)
+    assert np.array_equal(smb.spmm(s, b), [[1, 2], [6, 8]])
+    assert np.array_equal(smb.spmm_transposed(s, b), [[1, 2], [6, 8]])
+    s1 = smb.CsrMatrix(1, 2, np.array([0, 1]), np.array([1]), np.array([3.0], np.float32))
+    assert np.array_equal(smb.spmm_transposed(s1, np.array([[5.0, 7.0]], np.float32)),
+                          [[0, 0], [15, 21]])
+    pat = smb.SparsityPattern(1, 2, np.array([0, 1]), np.array([1]))
+    out = smb.sddmm(pat, np.array([[1.0, 2.0]], np.float32),
+                    np.array([[0.0, 0.0], [3.0, 4.0]], np.float32))
+    assert host(out.values).tolist() == [11.0]
+
+
+def test_empty_pattern_gives_zeros():
+    s = smb.SparsityPattern(2, 2, np.zeros(3, np.int32), np.zeros(0, np.int32)).zeros()
+    b = np.arange(4, dtype=np.float32).reshape(2, 2)
+    assert np.array_equal(smb.spmm(s, b), np.zeros((2, 2)))
+    assert np.array_equal(smb.spmm_transposed(s, b), np.zeros((2, 2)))
+
+
+def test_invalid_structures_rejected():
+    bad = [
+        (2, 2, [0, 1, 3], [0]),        # row_ptr end != nnz
+        (2, 2, [0, 2, 1], [0, 1]),     # decreasing row_ptr
+        (1, 2, [0, 1], [2]),           # col out of range
+        (1, 3, [0, 2], [1, 1]),        # duplicate col within a row
+    ]
+    for m, k, rp, ci in bad:
+        with pytest.raises(smb.InvalidArgumentError):
+            smb.CsrMatrix(m, k, np.array(rp), np.array(ci), np.ones(len(ci), np.float32))
+    with pytest.raises(smb.InvalidArgumentError):
+        smb.CsrMatrix(2, 2, np.array([0, 1]), np.array([0]), np.array([1.0], np.float32))
+    with pytest.raises(smb.InvalidArgumentError):
+        smb.CsrMatrix(1, 1, np.array([0, 1]), np.array([0]), np.array([1]))
+
+
+def test_csc_index_is_row_sorted(oracle):
+    rng = np.random.default_rng(3)
+    rp, ci, v, dense = random_csr(rng, 300, 200, 0.2)
+    pat = smb.SparsityPattern(300, 200, rp, ci)
+    col_ptr, row_idx, perm = (host(t) for t in pat.csc())
+    want_order = np.argsort(ci, kind="stable")
+    rows = np.repeat(np.arange(300), np.diff(rp))
+    assert np.array_equal(perm, want_order)
+    assert np.array_equal(row_idx, rows[want_order])
+    assert np.array_equal(col_ptr[1:], np.cumsum(np.bincount(ci, minlength=200)))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_row_sums_numpy_pairwise_order(dtype):
+    rng = np.random.default_rng(12)
+    for n in [1, 7, 8, 9, 100, 128, 129, 257, 1000, 1024, 4096]:
+        a = (rng.standard_normal((33, n)) * np.exp(3 * rng.standard_normal((33, n)))).astype(dtype)
+        assert bits_equal(smb.row_sums(a), a.sum(axis=1))
+
+
+@pytest.mark.parametrize("nesterov", [False, True])
+def test_optimizer_ten_steps_bitwise(nesterov):
+    # pkg/tests/test_nn.py:437-467: fp32 scalar recurrence with explicit rounding
+    mu, eta = 0.9, 0.05
+    rng = np.random.default_rng(33)
+    rp, ci, v, _ = random_csr(rng, 3, 3, 1.0)
+    layer = smb.SparseLinearLayer(smb.SparsityPattern(3, 3, rp, ci), v, np.zeros(3, np.float32),
+                                  smb.Momentum(mu, nesterov=nesterov))
+    nnz = layer.weights.nnz
+    grads = rng.standard_normal((10, nnz)).astype(np.float32)
+    w, vv = v.copy(), np.zeros(nnz, np.float32)
+    mu32, one, c_v, c_g = np.float32(mu), np.float32(1), np.float32(-eta * mu), np.float32(-eta)
+    for g in grads:
+        for i in range(nnz):
+            vv[i] = np.float32(np.float32(mu32 * vv[i]) + np.float32(one * g[i]))
+            if nesterov:
+                w[i] = np.float32(np.float32(one * w[i]) + np.float32(c_v * vv[i]))
+                w[i] = np.float32(np.float32(one * w[i]) + np.float32(c_g * g[i]))
+            else:
+                w[i] = np.float32(np.float32(one * w[i]) + np.float32(c_g * vv[i]))
+    for g in grads:
+        layer.grad.values.copy_(dev(g))
+        layer.grad_bias.zero_()
+        layer.optimize(eta)
+    assert bits_equal(host(layer.weights.values), w)
+    assert bits_equal(host(layer.velocity.values), vv)
+
+
+def test_fused_sddmm_update_matches_separate_ops(oracle):
+    """smb_sddmm_update == sddmm + row_sums + the Nesterov sparse_combine
+    sequence, bit for bit (nn.py:183-198)."""
+    rng = np.random.default_rng(8)
+    m, k, n = 257, 300, 100
+    rp, ci, v, _ = random_csr(rng, m, k, 0.1)
+    d = rng.standard_normal((m, n)).astype(np.float32)
+    x = rng.standard_normal((k, n)).astype(np.float32)
+    vel = rng.standard_normal(v.shape[0]).astype(np.float32)
+    bias = rng.standard_normal(m).astype(np.float32)
+    vb = rng.standard_normal(m).astype(np.float32)
+    eta, mu = 0.01, 0.9
+    # oracle sequence
+    g = oracle.sddmm(rp, ci, d, x)
+    gb = d.sum(axis=1)
+    w_o, v_o, b_o, vb_o = v.copy(), vel.copy(), bias.copy(), vb.copy()
+    oracle.axpby(mu, v_o, 1.0, g)
+    oracle.axpby(1.0, w_o, -eta * mu, v_o)
+    oracle.axpby(1.0, w_o, -eta, g)
+    vb_o *= np.float32(mu)
+    vb_o += gb
+    b_o += np.float32(-eta * mu) * vb_o
+    b_o += np.float32(-eta) * gb
+    # fused kernel
+    pat = smb.SparsityPattern(m, k, rp, ci)
+    tv, tvel, tb, tvb = dev(v), dev(vel), dev(bias), dev(vb)
+    td, tx = dev(d), dev(x)  # keep the operands alive across the async launch
+    from paper_2407_17437_b200 import _lib
+    _lib.call("smb_sddmm_update", _lib.SMB_F32, pat.handle, tc.ptr(td), n, tc.ptr(tx), n, n,
+              tc.ptr(tv), tc.ptr(tvel), None, tc.ptr(tb), tc.ptr(tvb), None,
+              _lib.SMB_OPT_NESTEROV, mu, eta, tc.stream_ptr())
+    torch.cuda.synchronize()
+    for got, want in [(tv, w_o), (tvel, v_o), (tb, b_o), (tvb, vb_o)]:
+        assert bits_equal(host(got), want)
+
+
+def test_relu_and_mask_match_numpy():
+    # bit-exact including signed zeros; NaN payloads are unspecified by IEEE
+    # (the GPU returns the canonical NaN), so NaNs only need to stay NaN
+    def same(a, b):
+        nan = np.isnan(a)
+        return np.array_equal(nan, np.isnan(b)) and bits_equal(a[~nan], b[~nan])
+
+    x = np.array([[-1.0, -0.0, 0.0, 2.0, np.nan]], np.float32)
+    y = host(smb.ReLU().forward(dev(x)))
+    assert same(y, np.maximum(x, 0))
+    d = np.array([[-3.0, 1.0, -2.0, 4.0, 5.0]], np.float32)
+    got = host(smb.ReLU().backward(dev(d), dev(x)))
+    assert same(got, d * (x > 0))
+
+
+def test_xavier_device_matches_numpy_stream():
+    from paper_2407_17437_b200.sparsity import Rng
+    for seed, n_in, n_out, nnz in [(3, 3072, 1024, 24461), (0, 10, 7, None), (11, 512, 10, 3117)]:
+        r1, r2 = Rng(seed).stream("init"), Rng(seed).stream("init")
+        a = np.sqrt(6.0 / (n_in + n_out))
+        size = n_out * n_in if nnz is None else nnz
+        want = r1.uniform(-a, a, size=size).astype(np.float32)
+        got = host(smb.xavier_init(n_in, n_out, r2, nnz=nnz))
+        assert bits_equal(got, want)
+        # the host stream advanced identically
+        assert r1.random() == r2.random()
+
+
+def test_softmax_ce_gradient_tolerance():
+    rng = np.random.default_rng(4)
+    y = (3 * rng.standard_normal((10, 333))).astype(np.float32)
+    lab = rng.integers(0, 10, 333)
+    t = np.zeros((10, 333), np.float32)
+    t[lab, np.arange(333)] = 1
+    z = y - y.max(axis=0, keepdims=True)
+    e = np.exp(z)
+    want = (e / e.sum(axis=0, keepdims=True) - t) / 333
+    got = host(smb.SoftmaxCrossEntropyLoss().gradient_scaled(dev(y), dev(t), 333))
+    assert rel_err(got, want) <= 1e-6
+    loss_want = float(np.sum(np.log(e.sum(axis=0)) - (z * t).sum(axis=0)))
+    assert abs(smb.softmax_ce_loss(dev(y), dev(t)) - loss_want) <= 1e-4 * abs(loss_want)
