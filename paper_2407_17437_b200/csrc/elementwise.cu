@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(256)
     softmax_step_kernel(const T* __restrict__ y, int64_t ld_y, const T* __restrict__ t,
                         int64_t ld_t, int64_t classes, int64_t n, T divisor, T* dy, int64_t ld_dy,
                         double* loss_out, double* loss_parts, unsigned* ticket, T* bias, T* vbias,
-                        T* grad_bias, OptConsts<T> opt, int32_t* counter, int32_t modulo) {
+                        T* grad_bias, OptConsts<T> opt, int32_t* counter, int32_t modulo,
+                        int stage_rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_warp[8];
   __shared__ bool s_last;
@@ -130,9 +131,20 @@ __global__ void __launch_bounds__(256)
     *counter = (modulo > 0 && v >= modulo) ? 0 : v;
   }
   if (grad_bias == nullptr && !(opt.kind != SMB_OPT_NONE && bias)) return;
+  // stage_rows: the whole classes x n block of d_y fits the dynamic smem the
+  // host reserved -> one coalesced pass, then the sums read shared memory
   T* leaf = reinterpret_cast<T*>(smem_raw) + warp * warp_pairwise_leaves((int)n);
+  T* staged = reinterpret_cast<T*>(smem_raw) + (blockDim.x >> 5) * warp_pairwise_leaves((int)n);
+  if (stage_rows) {
+    const int n32 = (int)n;
+    for (int c = 0; c < (int)classes; ++c)
+      for (int col = threadIdx.x; col < n32; col += blockDim.x)
+        staged[c * n32 + col] = dy[c * ld_dy + col];
+    __syncthreads();
+  }
   for (int64_t c = warp; c < classes; c += (blockDim.x >> 5)) {
-    const T g = warp_pairwise_sum(dy + c * ld_dy, (int)n, leaf);
+    const T* src = stage_rows ? staged + c * n : dy + c * ld_dy;
+    const T g = warp_pairwise_sum(src, (int)n, leaf);
     if (lane == 0) {
       if (grad_bias) grad_bias[c] = g;
       if (opt.kind != SMB_OPT_NONE && bias) {
@@ -309,7 +321,7 @@ extern "C" int smb_bias_grad_update(int dtype, const void* d_out, int64_t ld, in
 }
 
 extern "C" size_t smb_softmax_ce_workspace_bytes(int64_t n) {
-  return 256 + sizeof(double) * (size_t)ceil_div(n > 0 ? n : 1, 256);
+  return 256 + sizeof(double) * (size_t)ceil_div(n > 0 ? n : 1, 128);
 }
 
 static int softmax_launch(int dtype, const void* y, int64_t ld_y, const void* t, int64_t ld_t,
@@ -323,20 +335,25 @@ static int softmax_launch(int dtype, const void* y, int64_t ld_y, const void* t,
   SMB_REQUIRE(n <= (int64_t(1) << 30), "softmax: batch too wide");
   return dispatch_dtype(dtype, "smb_softmax_ce", [&](auto tag) {
     using T = decltype(tag);
-    // multi-CTA needs the workspace (ticket + per-CTA loss partials)
-    const unsigned grid = workspace ? (unsigned)ceil_div(n > 0 ? n : 1, 256) : 1u;
+    // multi-CTA (128 columns each) needs the workspace (ticket + per-CTA
+    // loss partials); without it one CTA loops over all columns
+    const int threads = workspace ? 128 : 256;
+    const unsigned grid = workspace ? (unsigned)ceil_div(n > 0 ? n : 1, threads) : 1u;
     unsigned* ticket = workspace ? static_cast<unsigned*>(workspace) : nullptr;
     double* parts = workspace ? reinterpret_cast<double*>(static_cast<char*>(workspace) + 256)
                               : nullptr;
-    const size_t dyn = sizeof(T) * 8 * (size_t)warp_pairwise_leaves((int)n);
+    const bool rows = grad_bias != nullptr || (opt_kind != SMB_OPT_NONE && bias != nullptr);
+    size_t dyn = rows ? sizeof(T) * (threads / 32) * (size_t)warp_pairwise_leaves((int)n) : 0;
+    const size_t block = sizeof(T) * (size_t)(classes * n);
+    const int stage = rows && dyn + block <= 160 * 1024;
+    if (stage) dyn += block;
     auto kern = softmax_step_kernel<T>;
-    if (dyn > 40 * 1024)
-      ensure_smem(kern, dyn);
-    kern<<<grid, 256, dyn, as_stream(stream)>>>(
+    if (dyn > 40 * 1024) ensure_smem(kern, dyn);
+    kern<<<grid, threads, dyn, as_stream(stream)>>>(
         static_cast<const T*>(y), ld_y, static_cast<const T*>(t), ld_t, classes, n,
         static_cast<T>(divisor), static_cast<T*>(d_y), ld_dy, loss_out, parts, ticket,
         static_cast<T*>(bias), static_cast<T*>(vbias), static_cast<T*>(grad_bias),
-        make_opt<T>(opt_kind, mu, eta), counter, modulo);
+        make_opt<T>(opt_kind, mu, eta), counter, modulo, stage);
     return check_launch("smb_softmax_ce");
   });
 }

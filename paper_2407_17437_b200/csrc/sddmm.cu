@@ -37,9 +37,11 @@ struct SddmmCfg {
   static constexpr int LDS = kChunk + VW;    // padded smem row (elements)
   static constexpr int VPR = kChunk / VW;    // 16 B vectors per staged row
   static constexpr int SLOTS = TILE / 4;  // staged d_out rows per tile
-  // fp32: 512-tile x 4 stages = 200 KB (1 CTA, 16 warps / SM),
-  //       128-tile x 6 stages = 77 KB (2 CTAs / SM)
-  static constexpr int STAGES = TILE >= 512 ? 4 : 6;
+  // power-of-two ring (stage = chunk & (STAGES-1)); fp32:
+  //   512-tile x 4 stages = 200 KB (1 CTA, 16 warps / SM),
+  //   128-tile x 8 stages = 102 KB (2 CTAs / SM); fp64 128-tile x 4 = 92 KB
+  static constexpr int STAGES = TILE >= 512 ? 4 : (sizeof(T) == 4 ? 8 : 4);
+  static_assert((STAGES & (STAGES - 1)) == 0, "power-of-two ring");
   static constexpr size_t stage_elems = size_t(TILE + SLOTS) * LDS;
   static constexpr size_t smem_bytes = STAGES * stage_elems * sizeof(T);
   static_assert(TILE % VPR == 0, "tile / vector split");
@@ -128,7 +130,9 @@ __global__ void __launch_bounds__(TILE)
   const int64_t row = tile_row_of<TILE>(p, r0, s_rp, row_ptr, m);
   const int slot = (int)imin(row - r0, C::SLOTS);  // SLOTS == "not staged"
   const int n_staged = (int)imin(C::SLOTS, m - r0);
-  const int64_t n_chunks = (n + kChunk - 1) / kChunk;
+  // batch widths are far below 2^31: all chunk / column arithmetic is 32-bit
+  const int n32 = (int)n;
+  const int n_chunks = (n32 + kChunk - 1) / kChunk;
 
   // ---- fixed copy slots of this thread (computed once) ----
   // x rows: vector v = tid % VPR of rows tid/VPR + k*TILE/VPR, k < VPR
@@ -136,10 +140,12 @@ __global__ void __launch_bounds__(TILE)
   const T* xsrc[VPR];
   unsigned xdst[VPR];
   int xok[VPR];
+  int xfull[VPR];  // bytes of a full-chunk copy: 16 for an active row, else 0
 #pragma unroll
   for (int k = 0; k < VPR; ++k) {
     const int r = tid / VPR + k * (TILE / VPR);
     xok[k] = r < n_active;
+    xfull[k] = xok[k] ? 16 : 0;
     xsrc[k] = x + (int64_t)s_col[r] * ld_x + v * VW;
     xdst[k] = (unsigned)((r * LDS + v * VW) * sizeof(T));
   }
@@ -159,11 +165,20 @@ __global__ void __launch_bounds__(TILE)
   const unsigned sbase = smem_u32(smem);
   constexpr unsigned kStageBytes = (unsigned)(C::stage_elems * sizeof(T));
 
-  auto issue = [&](int64_t ch) {
-    const unsigned st = sbase + (unsigned)(ch % S) * kStageBytes;
-    const int64_t t0 = ch * kChunk;
+  auto issue = [&](int ch) {
+    const unsigned st = sbase + (unsigned)(ch & (S - 1)) * kStageBytes;
+    const int t0 = ch * kChunk;
+    if (VEC && t0 + kChunk <= n32) {
+      // full chunk: no bounds, fixed copy sizes
+#pragma unroll
+      for (int k = 0; k < VPR; ++k) cp_async16(st + xdst[k], xsrc[k] + t0, xfull[k]);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        if (dcopy[c]) cp_async16(st + ddst[c], dsrc[c] + t0, 16);
+      return;
+    }
     // elements of this thread's vector inside [0, n)
-    const int valid = (int)imax(0, imin(VW, n - (t0 + v * VW)));
+    const int valid = max(0, min(VW, n32 - (t0 + v * VW)));
 #pragma unroll
     for (int k = 0; k < VPR; ++k) copy_vec<T, VEC>(st + xdst[k], xsrc[k] + t0, xok[k] ? valid : 0);
 #pragma unroll
@@ -180,17 +195,17 @@ __global__ void __launch_bounds__(TILE)
   T acc = T(-0.0);
   const T* drow = d_out + row * ld_d;
   using V = typename Vec16<T>::type;
-  for (int64_t ch = 0; ch < n_chunks; ++ch) {
+  for (int ch = 0; ch < n_chunks; ++ch) {
     cp_async_wait<S - 2>();
-    __syncthreads();  // chunk ch landed for everyone; stage (ch-1)%S is free
+    __syncthreads();  // chunk ch landed for everyone; stage (ch-1)&(S-1) is free
     if (ch + S - 1 < n_chunks) issue(ch + S - 1);
     cp_async_commit();
     if (active) {
-      const T* xs = smem + (ch % S) * C::stage_elems;
+      const T* xs = smem + (ch & (S - 1)) * C::stage_elems;
       const T* xr = xs + tid * LDS;
       const T* dr = xs + (TILE + slot) * LDS;
-      const int64_t t0 = ch * kChunk;
-      const int cnt = (int)imin(kChunk, n - t0);
+      const int t0 = ch * kChunk;
+      const int cnt = min(kChunk, n32 - t0);
       if (cnt == kChunk) {
 #pragma unroll
         for (int u = 0; u < VPR; ++u) {

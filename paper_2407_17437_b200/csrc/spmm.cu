@@ -96,10 +96,11 @@ struct EpiArgs {
   OptConsts<T> opt;
 };
 
-// widest CTA per row: 32 warps with scalar lanes, 16 warps with 16-byte
-// lanes, 8 warps with 32-byte lanes (keeps the U-deep ring in registers)
+// at most 8 warps per CTA: a 256-thread bound leaves up to 255 registers per
+// thread, so the U-deep prefetch ring stays in flight (with a 64-register cap
+// the compiler sinks the ring's loads next to their uses)
 template <int W>
-constexpr int max_threads_for() { return W * 4 > 16 ? 256 : (W > 1 ? 512 : 1024); }
+constexpr int max_threads_for() { return 256; }
 
 template <typename T, int W, int U, int EPI, bool PERM>
 __global__ void __launch_bounds__(max_threads_for<W>())
@@ -122,59 +123,79 @@ __global__ void __launch_bounds__(max_threads_for<W>())
 
   const int32_t s_begin = seg_ptr[row];
   const int32_t s_end = seg_ptr[row + 1];
-  const T* dcol = dense + col0;
+  // lanes past the batch read column 0 (in bounds, never stored): every ring
+  // refill can then be unconditional -- a predicated refill compiles to a
+  // load plus a predicated move that stalls on the load right away
+  const T* dcol = dense + (valid > 0 ? col0 : 0);
   const uint32_t ldu = (uint32_t)ld_dense;  // row offsets as one IMAD.WIDE.U32
   // warp-uniform: every lane of this warp owns W valid columns
   const bool full_chunk = (chunk + 1) * (32 * W) <= n;
 
-  // 32 (idx, val) pairs per coalesced load, broadcast by shuffles; a U-deep
-  // ring of dense-row fragments, each slot refilled as soon as it is consumed
-  for (int32_t s0 = s_begin; s0 < s_end; s0 += 32) {
-    const int cnt = min(32, s_end - s0);
-    int my_idx = 0;
-    T my_val = T(0);
-    if (lane < cnt) {
-      my_idx = idx[s0 + lane];
-      my_val = PERM ? vals[perm[s0 + lane]] : vals[s0 + lane];
+  // The segment is walked in groups of 32 (idx, val) pairs (one coalesced
+  // load per group, broadcast by shuffles; the NEXT group is always loaded a
+  // group ahead).  A U-deep register ring of dense-row fragments runs
+  // continuously across groups: the slot consumed at position s is refilled
+  // with position s + U (U divides 32, so a position's slot is s % U in every
+  // group).
+  const int len = s_end - s_begin;
+  auto load_group = [&](int g, int& gi, T& gv) {
+    const int32_t s = s_begin + g * 32 + lane;
+    gi = 0;
+    gv = T(0);
+    if (s < s_end) {
+      gi = idx[s];
+      gv = PERM ? vals[perm[s]] : vals[s];
     }
-    Frag<T, W> xs[U];
-    if (cnt == 32 && full_chunk) {
-      // fast path: fully unrolled, no runtime predicates
+  };
+  int idx_c, idx_n;
+  T val_c, val_n;
+  load_group(0, idx_c, val_c);
+  load_group(1, idx_n, val_n);
+  // lanes with 0 < valid < W (the batch tail) need element-wise loads
+  const bool lane_full = valid == W || valid == 0;
+  auto refill = [&](Frag<T, W>& f, int src) {
+    const T* p = dcol + (size_t)(uint32_t)src * ldu;
+    if (lane_full) load_frag_full<T, W>(f, p);
+    else load_frag<T, W>(f, p, valid);
+  };
+  Frag<T, W> xs[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t src = (uint32_t)__shfl_sync(0xffffffffu, my_idx, u);
-        load_frag_full<T, W>(xs[u], dcol + (size_t)src * ldu);
-      }
+  for (int u = 0; u < U; ++u) refill(xs[u], __shfl_sync(0xffffffffu, idx_c, u));
+  const int ngroups = (len + 31) / 32;
+  for (int g = 0; g < ngroups; ++g) {
+    const int cnt = min(32, len - g * 32);
+    if (cnt == 32 && full_chunk) {
+      // fast path: fully unrolled, unconditional refills (positions past the
+      // row end carry index 0 and are never consumed)
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
-        const T v = __shfl_sync(0xffffffffu, my_val, q);
+        const T v = __shfl_sync(0xffffffffu, val_c, q);
 #pragma unroll
         for (int j = 0; j < W; ++j) acc.v[j] = add_rn(acc.v[j], mul_rn(v, xs[q % U].v[j]));
-        if (q + U < 32) {
-          const uint32_t nxt = (uint32_t)__shfl_sync(0xffffffffu, my_idx, q + U);
-          load_frag_full<T, W>(xs[q % U], dcol + (size_t)nxt * ldu);
-        }
+        const uint32_t nxt = (uint32_t)(q + U < 32 ? __shfl_sync(0xffffffffu, idx_c, q + U)
+                                                   : __shfl_sync(0xffffffffu, idx_n, q + U - 32));
+        load_frag_full<T, W>(xs[q % U], dcol + (size_t)nxt * ldu);
       }
-      continue;
-    }
+    } else {
+      for (int q0 = 0; q0 < cnt; q0 += U) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int src = __shfl_sync(0xffffffffu, my_idx, u & 31);
-      if (u < cnt && valid > 0) load_frag<T, W>(xs[u], dcol + (int64_t)src * ld_dense, valid);
-    }
-    for (int q = 0; q < cnt; q += U) {
+        for (int u = 0; u < U; ++u) {
+          const int q = q0 + u;
+          const T v = __shfl_sync(0xffffffffu, val_c, q & 31);
+          const int pos = q + U;  // refill target, possibly in the next group
+          const int nc = __shfl_sync(0xffffffffu, idx_c, pos & 31);
+          const int nn = __shfl_sync(0xffffffffu, idx_n, pos & 31);
+          if (q < cnt) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const T v = __shfl_sync(0xffffffffu, my_val, (q + u) & 31);
-        const int nxt = __shfl_sync(0xffffffffu, my_idx, (q + u + U) & 31);
-        if (q + u < cnt) {
-#pragma unroll
-          for (int j = 0; j < W; ++j) acc.v[j] = add_rn(acc.v[j], mul_rn(v, xs[u].v[j]));
-          if (q + u + U < cnt && valid > 0)
-            load_frag<T, W>(xs[u], dcol + (int64_t)nxt * ld_dense, valid);
+            for (int j = 0; j < W; ++j) acc.v[j] = add_rn(acc.v[j], mul_rn(v, xs[u].v[j]));
+            refill(xs[u], pos < 32 ? nc : nn);
+          }
         }
       }
     }
+    idx_c = idx_n;
+    val_c = val_n;
+    load_group(g + 2, idx_n, val_n);
   }
 
   if constexpr (EPI == kEpiBiasAct) {
@@ -230,7 +251,11 @@ bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm
   // the separate warp-per-row bias kernel.
   const bool fuse = EPI == kEpiMask && epi.rowsum && n_rows >= 2 * 148 &&
                     chunks <= max_threads_for<W>() / 32;
-  const int warps = fuse ? (int)chunks : (int)imin(8, chunks);
+  // unfused: narrow CTAs (as few as 1 warp) when rows are few, so the warps
+  // of a short, wide layer still spread over all 148 SMs
+  int warps = (int)imin(8, chunks);
+  while (warps > 1 && n_rows * ceil_div(chunks, warps) < 2 * 148) warps >>= 1;
+  if (fuse) warps = (int)chunks;
   const int64_t gy = ceil_div(chunks, warps);
   size_t dyn = 0;
   if (fuse) dyn = sizeof(T) * (size_t)(((n + 3) & ~int64_t(3)) + warp_pairwise_leaves((int)n));
@@ -269,7 +294,7 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
     done = launch_rows<T, VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                             out, ld_out, epi, st);
   else
-    done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+    done = launch_rows<T, 1, 32, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                             out, ld_out, epi, st);
   if (rowsum_done) *rowsum_done = done;
   return check_launch(name);

@@ -139,8 +139,15 @@ class FusedTrainStep:
         f32 = torch.float32
         self.n_in = self.units[0].k
         self.classes = self.units[-1].m
-        self.x_in = torch.zeros((self.n_in, ld), dtype=f32, device=dev)
-        self.t_in = torch.zeros((self.classes, ld), dtype=f32, device=dev)
+        # two input slots: train_batch() copies batch k+1 into one slot on a
+        # copy stream while the step of batch k reads the other
+        self.x_slots = [torch.zeros((self.n_in, ld), dtype=f32, device=dev) for _ in range(2)]
+        self.t_slots = [torch.zeros((self.classes, ld), dtype=f32, device=dev) for _ in range(2)]
+        self.x_in, self.t_in = self.x_slots[0], self.t_slots[0]
+        self._slot = 0
+        self._next_slot = 0
+        self._copy_stream = None
+        self._slot_ready = self._slot_free = None
         self.acts = [torch.zeros((u.m, ld), dtype=f32, device=dev) for u in self.units]
         self.dys = [torch.zeros((u.m, ld), dtype=f32, device=dev) for u in self.units]
         self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -230,14 +237,15 @@ class FusedTrainStep:
         st = stream_ptr()
         B, ld = self.B, self.ld
         F32 = _lib.SMB_F32
+        x_in, t_in = self.x_slots[self._slot], self.t_slots[self._slot]
         if gather:
             d = self.data
             self._call("gather", "smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features,
-                       ptr(self.perm), ptr(self.counter), 0, B, ptr(self.x_in), ld, st)
+                       ptr(self.perm), ptr(self.counter), 0, B, ptr(x_in), ld, st)
             self._call("gather", "smb_gather_columns", F32, ptr(d.T), d.n_samples, d.classes,
-                       ptr(self.perm), ptr(self.counter), 0, B, ptr(self.t_in), ld, st)
+                       ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in), ld, st)
         # forward: a_l = act(W_l a_{l-1} + b_l)
-        x = self.x_in
+        x = x_in
         for li, (u, a) in enumerate(zip(self.units, self.acts)):
             lay = u.layer
             if u.sparse:
@@ -256,7 +264,7 @@ class FusedTrainStep:
         top = self.units[-1]
         b, vb, gb, kind, mu = self._bias_target(top, fuse_update)
         self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
-                   ptr(self.t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]), ld,
+                   ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]), ld,
                    ptr(self.loss), b, vb, gb, kind, mu, float(eta),
                    ptr(self.counter) if gather else None, int(self.steps_per_epoch),
                    ptr(self._ce_ws), st)
@@ -266,7 +274,7 @@ class FusedTrainStep:
             u = self.units[li]
             lay = u.layer
             dy = self.dys[li]
-            x_prev = self.acts[li - 1] if li > 0 else self.x_in
+            x_prev = self.acts[li - 1] if li > 0 else x_in
             if li > 0:
                 below = self.units[li - 1]
                 mask = self.acts[li - 1] if below.relu else None
@@ -340,27 +348,16 @@ class FusedTrainStep:
         else:
             self._launch_updates_from_flat(eta)
 
-    def _graph(self, eta: float, gather: bool, part: str):
-        key = (float(eta), gather, part)
-        g = self._graphs.get(key)
-        if g is None:
-            # warm up eagerly on a side stream (cuBLAS handles, smem attributes),
-            # then restore the state the warm-up touched by re-running nothing:
-            # capture only records, it does not execute.
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._run_eager(eta, gather, part)
-            self._graphs[key] = g
-        return g
-
-    def step(self, eta: float, gather: bool | None = None) -> None:
+    def step(self, eta: float, gather: bool | None = None, slot: int = 0) -> None:
         """One training step.  With gather (default when a dataset is
         attached) the batch comes from the device dataset at the device step
-        counter; otherwise the caller has filled ``x_in`` / ``t_in``."""
+        counter; otherwise the caller has filled input slot `slot`
+        (``x_slots[slot]`` / ``t_slots[slot]``; slot 0 is ``x_in`` / ``t_in``)."""
         if gather is None:
             gather = self.data is not None
         if gather and (self.data is None or self.perm is None):
             raise InvalidArgumentError("attach_dataset() and set_epoch() before gathering steps")
+        self._slot = 0 if gather else int(slot)
         if self.world == 1:
             self._replay_or_run(eta, gather, "all")
             return
@@ -374,31 +371,51 @@ class FusedTrainStep:
         if not self.use_graph:
             self._run_eager(eta, gather, part)
             return
-        key = (float(eta), gather, part)
-        if key not in self._graphs:
-            # the first execution is eager (initialises cuBLAS / kernel
-            # attributes outside capture); later ones replay the graph
+        key = (float(eta), gather, part, self._slot)
+        g = self._graphs.get(key)
+        if g is None:
+            # the first execution is eager (initialises cuBLAS handles and
+            # kernel attributes outside capture); capture only records, it
+            # does not execute, so the captured graph replays from step 2 on
             self._run_eager(eta, gather, part)
-            self._graph(eta, gather, part)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._run_eager(eta, gather, part)
+            self._graphs[key] = g
             return
-        self._graphs[key].replay()
+        g.replay()
 
     def train_batch(self, xb, tb, eta: float, loss_out=None) -> None:
         """One step on a host-supplied batch (the reference's per-batch call
         sequence, train.py:398-401): xb [features, B] and tb [classes, B]
-        (ideally pinned host tensors) are copied into the device input
-        buffers on the current stream, the captured step runs, and the batch
-        loss is copied into `loss_out` (a pinned float64 host tensor) when
-        given.  Stream-ordered; nothing synchronises."""
+        (pinned host tensors for asynchronous copies) are copied into one of
+        two device input slots on a copy stream, so the copy of batch k+1
+        overlaps the step of batch k; the captured step then runs on the
+        current stream and the batch loss is copied into `loss_out` (a pinned
+        float64 host tensor) when given.  Stream-ordered; nothing
+        synchronises with the host."""
         B = self.B
-        x_dst = self.x_in[:, :B]
-        t_dst = self.t_in[:, :B]
-        if tuple(xb.shape) != tuple(x_dst.shape) or tuple(tb.shape) != tuple(t_dst.shape):
+        if tuple(xb.shape) != (self.n_in, B) or tuple(tb.shape) != (self.classes, B):
             raise InvalidArgumentError(
-                f"expected batch shapes {tuple(x_dst.shape)} / {tuple(t_dst.shape)}")
-        x_dst.copy_(torch.as_tensor(xb), non_blocking=True)
-        t_dst.copy_(torch.as_tensor(tb), non_blocking=True)
-        self.step(eta, gather=False)
+                f"expected batch shapes {(self.n_in, B)} / {(self.classes, B)}")
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=self.dev)
+            self._slot_ready = [torch.cuda.Event() for _ in range(2)]
+            self._slot_free = [torch.cuda.Event() for _ in range(2)]
+            for e in self._slot_free:
+                e.record()
+        slot = self._next_slot
+        self._next_slot ^= 1
+        cs = self._copy_stream
+        main = torch.cuda.current_stream()
+        cs.wait_event(self._slot_free[slot])  # the step that read this slot is done
+        with torch.cuda.stream(cs):
+            self.x_slots[slot][:, :B].copy_(torch.as_tensor(xb), non_blocking=True)
+            self.t_slots[slot][:, :B].copy_(torch.as_tensor(tb), non_blocking=True)
+            self._slot_ready[slot].record(cs)
+        main.wait_event(self._slot_ready[slot])
+        self.step(eta, gather=False, slot=slot)
+        self._slot_free[slot].record(main)
         if loss_out is not None:
             loss_out.copy_(self.loss, non_blocking=True)
 

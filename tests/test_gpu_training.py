@@ -70,7 +70,9 @@ def _fused_and_layerwise(chain, density, seed, B, steps, eta=0.05):
         xb = torch.from_numpy(np.ascontiguousarray(data.Xtrain[:, b])).cuda()
         tb = torch.from_numpy(np.ascontiguousarray(data.Ttrain[:, b])).cuda()
         y = m_layer.feedforward(xb)
-        d = loss.gradient(y, tb) / B
+        # (softmax(y) - t) / B with IEEE division like numpy (train.py:399);
+        # torch's `cuda_tensor / python_scalar` multiplies by the reciprocal
+        d = loss.gradient_scaled(y, tb, B)
         m_layer.backpropagate(y, d)
         m_layer.optimize(eta)
     torch.cuda.synchronize()
