@@ -167,6 +167,18 @@ SMB_API int smb_sddmm_update(int dtype, const smb_pattern* pattern, const void* 
                      void* grad_out, void* bias, void* velocity_bias, void* grad_bias_out,
                      int opt_kind, double mu, double eta, void* stream);
 
+/* smb_sddmm_update with the pre-update values read from `values` and the
+ * updated values written to `values_out` (may equal `values`).  Lets the
+ * training step keep two value buffers so the transposed SpMM of the same
+ * layer (which must see the pre-update weights, train.py:400-401) can run
+ * concurrently with the update on another stream. */
+SMB_API int smb_sddmm_update_into(int dtype, const smb_pattern* pattern, const void* d_out,
+                                  int64_t ld_dout, const void* x, int64_t ld_x, int64_t n,
+                                  const void* values, void* values_out, void* velocity,
+                                  void* grad_out, void* bias, void* velocity_bias,
+                                  void* grad_bias_out, int opt_kind, double mu, double eta,
+                                  void* stream);
+
 /* grad_bias = row_sums(d_out) (numpy pairwise order) and the bias optimizer
  * update; one warp per row (nn.py:184, 118-131).  Dense layers and any
  * layer whose output gradient was not produced by smb_spmm_t_bias. */
@@ -187,9 +199,9 @@ SMB_API int smb_row_sums(int dtype, const void* dense, int64_t m, int64_t n, int
 /* d_y = (softmax_columns(y) - t) / divisor   (nn.py:385-389, 411-417 and the
  * "/ batch_size" of train.py:399).  y, t, d_y are classes x n.  If loss_out
  * (device double[1]) is not NULL it receives softmax_ce_loss(y, t)
- * (nn.py:397-408, summed over the batch, not divided).  exp is evaluated in
- * double and rounded (numpy's float32 exp is not correctly rounded, so this
- * op is tolerance-exact, not bit-exact). */
+ * (nn.py:397-408, summed over the batch, not divided).  exp is the
+ * full-accuracy expf (<= 2 ulp; numpy's float32 exp is not correctly rounded
+ * either), so this op is tolerance-exact, not bit-exact. */
 SMB_API int smb_softmax_ce_grad(int dtype, const void* y, int64_t ld_y, const void* t, int64_t ld_t,
                         int64_t classes, int64_t n, double divisor, void* d_y, int64_t ld_dy,
                         double* loss_out, void* stream);

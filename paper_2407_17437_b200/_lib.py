@@ -56,6 +56,10 @@ SIGNATURES = {
         [_i32, _p, _i64, _p, _i64, _i64, _i64, _f64, _p, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
          _p, _i32, _p, _p],
     ),
+    "smb_sddmm_update_into": (
+        _i32,
+        [_i32, _p, _p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _i32, _f64, _f64, _p],
+    ),
     "smb_optimizer_step": (_i32, [_i32, _p, _p, _p, _i64, _i32, _f64, _f64, _p]),
     "smb_row_sums": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p]),
     "smb_softmax_ce_grad": (

@@ -61,6 +61,14 @@ __global__ void __launch_bounds__(kRowWarps * 32)
   }
 }
 
+// full-accuracy (non-intrinsic) exp / log in the value type: expf is within
+// 2 ulp like numpy's own float32 exp (documented max 2.52 ulp), so the
+// softmax is tolerance-exact, not bit-exact, against the reference
+__device__ __forceinline__ float exp_full(float x) { return expf(x); }
+__device__ __forceinline__ double exp_full(double x) { return exp(x); }
+__device__ __forceinline__ float log_full(float x) { return logf(x); }
+__device__ __forceinline__ double log_full(double x) { return log(x); }
+
 // ---- softmax cross-entropy step (nn.py:385-417, train.py:399) -------------
 // One thread per sample column: z = y - max, e = exp(z) (double, rounded),
 // s = sum_c e (sequential, numpy's axis-0 order), d = (e/s - t) / divisor.
@@ -68,15 +76,18 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 // and across CTAs by the last CTA to finish (ticket), which then also runs
 // the last layer's bias row sums / update and advances the step counter.
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     softmax_step_kernel(const T* __restrict__ y, int64_t ld_y, const T* __restrict__ t,
                         int64_t ld_t, int64_t classes, int64_t n, T divisor, T* dy, int64_t ld_dy,
                         double* loss_out, double* loss_parts, unsigned* ticket, T* bias, T* vbias,
                         T* grad_bias, OptConsts<T> opt, int32_t* counter, int32_t modulo,
                         int stage_rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double s_warp[8];
+  __shared__ double s_warp[32];
   __shared__ bool s_last;
+  // dynamic smem: [warps x pairwise leaves][classes x n staged d_y block]
+  T* stage_dst =
+      reinterpret_cast<T*>(smem_raw) + (blockDim.x >> 5) * warp_pairwise_leaves((int)n);
   double local = 0.0;
   for (int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; col < n;
        col += (int64_t)gridDim.x * blockDim.x) {
@@ -85,20 +96,42 @@ __global__ void __launch_bounds__(256)
       const T v = y[c * ld_y + col];
       mx = (v > mx || v != v) ? v : mx;
     }
-    T s = T(0);
-    double zt = 0.0;
-    for (int64_t c = 0; c < classes; ++c) {
-      const T z = sub_rn(y[c * ld_y + col], mx);
-      const T e = static_cast<T>(exp(static_cast<double>(z)));
-      dy[c * ld_dy + col] = e;
-      s = add_rn(s, e);
-      zt += static_cast<double>(z) * static_cast<double>(t[c * ld_t + col]);
+    T s = T(0), zt = T(0);
+    constexpr int kRegC = 16;  // e kept in registers for up to 16 classes
+    T er[kRegC];
+    if (classes <= kRegC) {
+#pragma unroll
+      for (int c = 0; c < kRegC; ++c) {
+        if (c < classes) {
+          const T z = sub_rn(y[c * ld_y + col], mx);
+          er[c] = exp_full(z);
+          s = add_rn(s, er[c]);
+          zt = add_rn(zt, mul_rn(z, t[c * ld_t + col]));
+        }
+      }
+    } else {
+      for (int64_t c = 0; c < classes; ++c) {
+        const T z = sub_rn(y[c * ld_y + col], mx);
+        const T e = exp_full(z);
+        dy[c * ld_dy + col] = e;
+        s = add_rn(s, e);
+        zt = add_rn(zt, mul_rn(z, t[c * ld_t + col]));
+      }
     }
-    for (int64_t c = 0; c < classes; ++c) {
-      const T pr = div_rn(dy[c * ld_dy + col], s);
-      dy[c * ld_dy + col] = div_rn(sub_rn(pr, t[c * ld_t + col]), divisor);
+    auto emit = [&](int64_t c, T e) {
+      const T g = div_rn(sub_rn(div_rn(e, s), t[c * ld_t + col]), divisor);
+      dy[c * ld_dy + col] = g;
+      // single CTA: keep the block in shared memory for the bias row sums
+      if (stage_rows && gridDim.x == 1) stage_dst[c * n + col] = g;
+    };
+    if (classes <= kRegC) {
+#pragma unroll
+      for (int c = 0; c < kRegC; ++c)
+        if (c < classes) emit(c, er[c]);
+    } else {
+      for (int64_t c = 0; c < classes; ++c) emit(c, dy[c * ld_dy + col]);
     }
-    local += log(static_cast<double>(s)) - zt;
+    local += static_cast<double>(sub_rn(log_full(s), zt));
   }
   // fixed-order block reduction of the loss
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -134,12 +167,26 @@ __global__ void __launch_bounds__(256)
   // stage_rows: the whole classes x n block of d_y fits the dynamic smem the
   // host reserved -> one coalesced pass, then the sums read shared memory
   T* leaf = reinterpret_cast<T*>(smem_raw) + warp * warp_pairwise_leaves((int)n);
-  T* staged = reinterpret_cast<T*>(smem_raw) + (blockDim.x >> 5) * warp_pairwise_leaves((int)n);
-  if (stage_rows) {
-    const int n32 = (int)n;
-    for (int c = 0; c < (int)classes; ++c)
-      for (int col = threadIdx.x; col < n32; col += blockDim.x)
-        staged[c * n32 + col] = dy[c * ld_dy + col];
+  T* staged = stage_dst;
+  if (stage_rows && gridDim.x == 1) {
+    __syncthreads();  // the single CTA wrote the block while computing it
+  } else if (stage_rows) {
+    // 8 independent loads in flight per thread (a plain loop serialises one
+    // L2 round trip per element)
+    const int n32 = (int)n, total = (int)classes * n32, nt = blockDim.x;
+    for (int base = threadIdx.x; base < total; base += 8 * nt) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = base + u * nt;
+        v[u] = e < total ? dy[(int64_t)(e / n32) * ld_dy + e % n32] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = base + u * nt;
+        if (e < total) staged[e] = v[u];
+      }
+    }
     __syncthreads();
   }
   for (int64_t c = warp; c < classes; c += (blockDim.x >> 5)) {
@@ -337,15 +384,21 @@ static int softmax_launch(int dtype, const void* y, int64_t ld_y, const void* t,
     using T = decltype(tag);
     // multi-CTA (128 columns each) needs the workspace (ticket + per-CTA
     // loss partials); without it one CTA loops over all columns
-    const int threads = workspace ? 128 : 256;
-    const unsigned grid = workspace ? (unsigned)ceil_div(n > 0 ? n : 1, threads) : 1u;
+    // One 1024-thread CTA whenever the classes x n block of d_y fits shared
+    // memory (it then stays on chip for the bias row sums: no cross-CTA
+    // ticket, no global round trip); else 128-column CTAs + last-CTA epilogue
+    // (needs the workspace).
+    const bool rows = grad_bias != nullptr || (opt_kind != SMB_OPT_NONE && bias != nullptr);
+    const size_t block = sizeof(T) * (size_t)(classes * n);
+    const size_t leaves1 = sizeof(T) * 32 * (size_t)warp_pairwise_leaves((int)n);
+    const bool single = !workspace || (leaves1 + block <= 180 * 1024 && n <= 64 * 1024);
+    const int threads = single ? 1024 : 128;
+    const unsigned grid = single ? 1u : (unsigned)ceil_div(n > 0 ? n : 1, threads);
     unsigned* ticket = workspace ? static_cast<unsigned*>(workspace) : nullptr;
     double* parts = workspace ? reinterpret_cast<double*>(static_cast<char*>(workspace) + 256)
                               : nullptr;
-    const bool rows = grad_bias != nullptr || (opt_kind != SMB_OPT_NONE && bias != nullptr);
     size_t dyn = rows ? sizeof(T) * (threads / 32) * (size_t)warp_pairwise_leaves((int)n) : 0;
-    const size_t block = sizeof(T) * (size_t)(classes * n);
-    const int stage = rows && dyn + block <= 160 * 1024;
+    const int stage = rows && dyn + block <= 180 * 1024;
     if (stage) dyn += block;
     auto kern = softmax_step_kernel<T>;
     if (dyn > 40 * 1024) ensure_smem(kern, dyn);

@@ -29,17 +29,20 @@
 namespace smb {
 namespace {
 
-constexpr int kChunk = 16;  // batch columns per pipeline stage
-
-template <typename T, int TILE>
+// TILE nonzeros per CTA, CH batch columns per pipeline stage
+template <typename T, int TILE, int CH>
 struct SddmmCfg {
+  static constexpr int kChunk = CH;
   static constexpr int VW = 16 / sizeof(T);  // elements per 16 B
   static constexpr int LDS = kChunk + VW;    // padded smem row (elements)
   static constexpr int VPR = kChunk / VW;    // 16 B vectors per staged row
   static constexpr int SLOTS = TILE / 4;  // staged d_out rows per tile
   // power-of-two ring (stage = chunk & (STAGES-1)); fp32:
-  //   512-tile x 4 stages = 200 KB (1 CTA, 16 warps / SM),
-  //   128-tile x 8 stages = 102 KB (2 CTAs / SM); fp64 128-tile x 4 = 92 KB
+  //   512-tile x 16 cols x 4 stages = 200 KB (1 CTA, 16 warps / SM),
+  //   128-tile x 16 cols x 8 stages = 102 KB (2 CTAs / SM),
+  //   128-tile x 32 cols x 8 stages = 184 KB (1 CTA / SM: single-wave layers,
+  //   where the per-chain critical path, not throughput, sets the time);
+  //   fp64 128-tile x 16 cols x 4 = 92 KB
   static constexpr int STAGES = TILE >= 512 ? 4 : (sizeof(T) == 4 ? 8 : 4);
   static_assert((STAGES & (STAGES - 1)) == 0, "power-of-two ring");
   static constexpr size_t stage_elems = size_t(TILE + SLOTS) * LDS;
@@ -104,15 +107,16 @@ __device__ __forceinline__ void copy_vec(unsigned dst, const T* src, int valid_e
 
 // ALL: every tile's d_out rows fit the SLOTS staging rows (checked on the
 // host from the pattern's tile spans), so the hot loop has no fallback path.
-template <typename T, int TILE, bool VEC, bool ALL>
+template <typename T, int TILE, int CH, bool VEC, bool ALL>
 __global__ void __launch_bounds__(TILE)
     sddmm_pipe_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                       const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
                       const T* __restrict__ d_out, int64_t ld_d, const T* __restrict__ x,
-                      int64_t ld_x, int64_t n, T* values, T* velocity, T* grad_out,
-                      OptConsts<T> opt) {
-  using C = SddmmCfg<T, TILE>;
+                      int64_t ld_x, int64_t n, const T* values, T* values_out, T* velocity,
+                      T* grad_out, OptConsts<T> opt) {
+  using C = SddmmCfg<T, TILE, CH>;
   constexpr int S = C::STAGES, VW = C::VW, VPR = C::VPR, LDS = C::LDS;
+  constexpr int kChunk = C::kChunk;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
   __shared__ int32_t s_col[TILE];
@@ -234,8 +238,13 @@ __global__ void __launch_bounds__(TILE)
   const T g = (n == 0) ? T(0) : acc;  // tensor_core.py:283-284: zero batch -> zeros
   if (grad_out) grad_out[p] = g;
   if (opt.kind != SMB_OPT_NONE) {
-    T dummy = T(0);
-    apply_update(opt, g, values + p, velocity ? velocity + p : &dummy);
+    // read the pre-update value from `values`, write the result to
+    // `values_out` (== values for the in-place update)
+    T w = values[p];
+    T v = velocity ? velocity[p] : T(0);
+    apply_update(opt, g, &w, &v);
+    values_out[p] = w;
+    if (velocity) velocity[p] = v;
   }
 }
 
@@ -247,9 +256,10 @@ int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* v
 
 template <typename T>
 int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, const void* x,
-                      int64_t ld_x, int64_t n, void* values, void* velocity, void* grad_out,
-                      void* bias, void* vbias, void* grad_bias_out, int opt_kind, double mu,
-                      double eta, void* stream, const char* name) {
+                      int64_t ld_x, int64_t n, const void* values, void* values_out,
+                      void* velocity, void* grad_out, void* bias, void* vbias,
+                      void* grad_bias_out, int opt_kind, double mu, double eta, void* stream,
+                      const char* name) {
   const OptConsts<T> opt = make_opt<T>(opt_kind, mu, eta);
   cudaStream_t st = as_stream(stream);
   if (pat->ntiles > 0) {
@@ -263,18 +273,26 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       kernel<<<(unsigned)ceil_div(pat->nnz, tile), tile, bytes, st>>>(
           pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz,
           static_cast<const T*>(d_out), ld_d, static_cast<const T*>(x), ld_x, n,
-          static_cast<T*>(values), static_cast<T*>(velocity), static_cast<T*>(grad_out), opt);
+          static_cast<const T*>(values), static_cast<T*>(values_out), static_cast<T*>(velocity),
+          static_cast<T*>(grad_out), opt);
     };
     // every tile's d_out rows staged -> fallback-free kernel
     const bool all = (big ? pat->span512 : pat->span128) <= (big ? 512 : 128) / 4;
+    // a single wave of 128-tiles: the per-chain critical path sets the time,
+    // so take 32-column chunks (half the per-column barrier / copy overhead)
+    const bool one_wave = sizeof(T) == 4 && pat->ntiles <= 148;
     if (big) {
-      if (vec && all) go(sddmm_pipe_kernel<T, 512, true, true>, 512, SddmmCfg<T, 512>::smem_bytes);
-      else if (vec) go(sddmm_pipe_kernel<T, 512, true, false>, 512, SddmmCfg<T, 512>::smem_bytes);
-      else go(sddmm_pipe_kernel<T, 512, false, false>, 512, SddmmCfg<T, 512>::smem_bytes);
+      using C = SddmmCfg<T, 512, 16>;
+      if (vec && all) go(sddmm_pipe_kernel<T, 512, 16, true, true>, 512, C::smem_bytes);
+      else if (vec) go(sddmm_pipe_kernel<T, 512, 16, true, false>, 512, C::smem_bytes);
+      else go(sddmm_pipe_kernel<T, 512, 16, false, false>, 512, C::smem_bytes);
+    } else if (one_wave && vec && all) {
+      go(sddmm_pipe_kernel<T, 128, 32, true, true>, 128, SddmmCfg<T, 128, 32>::smem_bytes);
     } else {
-      if (vec && all) go(sddmm_pipe_kernel<T, 128, true, true>, 128, SddmmCfg<T, 128>::smem_bytes);
-      else if (vec) go(sddmm_pipe_kernel<T, 128, true, false>, 128, SddmmCfg<T, 128>::smem_bytes);
-      else go(sddmm_pipe_kernel<T, 128, false, false>, 128, SddmmCfg<T, 128>::smem_bytes);
+      using C = SddmmCfg<T, 128, 16>;
+      if (vec && all) go(sddmm_pipe_kernel<T, 128, 16, true, true>, 128, C::smem_bytes);
+      else if (vec) go(sddmm_pipe_kernel<T, 128, 16, true, false>, 128, C::smem_bytes);
+      else go(sddmm_pipe_kernel<T, 128, 16, false, false>, 128, C::smem_bytes);
     }
     const int rc = check_launch(name);
     if (rc != SMB_OK) return rc;
@@ -296,13 +314,13 @@ extern "C" int smb_sddmm(int dtype, const smb_pattern* pat, const void* a, int64
   SMB_REQUIRE(n >= 0 && lda >= n && ldb >= n, "smb_sddmm: bad batch width / leading dimension");
   SMB_REQUIRE(pat->nnz == 0 || out_values != nullptr, "smb_sddmm: null output");
   if (dtype == SMB_F32)
-    return sddmm_update_impl<float>(pat, a, lda, b, ldb, n, nullptr, nullptr, out_values, nullptr,
-                                    nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0, stream,
+    return sddmm_update_impl<float>(pat, a, lda, b, ldb, n, nullptr, nullptr, nullptr, out_values,
+                                    nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0, stream,
                                     "smb_sddmm");
   if (dtype == SMB_F64)
-    return sddmm_update_impl<double>(pat, a, lda, b, ldb, n, nullptr, nullptr, out_values,
-                                     nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0, stream,
-                                     "smb_sddmm");
+    return sddmm_update_impl<double>(pat, a, lda, b, ldb, n, nullptr, nullptr, nullptr,
+                                     out_values, nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0,
+                                     stream, "smb_sddmm");
   set_error("smb_sddmm: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
 }
@@ -312,8 +330,21 @@ extern "C" int smb_sddmm_update(int dtype, const smb_pattern* pat, const void* d
                                 void* values, void* velocity, void* grad_out, void* bias,
                                 void* velocity_bias, void* grad_bias_out, int opt_kind, double mu,
                                 double eta, void* stream) {
+  return smb_sddmm_update_into(dtype, pat, d_out, ld_dout, x, ld_x, n, values, values, velocity,
+                               grad_out, bias, velocity_bias, grad_bias_out, opt_kind, mu, eta,
+                               stream);
+}
+
+extern "C" int smb_sddmm_update_into(int dtype, const smb_pattern* pat, const void* d_out,
+                                     int64_t ld_dout, const void* x, int64_t ld_x, int64_t n,
+                                     const void* values, void* values_out, void* velocity,
+                                     void* grad_out, void* bias, void* velocity_bias,
+                                     void* grad_bias_out, int opt_kind, double mu, double eta,
+                                     void* stream) {
   clear_error();
   SMB_REQUIRE(pat != nullptr, "smb_sddmm_update: null pattern");
+  SMB_REQUIRE(opt_kind == SMB_OPT_NONE || values_out != nullptr || pat->nnz == 0,
+              "smb_sddmm_update: null output values");
   SMB_REQUIRE(n >= 0 && ld_dout >= n && ld_x >= n,
               "smb_sddmm_update: bad batch width / leading dimension");
   SMB_REQUIRE(opt_kind >= SMB_OPT_NONE && opt_kind <= SMB_OPT_NESTEROV,
@@ -327,13 +358,13 @@ extern "C" int smb_sddmm_update(int dtype, const smb_pattern* pat, const void* d
                   velocity_bias != nullptr,
               "smb_sddmm_update: momentum needs a bias velocity buffer");
   if (dtype == SMB_F32)
-    return sddmm_update_impl<float>(pat, d_out, ld_dout, x, ld_x, n, values, velocity, grad_out,
-                                    bias, velocity_bias, grad_bias_out, opt_kind, mu, eta, stream,
-                                    "smb_sddmm_update");
+    return sddmm_update_impl<float>(pat, d_out, ld_dout, x, ld_x, n, values, values_out, velocity,
+                                    grad_out, bias, velocity_bias, grad_bias_out, opt_kind, mu,
+                                    eta, stream, "smb_sddmm_update");
   if (dtype == SMB_F64)
-    return sddmm_update_impl<double>(pat, d_out, ld_dout, x, ld_x, n, values, velocity, grad_out,
-                                     bias, velocity_bias, grad_bias_out, opt_kind, mu, eta,
-                                     stream, "smb_sddmm_update");
+    return sddmm_update_impl<double>(pat, d_out, ld_dout, x, ld_x, n, values, values_out,
+                                     velocity, grad_out, bias, velocity_bias, grad_bias_out,
+                                     opt_kind, mu, eta, stream, "smb_sddmm_update");
   set_error("smb_sddmm_update: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
 }

@@ -104,7 +104,8 @@ def flat_layout(units):
 
 
 class _Unit:
-    __slots__ = ("layer", "relu", "sparse", "m", "k", "grad_off", "bias_off", "nvals", "index")
+    __slots__ = ("layer", "relu", "sparse", "m", "k", "grad_off", "bias_off", "nvals", "index",
+                 "vals")
 
     def __init__(self, layer, relu, index=0):
         self.index = index
@@ -166,6 +167,19 @@ class FusedTrainStep:
             self.flat = torch.zeros(total, dtype=f32, device=dev)
         self._graphs = {}
         self.timer = None  # optional KernelTimer: per-launch CUDA events (eager only)
+        # Single-GPU steps run each sparse layer's SDDMM+update on a side
+        # stream, concurrently with the transposed-SpMM chain.  The update
+        # writes the second of two value buffers (ping-pong), so the
+        # transposed SpMM of the same layer keeps reading the pre-update
+        # weights (train.py:400-401); `parity` selects the current buffer.
+        self.overlap = self.world == 1
+        self._parity = 0
+        self._side = None
+        for u in self.units:
+            u.vals = None
+            if u.sparse and self.overlap:
+                cur = u.layer.weights.values
+                u.vals = [cur, cur.clone()]
 
     def _call(self, tag: str, name: str, *args) -> None:
         t = self.timer
@@ -268,13 +282,23 @@ class FusedTrainStep:
                    ptr(self.loss), b, vb, gb, kind, mu, float(eta),
                    ptr(self.counter) if gather else None, int(self.steps_per_epoch),
                    ptr(self._ce_ws), st)
-        # backward, last layer first: d_{l-1} (+ bias side of layer l-1), then
-        # the weight side of layer l (spmm_t reads the pre-update W_l)
+        # backward, last layer first: d_{l-1} (+ bias side of layer l-1) on the
+        # main stream; the weight side of layer l (SDDMM + update) either
+        # follows it in order, or -- single GPU -- runs on the side stream as
+        # soon as d_l exists, writing the other value buffer (spmm_t keeps
+        # reading the pre-update W_l, train.py:400-401)
+        overlap = self.overlap and fuse_update
+        main = torch.cuda.current_stream()
+        side = self._side_stream() if overlap else None
         for li in range(len(self.units) - 1, -1, -1):
             u = self.units[li]
             lay = u.layer
             dy = self.dys[li]
             x_prev = self.acts[li - 1] if li > 0 else x_in
+            if overlap and u.sparse:
+                side.wait_stream(main)  # d_l is ready
+                with torch.cuda.stream(side):
+                    self._weight_side(u, dy, x_prev, eta, fuse_update, stream_ptr())
             if li > 0:
                 below = self.units[li - 1]
                 mask = self.acts[li - 1] if below.relu else None
@@ -282,7 +306,7 @@ class FusedTrainStep:
                 b, vb, gb, kind, mu = self._bias_target(below, fuse_update)
                 if u.sparse:
                     self._call(f"spmm_t[{li}]", "smb_spmm_t_bias", F32, lay.weights.pattern.handle,
-                               ptr(lay.weights.values), ptr(dy), ld, B, ptr(mask),
+                               ptr(self._vals(u)), ptr(dy), ld, B, ptr(mask),
                                ld if mask is not None else 0, ptr(dst), ld, b, vb, gb, kind, mu,
                                float(eta), st)
                 else:
@@ -293,7 +317,29 @@ class FusedTrainStep:
                                    ptr(mask), ld, u.k, B, ptr(dst), ld, st)
                     self._call(f"bias[{li - 1}]", "smb_bias_grad_update", F32, ptr(dst), ld, u.k,
                                B, b, vb, gb, kind, mu, float(eta), st)
-            self._weight_side(u, dy, x_prev, eta, fuse_update, st)
+            if not (overlap and u.sparse):
+                self._weight_side(u, dy, x_prev, eta, fuse_update, st)
+        if overlap:
+            main.wait_stream(side)  # join: the step ends when every update has
+
+    def _side_stream(self):
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.dev)
+        return self._side
+
+    def _vals(self, u):
+        """The current (pre-update) value buffer of sparse unit u."""
+        return u.vals[self._parity] if u.vals is not None else u.layer.weights.values
+
+    def _flip_parity(self) -> None:
+        """After an overlapped step the updated weights live in the other
+        buffer: point the layer's CsrMatrix at it."""
+        if not self.overlap:
+            return
+        self._parity ^= 1
+        for u in self.units:
+            if u.vals is not None:
+                u.layer.weights.values = u.vals[self._parity]
 
     def _weight_side(self, u, dy, x_prev, eta, fuse_update, st):
         lay = u.layer
@@ -304,9 +350,11 @@ class FusedTrainStep:
         if u.sparse:
             vel = lay.velocity.values if lay.velocity is not None else None
             g_out = None if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals]
-            self._call(f"sddmm_update[{u.index}]", "smb_sddmm_update", F32,
+            w_in = self._vals(u)
+            w_out = u.vals[self._parity ^ 1] if (u.vals is not None and fuse_update) else w_in
+            self._call(f"sddmm_update[{u.index}]", "smb_sddmm_update_into", F32,
                        lay.weights.pattern.handle, ptr(dy), ld, ptr(x_prev), ld, B,
-                       ptr(lay.weights.values), ptr(vel), ptr(g_out), None, None, None, kind,
+                       ptr(w_in), ptr(w_out), ptr(vel), ptr(g_out), None, None, None, kind,
                        float(opt.mu), float(eta), st)
             return
         # dense layer: cuBLAS FP32 weight gradient + exact update
@@ -360,6 +408,7 @@ class FusedTrainStep:
         self._slot = 0 if gather else int(slot)
         if self.world == 1:
             self._replay_or_run(eta, gather, "all")
+            self._flip_parity()
             return
         import torch.distributed as dist
 
@@ -371,7 +420,7 @@ class FusedTrainStep:
         if not self.use_graph:
             self._run_eager(eta, gather, part)
             return
-        key = (float(eta), gather, part, self._slot)
+        key = (float(eta), gather, part, self._slot, self._parity)
         g = self._graphs.get(key)
         if g is None:
             # the first execution is eager (initialises cuBLAS handles and
