@@ -89,27 +89,44 @@ __global__ void __launch_bounds__(1024)
   T* stage_dst =
       reinterpret_cast<T*>(smem_raw) + (blockDim.x >> 5) * warp_pairwise_leaves((int)n);
   double local = 0.0;
+  // bias state of row `warp` (the first row this warp sums), loaded now
+  T pb_w = T(0), pb_v = T(0);
+  if ((threadIdx.x & 31) == 0 && (int64_t)(threadIdx.x >> 5) < classes && bias &&
+      opt.kind != SMB_OPT_NONE) {
+    pb_w = bias[threadIdx.x >> 5];
+    if (vbias) pb_v = vbias[threadIdx.x >> 5];
+  }
   for (int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; col < n;
        col += (int64_t)gridDim.x * blockDim.x) {
-    T mx = y[col];
-    for (int64_t c = 1; c < classes; ++c) {
-      const T v = y[c * ld_y + col];
-      mx = (v > mx || v != v) ? v : mx;
-    }
     T s = T(0), zt = T(0);
-    constexpr int kRegC = 16;  // e kept in registers for up to 16 classes
-    T er[kRegC];
+    constexpr int kRegC = 16;  // the column kept in registers for <= 16 classes
+    T er[kRegC], tr[kRegC];
     if (classes <= kRegC) {
+      // all loads of the column issued back to back (one memory round trip)
+#pragma unroll
+      for (int c = 0; c < kRegC; ++c) {
+        er[c] = c < classes ? y[c * ld_y + col] : T(0);
+        tr[c] = c < classes ? t[c * ld_t + col] : T(0);
+      }
+      T mx = er[0];
+#pragma unroll
+      for (int c = 1; c < kRegC; ++c)
+        if (c < classes) mx = (er[c] > mx || er[c] != er[c]) ? er[c] : mx;
 #pragma unroll
       for (int c = 0; c < kRegC; ++c) {
         if (c < classes) {
-          const T z = sub_rn(y[c * ld_y + col], mx);
+          const T z = sub_rn(er[c], mx);
           er[c] = exp_full(z);
           s = add_rn(s, er[c]);
-          zt = add_rn(zt, mul_rn(z, t[c * ld_t + col]));
+          zt = add_rn(zt, mul_rn(z, tr[c]));
         }
       }
     } else {
+      T mx = y[col];
+      for (int64_t c = 1; c < classes; ++c) {
+        const T v = y[c * ld_y + col];
+        mx = (v > mx || v != v) ? v : mx;
+      }
       for (int64_t c = 0; c < classes; ++c) {
         const T z = sub_rn(y[c * ld_y + col], mx);
         const T e = exp_full(z);
@@ -118,8 +135,8 @@ __global__ void __launch_bounds__(1024)
         zt = add_rn(zt, mul_rn(z, t[c * ld_t + col]));
       }
     }
-    auto emit = [&](int64_t c, T e) {
-      const T g = div_rn(sub_rn(div_rn(e, s), t[c * ld_t + col]), divisor);
+    auto emit = [&](int64_t c, T e, T tc) {
+      const T g = div_rn(sub_rn(div_rn(e, s), tc), divisor);
       dy[c * ld_dy + col] = g;
       // single CTA: keep the block in shared memory for the bias row sums
       if (stage_rows && gridDim.x == 1) stage_dst[c * n + col] = g;
@@ -127,9 +144,9 @@ __global__ void __launch_bounds__(1024)
     if (classes <= kRegC) {
 #pragma unroll
       for (int c = 0; c < kRegC; ++c)
-        if (c < classes) emit(c, er[c]);
+        if (c < classes) emit(c, er[c], tr[c]);
     } else {
-      for (int64_t c = 0; c < classes; ++c) emit(c, dy[c * ld_dy + col]);
+      for (int64_t c = 0; c < classes; ++c) emit(c, dy[c * ld_dy + col], t[c * ld_t + col]);
     }
     local += static_cast<double>(sub_rn(log_full(s), zt));
   }
@@ -152,7 +169,7 @@ __global__ void __launch_bounds__(1024)
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
+  if (gridDim.x > 1) __threadfence();
   if (threadIdx.x == 0 && gridDim.x > 1) {
     double tot = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) tot += loss_parts[b];
@@ -195,8 +212,11 @@ __global__ void __launch_bounds__(1024)
     if (lane == 0) {
       if (grad_bias) grad_bias[c] = g;
       if (opt.kind != SMB_OPT_NONE && bias) {
-        T dummy = T(0);
-        apply_update(opt, g, bias + c, vbias ? vbias + c : &dummy);
+        T w = c == warp ? pb_w : bias[c];
+        T v = c == warp ? pb_v : (vbias ? vbias[c] : T(0));
+        apply_update(opt, g, &w, &v);
+        bias[c] = w;
+        if (vbias) vbias[c] = v;
       }
     }
   }

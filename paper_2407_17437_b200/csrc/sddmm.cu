@@ -13,7 +13,7 @@
 // Mapping: one CTA = TILE (128 or 512) consecutive nonzeros of the CSR order,
 // one per thread, each running ONE sequential accumulation chain (required
 // for bit-exactness; the FADD latency is hidden by having 16 warps of
-// independent chains per SM).  The batch is walked in 16-column chunks
+// independent chains per SM).  The batch is walked in 32/64-column chunks
 // through a STAGES-deep ring in shared memory, filled with 16-byte cp.async
 // (LDGSTS) copies of the gathered x rows and of the few d_out rows the tile
 // touches; one barrier per chunk.  Every thread owns a fixed set of copy
@@ -30,20 +30,18 @@ namespace smb {
 namespace {
 
 // TILE nonzeros per CTA, CH batch columns per pipeline stage
-template <typename T, int TILE, int CH>
+template <typename T, int TILE, int CH, int ST>
 struct SddmmCfg {
   static constexpr int kChunk = CH;
   static constexpr int VW = 16 / sizeof(T);  // elements per 16 B
   static constexpr int LDS = kChunk + VW;    // padded smem row (elements)
   static constexpr int VPR = kChunk / VW;    // 16 B vectors per staged row
   static constexpr int SLOTS = TILE / 4;  // staged d_out rows per tile
-  // power-of-two ring (stage = chunk & (STAGES-1)); fp32:
-  //   512-tile x 16 cols x 4 stages = 200 KB (1 CTA, 16 warps / SM),
-  //   128-tile x 16 cols x 8 stages = 102 KB (2 CTAs / SM),
-  //   128-tile x 32 cols x 8 stages = 184 KB (1 CTA / SM: single-wave layers,
-  //   where the per-chain critical path, not throughput, sets the time);
-  //   fp64 128-tile x 16 cols x 4 = 92 KB
-  static constexpr int STAGES = TILE >= 512 ? 4 : (sizeof(T) == 4 ? 8 : 4);
+  // power-of-two ring (stage = chunk & (STAGES-1)); defaults:
+  //   fp32 512-tile x 32 cols x 2 stages = 184 KB (1 CTA, 16 warps / SM),
+  //   fp32 128-tile x 64 cols x 2 stages =  87 KB (2 CTAs / SM),
+  //   fp64 128-tile x 16 cols x 4 stages =  92 KB
+  static constexpr int STAGES = ST;
   static_assert((STAGES & (STAGES - 1)) == 0, "power-of-two ring");
   static constexpr size_t stage_elems = size_t(TILE + SLOTS) * LDS;
   static constexpr size_t smem_bytes = STAGES * stage_elems * sizeof(T);
@@ -107,14 +105,14 @@ __device__ __forceinline__ void copy_vec(unsigned dst, const T* src, int valid_e
 
 // ALL: every tile's d_out rows fit the SLOTS staging rows (checked on the
 // host from the pattern's tile spans), so the hot loop has no fallback path.
-template <typename T, int TILE, int CH, bool VEC, bool ALL>
+template <typename T, int TILE, int CH, int ST, bool VEC, bool ALL>
 __global__ void __launch_bounds__(TILE)
     sddmm_pipe_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                       const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
                       const T* __restrict__ d_out, int64_t ld_d, const T* __restrict__ x,
                       int64_t ld_x, int64_t n, const T* values, T* values_out, T* velocity,
                       T* grad_out, OptConsts<T> opt) {
-  using C = SddmmCfg<T, TILE, CH>;
+  using C = SddmmCfg<T, TILE, CH, ST>;
   constexpr int S = C::STAGES, VW = C::VW, VPR = C::VPR, LDS = C::LDS;
   constexpr int kChunk = C::kChunk;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -133,7 +131,9 @@ __global__ void __launch_bounds__(TILE)
   __syncthreads();
   const int64_t row = tile_row_of<TILE>(p, r0, s_rp, row_ptr, m);
   const int slot = (int)imin(row - r0, C::SLOTS);  // SLOTS == "not staged"
-  const int n_staged = (int)imin(C::SLOTS, m - r0);
+  // only the rows this tile actually touches (r0 .. row of its last nonzero)
+  const int64_t last_row = tile_row_of<TILE>(p0 + n_active - 1, r0, s_rp, row_ptr, m);
+  const int n_staged = (int)imin(C::SLOTS, last_row - r0 + 1);
   // batch widths are far below 2^31: all chunk / column arithmetic is 32-bit
   const int n32 = (int)n;
   const int n_chunks = (n32 + kChunk - 1) / kChunk;
@@ -276,24 +276,37 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
           static_cast<const T*>(values), static_cast<T*>(values_out), static_cast<T*>(velocity),
           static_cast<T*>(grad_out), opt);
     };
-    // every tile's d_out rows staged -> fallback-free kernel
-    const bool all = (big ? pat->span512 : pat->span128) <= (big ? 512 : 128) / 4;
-    // a single wave of 128-tiles: the per-chain critical path sets the time,
-    // so take 32-column chunks (half the per-column barrier / copy overhead)
-    const bool one_wave = sizeof(T) == 4 && pat->ntiles <= 148;
-    if (big) {
-      using C = SddmmCfg<T, 512, 16>;
-      if (vec && all) go(sddmm_pipe_kernel<T, 512, 16, true, true>, 512, C::smem_bytes);
-      else if (vec) go(sddmm_pipe_kernel<T, 512, 16, true, false>, 512, C::smem_bytes);
-      else go(sddmm_pipe_kernel<T, 512, 16, false, false>, 512, C::smem_bytes);
-    } else if (one_wave && vec && all) {
-      go(sddmm_pipe_kernel<T, 128, 32, true, true>, 128, SddmmCfg<T, 128, 32>::smem_bytes);
-    } else {
-      using C = SddmmCfg<T, 128, 16>;
-      if (vec && all) go(sddmm_pipe_kernel<T, 128, 16, true, true>, 128, C::smem_bytes);
-      else if (vec) go(sddmm_pipe_kernel<T, 128, 16, true, false>, 128, C::smem_bytes);
-      else go(sddmm_pipe_kernel<T, 128, 16, false, false>, 128, C::smem_bytes);
-    }
+    // every tile's d_out rows staged -> fallback-free kernel (a 256-tile's
+    // span is bounded by its enclosing 512-tile's)
+    auto all_for = [&](int tile) {
+      return (tile == 128 ? pat->span128 : pat->span512) <= tile / 4;
+    };
+    static const int variant = [] {
+      const char* e = getenv("SMB_SDDMM_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
+#define SMB_GO(TL, CHK, STG)                                                              \
+  do {                                                                                     \
+    using C = SddmmCfg<T, TL, CHK, STG>;                                                   \
+    const bool all = all_for(TL);                                                          \
+    if (vec && all) go(sddmm_pipe_kernel<T, TL, CHK, STG, true, true>, TL, C::smem_bytes);  \
+    else if (vec) go(sddmm_pipe_kernel<T, TL, CHK, STG, true, false>, TL, C::smem_bytes);   \
+    else go(sddmm_pipe_kernel<T, TL, CHK, STG, false, false>, TL, C::smem_bytes);           \
+  } while (0)
+    // Double-buffered wide chunks: 64 columns for layers below one 512-tile
+    // wave, 32 columns (184 KB) for 512-tiles.  Measured on B200 against
+    // 16/32-column chunks with 4-8 stages (env SMB_SDDMM_VARIANT): the
+    // per-chunk barrier + copy issue, not the copy latency, dominated.
+    if (sizeof(T) == 4 && !big && variant == 1) SMB_GO(128, 32, 4);
+    else if (sizeof(T) == 4 && !big && variant == 3) SMB_GO(128, 32, 2);
+    else if (sizeof(T) == 4 && !big && variant == 4) SMB_GO(128, 16, 8);
+    else if (sizeof(T) == 4 && !big && variant == 5) SMB_GO(128, 64, 4);
+    else if (sizeof(T) == 4 && big && variant == 6) SMB_GO(512, 16, 4);
+    else if (sizeof(T) == 4 && big && variant == 7) SMB_GO(256, 64, 2);
+    else if (big) SMB_GO(512, 32, 2);
+    else if (sizeof(T) == 4) SMB_GO(128, 64, 2);
+    else SMB_GO(128, 16, 4);
+#undef SMB_GO
     const int rc = check_launch(name);
     if (rc != SMB_OK) return rc;
   }

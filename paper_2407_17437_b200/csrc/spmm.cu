@@ -147,10 +147,28 @@ __global__ void __launch_bounds__(max_threads_for<W>())
       gv = PERM ? vals[perm[s]] : vals[s];
     }
   };
-  int idx_c, idx_n;
-  T val_c, val_n;
+  // three groups in registers: current, next (refill targets) and the one
+  // after, whose load then has a whole group's time to land
+  int idx_c, idx_n, idx_nn;
+  T val_c, val_n, val_nn;
   load_group(0, idx_c, val_c);
   load_group(1, idx_n, val_n);
+  load_group(2, idx_nn, val_nn);
+  // epilogue operands that do not depend on the product: issue them now
+  T bias_r = T(0);
+  if constexpr (EPI == kEpiBiasAct) {
+    if (epi.bias != nullptr) bias_r = epi.bias[row];
+  }
+  Frag<T, W> mk;
+  T rb_w = T(0), rb_v = T(0);  // bias state of the fused row-sum update
+  if constexpr (EPI == kEpiMask) {
+    if (epi.mask != nullptr && valid > 0)
+      load_frag<T, W>(mk, epi.mask + row * epi.ld_mask + col0, valid);
+    if (epi.rowsum && threadIdx.x == 0 && epi.opt.kind != SMB_OPT_NONE && epi.rb_bias) {
+      rb_w = epi.rb_bias[row];
+      if (epi.rb_vbias) rb_v = epi.rb_vbias[row];
+    }
+  }
   // lanes with 0 < valid < W (the batch tail) need element-wise loads
   const bool lane_full = valid == W || valid == 0;
   auto refill = [&](Frag<T, W>& f, int src) {
@@ -195,15 +213,16 @@ __global__ void __launch_bounds__(max_threads_for<W>())
     }
     idx_c = idx_n;
     val_c = val_n;
-    load_group(g + 2, idx_n, val_n);
+    idx_n = idx_nn;
+    val_n = val_nn;
+    load_group(g + 3, idx_nn, val_nn);
   }
 
   if constexpr (EPI == kEpiBiasAct) {
     if (valid == 0) return;
     if (epi.bias != nullptr) {
-      const T b = epi.bias[row];
 #pragma unroll
-      for (int j = 0; j < W; ++j) acc.v[j] = add_rn(acc.v[j], b);
+      for (int j = 0; j < W; ++j) acc.v[j] = add_rn(acc.v[j], bias_r);
     }
     if (epi.relu) {
 #pragma unroll
@@ -213,8 +232,6 @@ __global__ void __launch_bounds__(max_threads_for<W>())
   } else {
     if (valid > 0) {
       if (epi.mask != nullptr) {
-        Frag<T, W> mk;
-        load_frag<T, W>(mk, epi.mask + row * epi.ld_mask + col0, valid);
 #pragma unroll
         for (int j = 0; j < W; ++j) acc.v[j] = mask_np(acc.v[j], mk.v[j]);
       }
@@ -233,8 +250,9 @@ __global__ void __launch_bounds__(max_threads_for<W>())
       if (lane == 0) {
         if (epi.rb_grad) epi.rb_grad[row] = g;
         if (epi.opt.kind != SMB_OPT_NONE && epi.rb_bias) {
-          T dummy = T(0);
-          apply_update(epi.opt, g, epi.rb_bias + row, epi.rb_vbias ? epi.rb_vbias + row : &dummy);
+          apply_update(epi.opt, g, &rb_w, &rb_v);
+          epi.rb_bias[row] = rb_w;
+          if (epi.rb_vbias) epi.rb_vbias[row] = rb_v;
         }
       }
     }

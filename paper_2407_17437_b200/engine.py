@@ -252,12 +252,24 @@ class FusedTrainStep:
         B, ld = self.B, self.ld
         F32 = _lib.SMB_F32
         x_in, t_in = self.x_slots[self._slot], self.t_slots[self._slot]
+        overlap = self.overlap and fuse_update
+        main = torch.cuda.current_stream()
+        side = self._side_stream() if overlap else None
         if gather:
             d = self.data
             self._call("gather", "smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features,
                        ptr(self.perm), ptr(self.counter), 0, B, ptr(x_in), ld, st)
-            self._call("gather", "smb_gather_columns", F32, ptr(d.T), d.n_samples, d.classes,
-                       ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in), ld, st)
+            if overlap:
+                # the label batch is only read by the softmax step: gather it
+                # beside the forward chain
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples,
+                               d.classes, ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in),
+                               ld, stream_ptr())
+            else:
+                self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples,
+                           d.classes, ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in), ld, st)
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
         for li, (u, a) in enumerate(zip(self.units, self.acts)):
@@ -277,6 +289,8 @@ class FusedTrainStep:
         # applies the last layer's bias side and advances the step counter
         top = self.units[-1]
         b, vb, gb, kind, mu = self._bias_target(top, fuse_update)
+        if gather and overlap:
+            main.wait_stream(side)  # label batch gathered
         self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
                    ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]), ld,
                    ptr(self.loss), b, vb, gb, kind, mu, float(eta),
@@ -287,9 +301,6 @@ class FusedTrainStep:
         # follows it in order, or -- single GPU -- runs on the side stream as
         # soon as d_l exists, writing the other value buffer (spmm_t keeps
         # reading the pre-update W_l, train.py:400-401)
-        overlap = self.overlap and fuse_update
-        main = torch.cuda.current_stream()
-        side = self._side_stream() if overlap else None
         for li in range(len(self.units) - 1, -1, -1):
             u = self.units[li]
             lay = u.layer
