@@ -57,6 +57,8 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="budget of the bounded CPU-baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="sparse", choices=["sparse", "masked"],
+                    help="masked = the masked-dense baseline (MaskedDense, cuBLAS FP32)")
     ap.add_argument("--sweep", action="store_true",
                     help="also report the config-2 density sweep (B=100 and 1024)")
     return ap.parse_args()
@@ -84,6 +86,16 @@ def measured_peaks():
         except Exception:
             pass
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def fp32_peak_tflops() -> float:
+    """FFMA peak measured on a B200 by scripts/fp32_peak.cu (profiles/fp32_peak.json);
+    the separately rounded mul+add the bit-exact kernels use runs at half of it."""
+    p = REPO / "profiles" / "fp32_peak.json"
+    try:
+        return float(json.loads(p.read_text())["fp32_ffma_tflops"])
+    except Exception:
+        return 74.4  # 148 SMs x 128 lanes x 2 flop x 1.965 GHz
 
 
 class ClockSampler:
@@ -160,7 +172,8 @@ def dist_env():
 
 def config_dict(args, ws):
     return {"workload": f"configs[1] point: MLP {args.layers.replace(',', '-')} ER d={args.density} "
-                        f"B={args.batch}/GPU fp32 Nesterov lr={args.lr}",
+                        f"B={args.batch}/GPU fp32 Nesterov lr={args.lr}"
+                        + ("" if args.backend == "sparse" else f" backend={args.backend}"),
             "layers": [int(x) for x in args.layers.split(",")], "density": args.density,
             "batch_per_gpu": args.batch, "global_batch": args.batch * ws,
             "train_samples": args.samples, "parallelism": f"dp{ws}",
@@ -176,7 +189,7 @@ def cpu_step_sample(args, global_batch, budget_s, min_steps=3, max_steps=200):
     threads = os.cpu_count() or 1
     O.set_threads(threads)
     chain = [int(x) for x in args.layers.split(",")]
-    ref = O.OracleMLP.build(chain, args.density, seed=args.seed)
+    ref = O.OracleMLP.build(chain, args.density, seed=args.seed, backend=args.backend)
     rng = np.random.default_rng(args.seed + 17)
     x = rng.standard_normal((chain[0], global_batch), dtype=np.float32)
     lab = rng.integers(0, chain[-1], global_batch)
@@ -203,7 +216,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     O.set_threads(threads)
     chain = [int(x) for x in args.layers.split(",")]
-    ref = O.OracleMLP.build(chain, args.density, seed=args.seed)
+    ref = O.OracleMLP.build(chain, args.density, seed=args.seed, backend=args.backend)
     rng = np.random.default_rng(args.seed + 17)
     x = rng.standard_normal((chain[0], gb), dtype=np.float32)
     lab = rng.integers(0, chain[-1], gb)
@@ -248,7 +261,7 @@ def run_ours(args):
     chain = [int(x) for x in args.layers.split(",")]
     B, gb = args.batch, args.batch * ws
     cfg = smb.ExperimentConfig(layer_dims=chain, density=args.density, batch_size=B, lr=args.lr,
-                               seed=args.seed)
+                               seed=args.seed, backend=args.backend)
     model, plan = smb.build_model(cfg)
     data = smb.synthetic_dataset(seed=args.seed, n_samples=args.samples, features=chain[0],
                                  classes=chain[-1])
@@ -319,15 +332,18 @@ def run_ours(args):
     b2b_ms = max_over_ranks(s_ev.elapsed_time(e_ev))
 
     # ---- per-kernel spans (eager, GPU held while the step is enqueued) ----
+    # kernels serialised (no side-stream overlap) so each span is that
+    # kernel's own duration
     timer = KernelTimer()
     step.timer, step.use_graph = timer, False
+    overlap_saved, step.overlap = step.overlap, False
     nk = min(10, args.steps)
     for i in range(nk):
         flush.fill_(float(i))
         KernelTimer.hold_gpu()
         step.step(eta)
     summ = timer.summary()
-    step.timer, step.use_graph = None, True
+    step.timer, step.use_graph, step.overlap = None, True, overlap_saved
     units = step.units
     best = None
     kernels = {}
@@ -357,10 +373,17 @@ def run_ours(args):
                     f"{args.layers}|{args.density}|{B}|{tag}")
             except Exception:
                 traffic = None
-        roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+        # t_roof = max(bytes / HBM, flops / FP32 peak)
+        flops = 2 * u.nvals * B
+        fp32 = fp32_peak_tflops()
+        t_bytes, t_flops = b / (hbm * 1e9), flops / (fp32 * 1e12)
+        roofline = {"bound": "hbm" if t_bytes >= t_flops else "fp32",
+                    "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4), "traffic": traffic, "kernel": tag,
-                    "kernel_us": round(us, 2), "algorithmic_bytes": b,
-                    "peak_source": peak_src,
+                    "kernel_us": round(us, 2), "algorithmic_bytes": b, "flops": flops,
+                    "peak_source": peak_src, "fp32_peak_tflops": fp32,
+                    "t_roof_us": round(1e6 * max(t_bytes, t_flops), 3),
+                    "roof_frac": round(max(t_bytes, t_flops) / (us * 1e-6), 4),
                     "pairs_per_s": round(u.nvals * B / (us * 1e-6), 1)}
 
     # ---- end to end through the public API: pinned host batches ----
@@ -425,28 +448,37 @@ def density_sweep(args, steps=20):
                                  classes=chain[-1])
     ddata = smb.DeviceDataset(data)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    def time_backend(d, B, backend):
+        model, plan = smb.build_model(smb.ExperimentConfig(
+            layer_dims=chain, density=d, batch_size=B, lr=args.lr, seed=args.seed,
+            backend=backend))
+        st = smb.FusedTrainStep(model, B)
+        st.attach_dataset(ddata)
+        st.set_epoch(np.random.default_rng(0).permutation(20_480))
+        for _ in range(3):
+            st.step(args.lr)
+        tot = 0.0
+        for i in range(steps):
+            flush.fill_(float(i))
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            st.step(args.lr)
+            e.record()
+            e.synchronize()
+            tot += s.elapsed_time(e)
+        del st, model
+        return plan, tot / steps
+
     out = []
     for B in (100, 1024):
         for d in (0.001, 0.005, 0.01, 0.05, 0.1, 0.2, 0.5):
-            model, plan = smb.build_model(smb.ExperimentConfig(
-                layer_dims=chain, density=d, batch_size=B, lr=args.lr, seed=args.seed))
-            st = smb.FusedTrainStep(model, B)
-            st.attach_dataset(ddata)
-            st.set_epoch(np.random.default_rng(0).permutation(20_480))
-            for _ in range(3):
-                st.step(args.lr)
-            tot = 0.0
-            for i in range(steps):
-                flush.fill_(float(i))
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record()
-                st.step(args.lr)
-                e.record()
-                e.synchronize()
-                tot += s.elapsed_time(e)
+            plan, ms = time_backend(d, B, "sparse")
+            _, ms_m = time_backend(d, B, "masked")
             out.append({"density": d, "batch": B, "nnz": sum(plan.layer_nnz),
-                        "ms_per_step": round(tot / steps, 4),
-                        "samples_per_s": round(B * steps / (tot / 1e3), 1)})
+                        "ms_per_step": round(ms, 4),
+                        "samples_per_s": round(B / (ms / 1e3), 1),
+                        "masked_ms_per_step": round(ms_m, 4),
+                        "sparse_vs_masked": round(ms_m / ms, 3)})
     return out
 
 

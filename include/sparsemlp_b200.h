@@ -191,6 +191,14 @@ SMB_API int smb_bias_grad_update(int dtype, const void* d_out, int64_t ld, int64
 SMB_API int smb_optimizer_step(int dtype, void* param, void* velocity, const void* grad, int64_t count,
                        int opt_kind, double mu, double eta, void* stream);
 
+/* Masked-dense baseline update, DenseLinearLayer.optimize with a mask
+ * (nn.py:258-264, gradient masked as in backward nn.py:255-256):
+ * g' = grad*mask, velocity *= mask, _step_vector(param, g', velocity),
+ * param *= mask -- one pass over count elements. */
+SMB_API int smb_masked_optimizer_step(int dtype, void* param, void* velocity, const void* grad,
+                                      const void* mask, int64_t count, int opt_kind, double mu,
+                                      double eta, void* stream);
+
 /* out[i] = sum_t dense[i, t] in numpy's pairwise order (tensor_core.row_sums,
  * tensor_core.py:353-356). */
 SMB_API int smb_row_sums(int dtype, const void* dense, int64_t m, int64_t n, int64_t ld, void* out,

@@ -286,6 +286,7 @@ class Layer:
         self.vel = np.zeros_like(self.values)
         self.vbias = np.zeros_like(self.bias)
         self.mu, self.nesterov = mu, nesterov
+        self.mask = None  # masked-dense baseline: [n_out*n_in] 0/1 (nn.py:201-264)
 
     @property
     def W(self):
@@ -301,8 +302,11 @@ class OracleMLP:
         self.streams = Streams(seed)
 
     @classmethod
-    def build(cls, chain, density, seed=0, momentum=0.9, nesterov=True, dtype=np.float32):
-        """bench.build_model + Sequential.compile (bench.py:127-151, train.py:136-188)."""
+    def build(cls, chain, density, seed=0, momentum=0.9, nesterov=True, dtype=np.float32,
+              backend="sparse"):
+        """bench.build_model + Sequential.compile (bench.py:127-151, train.py:136-188).
+        backend "masked": the MaskedDense baseline -- the same pattern / init
+        draws scattered into dense storage plus a 0/1 mask (train.py:159-170)."""
         dens, nnz = er_plan(list(chain), density)
         st = Streams(seed)
         prng, irng = st("pattern"), st("init")
@@ -316,7 +320,19 @@ class OracleMLP:
             else:
                 rp, ci = sample_pattern(n_out, n_in, nnz[i], prng)
                 v = xavier(n_in, n_out, irng, nnz=nnz[i], dtype=dtype)
-                layers.append(Layer(n_in, n_out, relu, True, v, rp, ci, momentum, nesterov, dtype))
+                if backend == "masked":
+                    rows = np.repeat(np.arange(n_out), np.diff(rp))
+                    w = np.zeros((n_out, n_in), dtype=dtype)
+                    w[rows, ci] = v
+                    mk = np.zeros((n_out, n_in), dtype=dtype)
+                    mk[rows, ci] = 1
+                    lay = Layer(n_in, n_out, relu, False, w.reshape(-1), mu=momentum,
+                                nesterov=nesterov, dtype=dtype)
+                    lay.mask = mk.reshape(-1)
+                    layers.append(lay)
+                else:
+                    layers.append(
+                        Layer(n_in, n_out, relu, True, v, rp, ci, momentum, nesterov, dtype))
         m = cls(layers)
         m.streams = st
         return m
@@ -375,6 +391,8 @@ class OracleMLP:
                 d = spmm_t(lay.row_ptr, lay.col_idx, lay.values, lay.n_in, d)
             else:
                 g = (d @ x.T).reshape(-1)
+                if lay.mask is not None:  # nn.py:255-256
+                    g *= lay.mask
                 gb = d.sum(axis=1)
                 d = lay.W.T @ d
             grads.append((g, gb))
@@ -390,8 +408,12 @@ class OracleMLP:
                     axpby(1.0, lay.values, -eta, g)
                 else:
                     axpby(1.0, lay.values, -eta, lay.vel)
-            else:  # _step_vector on the dense weights (nn.py:118-131)
+            else:  # _step_vector on the dense weights (nn.py:118-131, 260-264)
+                if lay.mask is not None:
+                    lay.vel *= lay.mask
                 self._step_vector(lay.values, g, lay.vel, lay, eta, T)
+                if lay.mask is not None:
+                    lay.values *= lay.mask
             self._step_vector(lay.bias, gb, lay.vbias, lay, eta, T)
 
     @staticmethod

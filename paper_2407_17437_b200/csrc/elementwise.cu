@@ -34,6 +34,50 @@ __global__ void optimizer_kernel(T* __restrict__ w, T* __restrict__ v, const T* 
   }
 }
 
+// ---- masked-dense baseline update (DenseLinearLayer.optimize with a mask,
+// nn.py:258-264; grad masked as in backward, nn.py:255-256):
+//   g' = g*mask; v = v*mask; _step_vector(w, g', v); w = w*mask
+// one pass; multiplying by an exact 0/1 keeps numpy's signed zeros.
+template <typename T>
+__device__ __forceinline__ void masked_update_one(const OptConsts<T>& o, T* w, T* v, T g, T mk) {
+  T ww = *w, vv = v ? *v : T(0);
+  g = mul_rn(g, mk);
+  if (v) vv = mul_rn(vv, mk);
+  apply_update(o, g, &ww, &vv);
+  *w = mul_rn(ww, mk);
+  if (v) *v = vv;
+}
+
+template <typename T, bool VEC>
+__global__ void masked_optimizer_kernel(T* __restrict__ w, T* __restrict__ v,
+                                        const T* __restrict__ g, const T* __restrict__ mask,
+                                        int64_t count, OptConsts<T> o) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (VEC) {
+    using V = typename Vec16<T>::type;
+    constexpr int VW = Vec16<T>::N;
+    for (int64_t i = t0; i < count / VW; i += stride) {
+      V wv = reinterpret_cast<const V*>(w)[i];
+      V vv = v ? reinterpret_cast<const V*>(v)[i] : V{};
+      const V gv = __ldg(reinterpret_cast<const V*>(g) + i);
+      const V mv = __ldg(reinterpret_cast<const V*>(mask) + i);
+#pragma unroll
+      for (int j = 0; j < VW; ++j) {
+        T a = VecOps<T>::get(wv, j), b = VecOps<T>::get(vv, j);
+        masked_update_one(o, &a, v ? &b : nullptr, VecOps<T>::get(gv, j), VecOps<T>::get(mv, j));
+        VecOps<T>::set(wv, j, a);
+        VecOps<T>::set(vv, j, b);
+      }
+      reinterpret_cast<V*>(w)[i] = wv;
+      if (v) reinterpret_cast<V*>(v)[i] = vv;
+    }
+  } else {
+    for (int64_t i = t0; i < count; i += stride)
+      masked_update_one(o, w + i, v ? v + i : nullptr, g[i], mask[i]);
+  }
+}
+
 // ---- warp per row: pairwise row sum (tensor_core.py:353-356) and the bias
 // optimizer update (_step_vector, nn.py:118-131) --------------------------
 constexpr int kRowWarps = 8;
@@ -352,6 +396,36 @@ extern "C" int smb_optimizer_step(int dtype, void* param, void* velocity, const 
         static_cast<T*>(param), static_cast<T*>(velocity), static_cast<const T*>(grad), count,
         make_opt<T>(opt_kind, mu, eta));
     return check_launch("smb_optimizer_step");
+  });
+}
+
+extern "C" int smb_masked_optimizer_step(int dtype, void* param, void* velocity,
+                                         const void* grad, const void* mask, int64_t count,
+                                         int opt_kind, double mu, double eta, void* stream) {
+  clear_error();
+  SMB_REQUIRE(count >= 0, "smb_masked_optimizer_step: negative count");
+  SMB_REQUIRE(opt_kind >= SMB_OPT_NONE && opt_kind <= SMB_OPT_NESTEROV,
+              "smb_masked_optimizer_step: bad optimizer kind %d", opt_kind);
+  if (count == 0 || opt_kind == SMB_OPT_NONE) return SMB_OK;
+  SMB_REQUIRE(param && grad && mask, "smb_masked_optimizer_step: null pointer");
+  SMB_REQUIRE(opt_kind == SMB_OPT_GD || velocity,
+              "smb_masked_optimizer_step: momentum needs velocity");
+  return dispatch_dtype(dtype, "smb_masked_optimizer_step", [&](auto tag) {
+    using T = decltype(tag);
+    constexpr int VW = Vec16<T>::N;
+    const bool vec = count % VW == 0 && aligned16(param) && aligned16(grad) &&
+                     aligned16(mask) && (velocity == nullptr || aligned16(velocity));
+    const OptConsts<T> o = make_opt<T>(opt_kind, mu, eta);
+    cudaStream_t st = as_stream(stream);
+    if (vec)
+      masked_optimizer_kernel<T, true><<<grid_1d(count / VW, 256), 256, 0, st>>>(
+          static_cast<T*>(param), static_cast<T*>(velocity), static_cast<const T*>(grad),
+          static_cast<const T*>(mask), count, o);
+    else
+      masked_optimizer_kernel<T, false><<<grid_1d(count, 256), 256, 0, st>>>(
+          static_cast<T*>(param), static_cast<T*>(velocity), static_cast<const T*>(grad),
+          static_cast<const T*>(mask), count, o);
+    return check_launch("smb_masked_optimizer_step");
   });
 }
 

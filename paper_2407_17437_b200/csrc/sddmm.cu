@@ -30,13 +30,15 @@ namespace smb {
 namespace {
 
 // TILE nonzeros per CTA, CH batch columns per pipeline stage
-template <typename T, int TILE, int CH, int ST>
+template <typename T, int TILE, int CH, int ST, int SD = 4>
 struct SddmmCfg {
   static constexpr int kChunk = CH;
   static constexpr int VW = 16 / sizeof(T);  // elements per 16 B
   static constexpr int LDS = kChunk + VW;    // padded smem row (elements)
   static constexpr int VPR = kChunk / VW;    // 16 B vectors per staged row
-  static constexpr int SLOTS = TILE / 4;  // staged d_out rows per tile
+  // staged d_out rows per tile: TILE/4 (rows of >= 4 nonzeros on average),
+  // or TILE (SD = 1) for very sparse layers whose tiles span ~1 row per nonzero
+  static constexpr int SLOTS = TILE / SD;
   // power-of-two ring (stage = chunk & (STAGES-1)); defaults:
   //   fp32 512-tile x 32 cols x 2 stages = 184 KB (1 CTA, 16 warps / SM),
   //   fp32 128-tile x 64 cols x 2 stages =  87 KB (2 CTAs / SM),
@@ -105,14 +107,14 @@ __device__ __forceinline__ void copy_vec(unsigned dst, const T* src, int valid_e
 
 // ALL: every tile's d_out rows fit the SLOTS staging rows (checked on the
 // host from the pattern's tile spans), so the hot loop has no fallback path.
-template <typename T, int TILE, int CH, int ST, bool VEC, bool ALL>
+template <typename T, int TILE, int CH, int ST, int SD, bool VEC, bool ALL>
 __global__ void __launch_bounds__(TILE)
     sddmm_pipe_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                       const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
                       const T* __restrict__ d_out, int64_t ld_d, const T* __restrict__ x,
                       int64_t ld_x, int64_t n, const T* values, T* values_out, T* velocity,
                       T* grad_out, OptConsts<T> opt) {
-  using C = SddmmCfg<T, TILE, CH, ST>;
+  using C = SddmmCfg<T, TILE, CH, ST, SD>;
   constexpr int S = C::STAGES, VW = C::VW, VPR = C::VPR, LDS = C::LDS;
   constexpr int kChunk = C::kChunk;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -278,21 +280,25 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     };
     // every tile's d_out rows staged -> fallback-free kernel (a 256-tile's
     // span is bounded by its enclosing 512-tile's)
-    auto all_for = [&](int tile) {
-      return (tile == 128 ? pat->span128 : pat->span512) <= tile / 4;
+    auto all_for = [&](int tile, int sd) {
+      return (tile == 128 ? pat->span128 : pat->span512) <= tile / sd;
     };
     static const int variant = [] {
       const char* e = getenv("SMB_SDDMM_VARIANT");
       return e ? atoi(e) : 0;
     }();
-#define SMB_GO(TL, CHK, STG)                                                              \
+#define SMB_GO_SD(TL, CHK, STG, SDV)                                                      \
   do {                                                                                     \
-    using C = SddmmCfg<T, TL, CHK, STG>;                                                   \
-    const bool all = all_for(TL);                                                          \
-    if (vec && all) go(sddmm_pipe_kernel<T, TL, CHK, STG, true, true>, TL, C::smem_bytes);  \
-    else if (vec) go(sddmm_pipe_kernel<T, TL, CHK, STG, true, false>, TL, C::smem_bytes);   \
-    else go(sddmm_pipe_kernel<T, TL, CHK, STG, false, false>, TL, C::smem_bytes);           \
+    using C = SddmmCfg<T, TL, CHK, STG, SDV>;                                              \
+    const bool all = all_for(TL, SDV);                                                     \
+    if (vec && all)                                                                        \
+      go(sddmm_pipe_kernel<T, TL, CHK, STG, SDV, true, true>, TL, C::smem_bytes);          \
+    else if (vec)                                                                          \
+      go(sddmm_pipe_kernel<T, TL, CHK, STG, SDV, true, false>, TL, C::smem_bytes);         \
+    else                                                                                   \
+      go(sddmm_pipe_kernel<T, TL, CHK, STG, SDV, false, false>, TL, C::smem_bytes);        \
   } while (0)
+#define SMB_GO(TL, CHK, STG) SMB_GO_SD(TL, CHK, STG, 4)
     // Double-buffered wide chunks: 64 columns for layers below one 512-tile
     // wave, 32 columns (184 KB) for 512-tiles.  Measured on B200 against
     // 16/32-column chunks with 4-8 stages (env SMB_SDDMM_VARIANT): the
@@ -304,9 +310,14 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     else if (sizeof(T) == 4 && big && variant == 6) SMB_GO(512, 16, 4);
     else if (sizeof(T) == 4 && big && variant == 7) SMB_GO(256, 64, 2);
     else if (big) SMB_GO(512, 32, 2);
+    // very sparse rows: a 128-tile spans more than 32 rows -> one staged
+    // d_out row per nonzero (139 KB, 1 CTA / SM) instead of the per-column
+    // global-load fallback
+    else if (sizeof(T) == 4 && !all_for(128, 4)) SMB_GO_SD(128, 64, 2, 1);
     else if (sizeof(T) == 4) SMB_GO(128, 64, 2);
     else SMB_GO(128, 16, 4);
 #undef SMB_GO
+#undef SMB_GO_SD
     const int rc = check_launch(name);
     if (rc != SMB_OK) return rc;
   }

@@ -14,7 +14,9 @@ of the reference's per-batch loop (train.py:389-402):
 spmm_t of layer l runs before the update of layer l (pre-update weights,
 train.py:400-401).  The layer-1 input gradient is never computed: the
 reference computes and discards it (train.py:216-220).  Dense (ER-saturated)
-layers use cuBLAS FP32 (TF32 off) plus the same exact bias/optimizer kernels.
+layers use cuBLAS FP32 (TF32 off) plus the same exact bias/optimizer kernels;
+masked-dense baseline layers (MaskedDense) add the mask in one fused update
+kernel (smb_masked_optimizer_step, nn.py:255-263).
 
 The kernel sequence is captured once into a CUDA graph per learning rate and
 replayed (a step is ~10 launches; replay removes the host launch cost).
@@ -166,6 +168,7 @@ class FusedTrainStep:
                 u.grad_off, u.bias_off = g_off, b_off
             self.flat = torch.zeros(total, dtype=f32, device=dev)
         self._graphs = {}
+        self._cap_stream = None
         self.timer = None  # optional KernelTimer: per-launch CUDA events (eager only)
         # Single-GPU steps run each sparse layer's SDDMM+update on a side
         # stream, concurrently with the transposed-SpMM chain.  The update
@@ -200,8 +203,6 @@ class FusedTrainStep:
             if not isinstance(lay, (SparseLinearLayer, DenseLinearLayer)):
                 raise ConfigurationError(
                     f"fused step supports Sparse/Dense layers with ReLU only, got {type(lay).__name__}")
-            if isinstance(lay, DenseLinearLayer) and lay.mask is not None:
-                raise ConfigurationError("fused step does not run the masked-dense baseline")
             relu = False
             if i + 1 < len(layers) and isinstance(layers[i + 1], ActivationLayer):
                 if not isinstance(layers[i + 1].fn, ReLU):
@@ -253,6 +254,7 @@ class FusedTrainStep:
         F32 = _lib.SMB_F32
         x_in, t_in = self.x_slots[self._slot], self.t_slots[self._slot]
         overlap = self.overlap and fuse_update
+        forked = False  # the side stream joins only after this step forked onto it
         main = torch.cuda.current_stream()
         side = self._side_stream() if overlap else None
         if gather:
@@ -263,6 +265,7 @@ class FusedTrainStep:
                 # the label batch is only read by the softmax step: gather it
                 # beside the forward chain
                 side.wait_stream(main)
+                forked = True
                 with torch.cuda.stream(side):
                     self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples,
                                d.classes, ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in),
@@ -308,6 +311,7 @@ class FusedTrainStep:
             x_prev = self.acts[li - 1] if li > 0 else x_in
             if overlap and u.sparse:
                 side.wait_stream(main)  # d_l is ready
+                forked = True
                 with torch.cuda.stream(side):
                     self._weight_side(u, dy, x_prev, eta, fuse_update, stream_ptr())
             if li > 0:
@@ -330,7 +334,7 @@ class FusedTrainStep:
                                B, b, vb, gb, kind, mu, float(eta), st)
             if not (overlap and u.sparse):
                 self._weight_side(u, dy, x_prev, eta, fuse_update, st)
-        if overlap:
+        if forked:
             main.wait_stream(side)  # join: the step ends when every update has
 
     def _side_stream(self):
@@ -374,9 +378,14 @@ class FusedTrainStep:
             torch.mm(dy[:, :B], x_prev[:, :B].T, out=gw)
         if fuse_update:
             vel = lay.velocity.view(-1) if lay.velocity is not None else None
-            self._call(f"update[{u.index}]", "smb_optimizer_step", F32, ptr(lay.weights),
-                       ptr(vel), ptr(gw), u.nvals, optimizer_kind(opt), float(opt.mu), float(eta),
-                       st)
+            if lay.mask is not None:  # masked-dense baseline (nn.py:255-263)
+                self._call(f"update[{u.index}]", "smb_masked_optimizer_step", F32,
+                           ptr(lay.weights), ptr(vel), ptr(gw), ptr(lay.mask), u.nvals,
+                           optimizer_kind(opt), float(opt.mu), float(eta), st)
+            else:
+                self._call(f"update[{u.index}]", "smb_optimizer_step", F32, ptr(lay.weights),
+                           ptr(vel), ptr(gw), u.nvals, optimizer_kind(opt), float(opt.mu),
+                           float(eta), st)
 
     def _launch_updates_from_flat(self, eta: float) -> None:
         st = stream_ptr()
@@ -392,8 +401,13 @@ class FusedTrainStep:
             else:
                 vals = lay.weights
                 vel = lay.velocity.view(-1) if lay.velocity is not None else None
-            self._call(f"update[{u.index}]", "smb_optimizer_step", _lib.SMB_F32, ptr(vals),
-                       ptr(vel), ptr(g), u.nvals, kind, float(opt.mu), float(eta), st)
+            if not u.sparse and lay.mask is not None:
+                self._call(f"update[{u.index}]", "smb_masked_optimizer_step", _lib.SMB_F32,
+                           ptr(vals), ptr(vel), ptr(g), ptr(lay.mask), u.nvals, kind,
+                           float(opt.mu), float(eta), st)
+            else:
+                self._call(f"update[{u.index}]", "smb_optimizer_step", _lib.SMB_F32, ptr(vals),
+                           ptr(vel), ptr(g), u.nvals, kind, float(opt.mu), float(eta), st)
             self._call(f"update_bias[{u.index}]", "smb_optimizer_step", _lib.SMB_F32,
                        ptr(lay.bias), ptr(lay.velocity_bias), ptr(gb), u.m, kind, float(opt.mu),
                        float(eta), st)
@@ -434,13 +448,21 @@ class FusedTrainStep:
         key = (float(eta), gather, part, self._slot, self._parity)
         g = self._graphs.get(key)
         if g is None:
-            # the first execution is eager (initialises cuBLAS handles and
+            # the first execution is eager, on the stream that is then
+            # captured (initialises cuBLAS handles / per-stream workspaces and
             # kernel attributes outside capture); capture only records, it
             # does not execute, so the captured graph replays from step 2 on
-            self._run_eager(eta, gather, part)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            cur = torch.cuda.current_stream()
+            if self._cap_stream is None:
+                self._cap_stream = torch.cuda.Stream(device=self.dev)
+            cs = self._cap_stream
+            cs.wait_stream(cur)
+            with torch.cuda.stream(cs):
                 self._run_eager(eta, gather, part)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cs):
+                self._run_eager(eta, gather, part)
+            cur.wait_stream(cs)
             self._graphs[key] = g
             return
         g.replay()

@@ -19,7 +19,7 @@ from .errors import ConfigurationError
 from .nn import Momentum, ReLU
 from .sparsity import er_densities, layer_pairs_from_chain
 from .tensor_core import to_numpy
-from .train import Dense, MultiStepSchedule, Sequential, Sparse
+from .train import Dense, MaskedDense, MultiStepSchedule, Sequential, Sparse
 
 __all__ = [
     "TABLE_LR_DEFAULTS",
@@ -66,9 +66,9 @@ class ExperimentConfig:
     def __post_init__(self):
         if not 0.0 < self.density <= 1.0:
             raise ConfigurationError(f"density must be in (0, 1], got {self.density}")
-        if self.backend != "sparse":
+        if self.backend not in ("sparse", "masked"):
             raise ConfigurationError(
-                f"backend must be 'sparse' on the B200 path, got {self.backend!r}")
+                f"backend must be 'sparse' or 'masked', got {self.backend!r}")
         if len(self.layer_dims) < 2:
             raise ConfigurationError("layer_dims needs input and output sizes at least")
 
@@ -86,8 +86,9 @@ class ExperimentConfig:
 
 
 def build_model(config: ExperimentConfig):
-    """ER plan -> Sequential of Sparse (or Dense when saturated) layers,
-    compiled with the config's seed.  Returns (model, plan)."""
+    """ER plan -> Sequential of Sparse (backend "sparse") or MaskedDense
+    (backend "masked") layers, Dense where the density saturates, compiled
+    with the config's seed (bench.py:127-151).  Returns (model, plan)."""
     plan = er_densities(layer_pairs_from_chain(config.layer_dims), config.density)
     model = Sequential()
     last = len(plan.layer_dims) - 1
@@ -98,8 +99,10 @@ def build_model(config: ExperimentConfig):
         opt = Momentum(config.momentum, nesterov=config.nesterov)
         if dens >= 1.0:
             model.add(Dense(n_out, activation=act, optimizer=opt))
-        else:
+        elif config.backend == "sparse":
             model.add(Sparse(n_out, dens, activation=act, optimizer=opt, nnz=nnz))
+        else:
+            model.add(MaskedDense(n_out, dens, activation=act, optimizer=opt, nnz=nnz))
     model.compile(input_size=config.layer_dims[0], batch_size=config.batch_size, seed=config.seed)
     return model, plan
 

@@ -291,12 +291,16 @@ class DenseLinearLayer:
         return dx
 
     def optimize(self, eta):
-        if self.mask is not None and self.velocity is not None:
-            self.velocity *= self.mask
-        _step(self.weights.view(-1), self.grad.contiguous().view(-1),
-              None if self.velocity is None else self.velocity.view(-1), self.optimizer, eta)
-        if self.mask is not None:
-            self.weights *= self.mask
+        vel = None if self.velocity is None else self.velocity.view(-1)
+        if self.mask is None:
+            _step(self.weights.view(-1), self.grad.contiguous().view(-1), vel, self.optimizer, eta)
+        else:
+            # velocity *= mask; _step_vector; weights *= mask (nn.py:258-263), one pass
+            opt = self.optimizer
+            _lib.call("smb_masked_optimizer_step", dtype_code(self.weights.dtype),
+                      ptr(self.weights), ptr(vel), ptr(self.grad.contiguous()), ptr(self.mask),
+                      self.weights.numel(), optimizer_kind(opt), float(opt.mu), float(eta),
+                      stream_ptr())
         _step(self.bias, self.grad_bias, self.velocity_bias, self.optimizer, eta)
 
 

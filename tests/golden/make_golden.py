@@ -153,18 +153,21 @@ def train_trace():
 
 
 def fingerprints():
-    """The run behind pkg/test_output.txt:26 (criterion 7): sparse backend,
-    seed 3, 2 epochs, B=100, synthetic blobs 50/class."""
-    cfg = sm.ExperimentConfig(
-        layer_dims=[3072, 1024, 512, 10], density=0.01, backend="sparse", epochs=2,
-        batch_size=100, seed=3, threads=1, eval_metrics=False,
-        dataset="synthetic:classes=10,features=3072,per_class=50,spread=1.0,test_per_class=5")
-    _, model = sm.run_training(cfg)
+    """The runs behind pkg/test_output.txt:26 (criterion 7): sparse and
+    masked backends, seed 3, 2 epochs, B=100, synthetic blobs 50/class."""
+    out = {}
+    for backend in ("sparse", "masked"):
+        cfg = sm.ExperimentConfig(
+            layer_dims=[3072, 1024, 512, 10], density=0.01, backend=backend, epochs=2,
+            batch_size=100, seed=3, threads=1, eval_metrics=False,
+            dataset="synthetic:classes=10,features=3072,per_class=50,spread=1.0,test_per_class=5")
+        _, model = sm.run_training(cfg)
+        out[f"{backend}_seed3_2epochs_B100_blobs50"] = sm.weights_fingerprint(model)
     recorded = (REF_SRC.parents[0] / "test_output.txt").read_text()
-    (HERE / "fingerprints.json").write_text(json.dumps({
-        "sparse_seed3_2epochs_B100_blobs50": sm.weights_fingerprint(model),
-        "recorded_prefix_test_output_txt_26": "69a2e92774f1" if "69a2e92774f1" in recorded else None,
-    }, indent=1))
+    out["recorded_prefix_test_output_txt_26"] = "69a2e92774f1" if "69a2e92774f1" in recorded else None
+    out["recorded_prefix_masked_test_output_txt_26"] = (
+        "cb8714b95a57" if "cb8714b95a57" in recorded else None)
+    (HERE / "fingerprints.json").write_text(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":

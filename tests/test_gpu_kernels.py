@@ -95,6 +95,22 @@ def test_sddmm_many_empty_rows_window_fallback(oracle):
     assert bits_equal(got, oracle.sddmm(rp, ci, a, b))
 
 
+@pytest.mark.parametrize("n", [1024, 70, 5])
+def test_sddmm_very_sparse_rows_one_slot_per_nonzero(oracle, n):
+    # 1-2 nonzeros per row: a 128-nonzero tile spans > 32 rows, so every
+    # nonzero gets its own staged d_out row (SD = 1 tiles)
+    m, k = 3000, 700
+    rng = np.random.default_rng(n)
+    counts = rng.integers(1, 3, size=m)
+    rp = np.zeros(m + 1, dtype=np.int32)
+    np.cumsum(counts, out=rp[1:])
+    ci = np.concatenate([np.sort(rng.choice(k, size=c, replace=False)) for c in counts]).astype(np.int32)
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float32)
+    got = host(smb.sddmm(smb.SparsityPattern(m, k, rp, ci), dev(a), dev(b)).values)
+    assert bits_equal(got, oracle.sddmm(rp, ci, a, b))
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_sparse_combine_bit_exact(oracle, dtype):
     rng = np.random.default_rng(55)

@@ -152,3 +152,33 @@ def test_sgd_train_reference_fingerprint_run(oracle):
                                          eval_metrics=False))
     assert [r.lr for r in recs] == [0.1, 0.1 * 0.1 ** 2]
     assert max_rel(model, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("backend", ["sparse", "masked"])
+def test_train_batch_host_buffers_equal_device_gather(backend):
+    """FusedTrainStep.train_batch (pinned host batches, double-buffered copies:
+    the e2e API bench.py times) == step() over the HBM dataset, bit for bit,
+    including the loss copied back to the host."""
+    chain, B, steps, eta = [3072, 1024, 512, 10], 128, 5, 0.03
+    data = smb.synthetic_dataset(seed=4, n_samples=B * steps, features=chain[0])
+    perm = np.random.default_rng(2).permutation(B * steps)
+    cfg = smb.ExperimentConfig(layer_dims=chain, density=0.01, seed=6, batch_size=B, lr=eta,
+                               backend=backend)
+    m_dev, _ = smb.build_model(cfg)
+    m_host, _ = smb.build_model(cfg)
+    st_dev = smb.FusedTrainStep(m_dev, B)
+    st_dev.attach_dataset(smb.DeviceDataset(data))
+    st_dev.set_epoch(perm)
+    st_host = smb.FusedTrainStep(m_host, B)
+    loss_host = torch.empty(1, dtype=torch.float64).pin_memory()
+    for k in range(steps):
+        st_dev.step(eta)
+        b = perm[k * B:(k + 1) * B]
+        xb = torch.from_numpy(np.ascontiguousarray(data.Xtrain[:, b])).pin_memory()
+        tb = torch.from_numpy(np.ascontiguousarray(data.Ttrain[:, b])).pin_memory()
+        st_host.train_batch(xb, tb, eta, loss_host)
+        torch.cuda.synchronize()
+        assert float(loss_host[0]) == st_dev.loss_value(), k
+    for (n1, a), (n2, b) in zip(params_host(m_dev), params_host(m_host)):
+        assert n1 == n2
+        assert bits_equal(a, b), n1

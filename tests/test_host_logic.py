@@ -107,6 +107,11 @@ def test_experiment_config_and_lr_table():
         smb.Sparse(0, 0.5)
     with pytest.raises(smb.InvalidArgumentError):
         smb.Momentum(1.0)
+    assert smb.ExperimentConfig(backend="masked").backend == "masked"  # bench.py:95-96
+    with pytest.raises(smb.ConfigurationError):
+        smb.ExperimentConfig(backend="dense")
+    with pytest.raises(smb.ConfigurationError):
+        smb.MaskedDense(10, 0.0)
 
 
 def test_shard_epoch_covers_every_sample_once():

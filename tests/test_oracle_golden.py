@@ -104,6 +104,18 @@ def test_reference_recorded_fingerprint(oracle):
     assert m.fingerprint().startswith(fp["recorded_prefix_test_output_txt_26"])
 
 
+def test_reference_recorded_masked_fingerprint(oracle):
+    """The masked-dense baseline (MaskedDense, train.py:159-170; nn.py:201-264)
+    of the same run reproduces the recorded masked fingerprint
+    (pkg/test_output.txt:26, cb8714b95a57...)."""
+    fp = json.loads((GOLDEN / "fingerprints.json").read_text())
+    xtr, ttr, _, _ = oracle.synthetic_blobs(10, 3072, 50, 1.0, 3, 5)
+    m = oracle.OracleMLP.build([3072, 1024, 512, 10], 0.01, seed=3, backend="masked")
+    m.train(xtr, ttr, 2, 100, oracle.multistep(0.1))
+    assert m.fingerprint() == fp["masked_seed3_2epochs_B100_blobs50"]
+    assert m.fingerprint().startswith(fp["recorded_prefix_masked_test_output_txt_26"])
+
+
 def test_pcg64_restatement_matches_numpy(oracle):
     """The device Xavier kernel's algorithm (PCG64 XSL-RR + LCG jump-ahead)
     against numpy's own generator and xavier_init's float64->fp32 mapping."""
