@@ -170,6 +170,34 @@ def fingerprints():
     (HERE / "fingerprints.json").write_text(json.dumps(out, indent=1))
 
 
+def archives():
+    """Model archives written by the reference's save_model (data_io.py:359-380)
+    for a small sparse and a small masked model after 3 training steps, plus
+    their fingerprints / size reports: interop fixtures for archive.py."""
+    from sparsemlp import data_io as dio
+
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((64, 30)).astype(np.float32)
+    t = np.zeros((10, 30), np.float32)
+    t[rng.integers(0, 10, 30), np.arange(30)] = 1
+    meta = {}
+    for backend in ("sparse", "masked"):
+        model, _ = sm.build_model(sm.ExperimentConfig(
+            layer_dims=[64, 48, 32, 10], density=0.2, seed=7, backend=backend, lr=0.05))
+        loss = rnn.SoftmaxCrossEntropyLoss()
+        for _ in range(3):
+            y = model.feedforward(x)
+            model.backpropagate(y, loss.gradient(y, t) / 30)
+            model.optimize(0.05)
+        d = HERE / f"archive_{backend}"
+        dio.save_model(model, d)
+        meta[backend] = {"fingerprint": sm.weights_fingerprint(model),
+                         "size_report": dio.model_size_report(model).to_dict(),
+                         "weight_file_bytes": dio.archive_weight_file_bytes(d),
+                         "forward_sum": float(np.sum(model.feedforward(x), dtype=np.float64))}
+    (HERE / "archives.json").write_text(json.dumps(meta, indent=1))
+
+
 if __name__ == "__main__":
     sm.set_num_threads(1)
     kernels()
@@ -177,5 +205,6 @@ if __name__ == "__main__":
     plans_and_init()
     train_trace()
     fingerprints()
+    archives()
     for f in sorted(HERE.iterdir()):
         print(f.name, f.stat().st_size)
