@@ -425,6 +425,8 @@ def run_ours(args):
         line["cpu_baseline"] = {"value": sps, "unit": UNIT, "cores": threads, "kind": "port",
                                 "sample": f"{nsteps} training steps at batch {gb} "
                                           f"({dt:.1f} s, oracle/ C kernels + numpy glue)"}
+    if rank == 0 and ws == 1:
+        line["inference_b1"] = inference_latency(args, model, cpu=not args.no_cpu_baseline)
     if args.sweep and ws == 1:
         line["sweep"] = density_sweep(args)
     if rank == 0:
@@ -434,6 +436,39 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def inference_latency(args, model, cpu: bool, repeats: int = 200):
+    """Batch-1 forward latency (bench.py:366-399 of the reference): host wall
+    clock per call, pinned input copy + logits read-back included, beside the
+    oracle port's forward of the same column on this host."""
+    import paper_2407_17437_b200 as smb
+
+    cfg = smb.ExperimentConfig(layer_dims=[int(x) for x in args.layers.split(",")],
+                               density=args.density, seed=args.seed, backend=args.backend)
+    r = smb.bench_inference(cfg, n_repeats=repeats, warmup=10, model=model)
+    out = {"median_ms": r["median_ms"], "min_ms": r["min_ms"], "repeats": repeats,
+           "api": "InferenceSession (one CUDA graph: H2D + forward + D2H)"}
+    if cpu:
+        from oracle import oracle as O
+
+        O.build()
+        O.set_threads(1)
+        ref = O.OracleMLP.build([int(x) for x in args.layers.split(",")], args.density,
+                                seed=args.seed, backend=args.backend)
+        x = np.random.default_rng(args.seed).standard_normal(
+            (ref.layers[0].n_in, 1)).astype(np.float32)
+        for _ in range(5):
+            ref.forward(x)
+        ts = []
+        for _ in range(50):
+            t0 = time.perf_counter()
+            ref.forward(x)
+            ts.append(time.perf_counter() - t0)
+        out["cpu_port_median_ms"] = 1e3 * float(np.median(ts))
+        out["cpu_port_cores"] = 1
+        O.set_threads(os.cpu_count() or 1)
+    return out
 
 
 def density_sweep(args, steps=20):

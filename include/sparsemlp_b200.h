@@ -191,6 +191,27 @@ SMB_API int smb_bias_grad_update(int dtype, const void* d_out, int64_t ld, int64
 SMB_API int smb_optimizer_step(int dtype, void* param, void* velocity, const void* grad, int64_t count,
                        int opt_kind, double mu, double eta, void* stream);
 
+/* Fused output-layer tail for one batch (nn.py:169-176 forward of the last
+ * sparse layer, nn.py:411-417 + train.py:399 softmax-CE gradient / divisor,
+ * nn.py:397-408 loss, nn.py:185 spmm_transposed, nn.py:89-91 ReLU.backward
+ * of the layer below):
+ *   y = W h + bias;  d_y = (softmax(y) - t) / divisor;  loss = summed CE;
+ *   d_h = (W^T d_y) * (h > 0)   (mask != 0; h is the post-ReLU input)
+ * with every accumulation in the reference's order (bit-identical to
+ * smb_spmm + smb_softmax_ce_grad + smb_spmm_t).  Activations are [rows, ld]
+ * row-major.  y may be NULL.  step_counter (may be NULL) is advanced modulo
+ * `modulo` like smb_softmax_ce_step.  The bias row sums of d_y / d_h are NOT
+ * computed (smb_bias_grad_update).  Valid when smb_tail_step_supported()
+ * (<= 32 output rows, layer small enough for one CTA's shared memory);
+ * workspace: smb_tail_step_workspace_bytes(n) zero-initialised bytes. */
+SMB_API int smb_tail_step_supported(int dtype, const smb_pattern* pattern);
+SMB_API size_t smb_tail_step_workspace_bytes(int64_t n);
+SMB_API int smb_tail_step(int dtype, const smb_pattern* pattern, const void* values,
+                          const void* h, int64_t ld_h, int mask, const void* bias, const void* t,
+                          int64_t ld_t, int64_t n, double divisor, void* y, int64_t ld_y,
+                          void* d_y, int64_t ld_dy, void* d_h, int64_t ld_dh, double* loss_out,
+                          int32_t* step_counter, int32_t modulo, void* workspace, void* stream);
+
 /* Masked-dense baseline update, DenseLinearLayer.optimize with a mask
  * (nn.py:258-264, gradient masked as in backward nn.py:255-256):
  * g' = grad*mask, velocity *= mask, _step_vector(param, g', velocity),

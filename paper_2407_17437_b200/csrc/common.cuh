@@ -66,6 +66,14 @@ __device__ __forceinline__ T mask_np(T d, T x) {
   return mul_rn(d, x > T(0) ? T(1) : T(0));
 }
 
+// full-accuracy (non-intrinsic) exp / log in the value type: expf is within
+// 2 ulp like numpy's own float32 exp (documented max 2.52 ulp), so the
+// softmax is tolerance-exact, not bit-exact, against the reference
+__device__ __forceinline__ float exp_full(float x) { return expf(x); }
+__device__ __forceinline__ double exp_full(double x) { return exp(x); }
+__device__ __forceinline__ float log_full(float x) { return logf(x); }
+__device__ __forceinline__ double log_full(double x) { return log(x); }
+
 // 16-byte vector of T
 template <typename T>
 struct Vec16;

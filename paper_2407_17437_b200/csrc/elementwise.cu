@@ -105,14 +105,6 @@ __global__ void __launch_bounds__(kRowWarps * 32)
   }
 }
 
-// full-accuracy (non-intrinsic) exp / log in the value type: expf is within
-// 2 ulp like numpy's own float32 exp (documented max 2.52 ulp), so the
-// softmax is tolerance-exact, not bit-exact, against the reference
-__device__ __forceinline__ float exp_full(float x) { return expf(x); }
-__device__ __forceinline__ double exp_full(double x) { return exp(x); }
-__device__ __forceinline__ float log_full(float x) { return logf(x); }
-__device__ __forceinline__ double log_full(double x) { return log(x); }
-
 // ---- softmax cross-entropy step (nn.py:385-417, train.py:399) -------------
 // One thread per sample column: z = y - max, e = exp(z) (double, rounded),
 // s = sum_c e (sequential, numpy's axis-0 order), d = (e/s - t) / divisor.

@@ -304,8 +304,21 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   // over more columns.  With few rows one column per lane spreads each row
   // over many more warps.
   auto enough = [&](int w) { return n >= 32 * w && n_rows * ceil_div(n, 32 * w) >= 148 * 8; };
+  static const int force_w = [] {  // tuning experiments only
+    const char* e = getenv("SMB_SPMM_W");
+    return e ? atoi(e) : 0;
+  }();
   bool done;
-  if (vec_ok && enough(2 * VW))
+  if (force_w == 1)
+    done = launch_rows<T, 1, 32, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                            out, ld_out, epi, st);
+  else if (force_w == 4 && vec_ok)
+    done = launch_rows<T, VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                            out, ld_out, epi, st);
+  else if (force_w == 8 && vec_ok)
+    done = launch_rows<T, 2 * VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
+                                                n, out, ld_out, epi, st);
+  else if (vec_ok && enough(2 * VW))
     done = launch_rows<T, 2 * VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
                                                 n, out, ld_out, epi, st);
   else if (vec_ok && enough(VW))

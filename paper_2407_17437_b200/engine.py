@@ -30,6 +30,8 @@ which every rank applies the identical update.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -78,6 +80,14 @@ class KernelTimer:
         return out
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
@@ -121,7 +131,7 @@ class _Unit:
 
 class FusedTrainStep:
     def __init__(self, model, batch_size: int, global_batch: int | None = None,
-                 process_group=None, use_graph: bool = True):
+                 process_group=None, use_graph: bool = True, fuse_tail: bool | None = None):
         self.units = self._parse(model)
         self.model = model
         self.B = int(batch_size)
@@ -167,6 +177,20 @@ class FusedTrainStep:
             for u, (g_off, b_off) in zip(self.units, layout):
                 u.grad_off, u.bias_off = g_off, b_off
             self.flat = torch.zeros(total, dtype=f32, device=dev)
+        # fused output-layer tail (smb_tail_step: last layer sparse, no
+        # activation, <= 32 outputs, small enough for one CTA's smem).  Off by
+        # default: on B200 at the config-2 point it measured ~10 us slower
+        # than spmm + softmax step + spmm_t; SMB_FUSE_TAIL=1 or
+        # fuse_tail=True selects it.
+        top = self.units[-1]
+        self.tail_ok = bool(
+            len(self.units) >= 2 and top.sparse and not top.relu
+            and _lib.load().smb_tail_step_supported(_lib.SMB_F32,
+                                                    top.layer.weights.pattern.handle))
+        want = fuse_tail if fuse_tail is not None else os.environ.get("SMB_FUSE_TAIL") == "1"
+        self.fuse_tail = bool(want and self.tail_ok)
+        self._tail_ws = torch.zeros(int(_lib.load().smb_tail_step_workspace_bytes(self.B)),
+                                    dtype=torch.uint8, device=dev) if self.tail_ok else None
         self._graphs = {}
         self._cap_stream = None
         self.timer = None  # optional KernelTimer: per-launch CUDA events (eager only)
@@ -275,8 +299,12 @@ class FusedTrainStep:
                            d.classes, ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in), ld, st)
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
+        tail = self.fuse_tail
+        L = len(self.units)
         for li, (u, a) in enumerate(zip(self.units, self.acts)):
             lay = u.layer
+            if tail and li == L - 1:
+                break
             if u.sparse:
                 self._call(f"spmm[{li}]", "smb_spmm", F32, ptr(lay.weights.row_ptr),
                            ptr(lay.weights.col_idx), ptr(lay.weights.values), u.m, u.k, ptr(x), ld,
@@ -294,11 +322,34 @@ class FusedTrainStep:
         b, vb, gb, kind, mu = self._bias_target(top, fuse_update)
         if gather and overlap:
             main.wait_stream(side)  # label batch gathered
-        self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
-                   ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]), ld,
-                   ptr(self.loss), b, vb, gb, kind, mu, float(eta),
-                   ptr(self.counter) if gather else None, int(self.steps_per_epoch),
-                   ptr(self._ce_ws), st)
+        if tail:
+            # one launch: logits -> softmax-CE gradient / B_global (+ loss,
+            # step counter) -> d_{L-2} = (W_top^T d_top) * mask
+            below = self.units[-2]
+            self._call("tail", "smb_tail_step", F32, top.layer.weights.pattern.handle,
+                       ptr(self._vals(top)), ptr(self.acts[-2]), ld, 1 if below.relu else 0,
+                       ptr(top.layer.bias), ptr(t_in), ld, B, float(self.B_global),
+                       ptr(self.acts[-1]), ld, ptr(self.dys[-1]), ld, ptr(self.dys[-2]), ld,
+                       ptr(self.loss), ptr(self.counter) if gather else None,
+                       int(self.steps_per_epoch), ptr(self._tail_ws), st)
+            # the bias sides of the top two layers cross columns: beside the
+            # critical path when overlapping
+            sides = ((top, self.dys[-1]), (below, self.dys[-2]))
+            if overlap:
+                side.wait_stream(main)
+                forked = True
+            with torch.cuda.stream(side) if overlap else _nullctx():
+                sst = stream_ptr()
+                for u, d_u in sides:
+                    bb, bv, bg, bk, bmu = self._bias_target(u, fuse_update)
+                    self._call(f"bias[{u.index}]", "smb_bias_grad_update", F32, ptr(d_u), ld, u.m,
+                               B, bb, bv, bg, bk, bmu, float(eta), sst)
+        else:
+            self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
+                       ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]),
+                       ld, ptr(self.loss), b, vb, gb, kind, mu, float(eta),
+                       ptr(self.counter) if gather else None, int(self.steps_per_epoch),
+                       ptr(self._ce_ws), st)
         # backward, last layer first: d_{l-1} (+ bias side of layer l-1) on the
         # main stream; the weight side of layer l (SDDMM + update) either
         # follows it in order, or -- single GPU -- runs on the side stream as
@@ -314,7 +365,7 @@ class FusedTrainStep:
                 forked = True
                 with torch.cuda.stream(side):
                     self._weight_side(u, dy, x_prev, eta, fuse_update, stream_ptr())
-            if li > 0:
+            if li > 0 and not (tail and li == L - 1):  # the tail produced d_{L-2}
                 below = self.units[li - 1]
                 mask = self.acts[li - 1] if below.relu else None
                 dst = self.dys[li - 1]
@@ -349,7 +400,7 @@ class FusedTrainStep:
     def _flip_parity(self) -> None:
         """After an overlapped step the updated weights live in the other
         buffer: point the layer's CsrMatrix at it."""
-        if not self.overlap:
+        if not any(u.vals is not None for u in self.units):
             return
         self._parity ^= 1
         for u in self.units:

@@ -287,3 +287,46 @@ def test_softmax_ce_gradient_tolerance():
     assert rel_err(got, want) <= 1e-6
     loss_want = float(np.sum(np.log(e.sum(axis=0)) - (z * t).sum(axis=0)))
     assert abs(smb.softmax_ce_loss(dev(y), dev(t)) - loss_want) <= 1e-4 * abs(loss_want)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [1024, 100, 37, 1])
+@pytest.mark.parametrize("mask", [True, False])
+def test_tail_step_equals_unfused_ops(dtype, n, mask):
+    """smb_tail_step == smb_spmm(+bias) -> smb_softmax_ce_grad(/divisor) ->
+    smb_spmm_t(*mask), bit for bit; loss within fp64 summation-order noise."""
+    from paper_2407_17437_b200 import _lib
+
+    rng = np.random.default_rng(n + (7 if mask else 0))
+    m, k = 10, 300
+    rp, ci, v, _ = random_csr(rng, m, k, 0.4, dtype, empty_rows=True)
+    s = smb.CsrMatrix(m, k, rp, ci, v)
+    code = tc.dtype_code(s.values.dtype)
+    assert _lib.load().smb_tail_step_supported(code, s.pattern.handle) == 1
+    h = dev(np.maximum(rng.standard_normal((k, n)), 0).astype(dtype))
+    bias = dev(rng.standard_normal(m).astype(dtype))
+    lab = rng.integers(0, m, n)
+    t = np.zeros((m, n), dtype)
+    t[lab, np.arange(n)] = 1
+    t = dev(t)
+    divisor = float(n + 3)
+    # unfused reference path (the layer API's kernels)
+    y_ref = smb.spmm(s, h, bias=bias)
+    dy_ref, loss_ref = smb.nn._ce_call(y_ref, t, divisor)
+    dh_ref = smb.spmm_transposed(s, dy_ref, mask=h if mask else None)
+    # fused
+    T = s.values.dtype
+    y = torch.empty((m, n), dtype=T, device="cuda")
+    dy = torch.empty_like(y)
+    dh = torch.empty((k, n), dtype=T, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(int(_lib.load().smb_tail_step_workspace_bytes(n)), dtype=torch.uint8,
+                     device="cuda")
+    _lib.call("smb_tail_step", code, s.pattern.handle, tc.ptr(s.values), tc.ptr(h), n,
+              1 if mask else 0, tc.ptr(bias), tc.ptr(t), n, n, divisor, tc.ptr(y), n,
+              tc.ptr(dy), n, tc.ptr(dh), n, tc.ptr(loss), None, 0, tc.ptr(ws), tc.stream_ptr())
+    assert bits_equal(host(y), host(y_ref))
+    assert bits_equal(host(dy), host(dy_ref))
+    assert bits_equal(host(dh), host(dh_ref))
+    assert abs(float(loss) - float(loss_ref)) <= 1e-12 * max(1.0, abs(float(loss_ref)))
+    assert int(ws[:4].view(torch.int32)) == 0  # ticket reset for the next launch
