@@ -259,6 +259,50 @@ __global__ void __launch_bounds__(max_threads_for<W>())
   }
 }
 
+// Single batch column (n == 1: batch-1 inference, bench.py:366-399): one
+// warp per output row.  The 32 lanes gather 32 products val(s) * x[idx(s)]
+// at once (coalesced index / value loads, one gathered x element each), park
+// them in shared memory and lane 0 adds them in ascending s -- the same
+// separately rounded multiply-then-add sequence as the batched kernel.
+constexpr int kSpmvWarps = 8;
+
+template <typename T, int EPI, bool PERM>
+__global__ void __launch_bounds__(kSpmvWarps * 32)
+    row_spmv_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
+                    const int32_t* __restrict__ perm, const T* __restrict__ vals,
+                    const T* __restrict__ dense, int64_t ld_dense, int64_t n_rows,
+                    T* __restrict__ out, int64_t ld_out, EpiArgs<T> epi) {
+  __shared__ T s_p[kSpmvWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * kSpmvWarps + warp;
+  if (row >= n_rows) return;
+  const int32_t s0 = seg_ptr[row], s1 = seg_ptr[row + 1];
+  T acc = T(0);
+  for (int32_t g = s0; g < s1; g += 32) {
+    const int32_t s = g + lane;
+    T p = T(0);
+    if (s < s1) {
+      const T v = PERM ? vals[perm[s]] : vals[s];
+      p = mul_rn(v, __ldg(dense + (int64_t)idx[s] * ld_dense));
+    }
+    s_p[warp][lane] = p;
+    __syncwarp();
+    if (lane == 0) {
+      const int cnt = min(32, s1 - g);
+      for (int j = 0; j < cnt; ++j) acc = add_rn(acc, s_p[warp][j]);
+    }
+    __syncwarp();
+  }
+  if (lane != 0) return;
+  if constexpr (EPI == kEpiBiasAct) {
+    if (epi.bias != nullptr) acc = add_rn(acc, epi.bias[row]);
+    if (epi.relu) acc = relu_np(acc);
+  } else {
+    if (epi.mask != nullptr) acc = mask_np(acc, epi.mask[row * epi.ld_mask]);
+  }
+  out[row * ld_out] = acc;
+}
+
 template <typename T, int W, int U, int EPI, bool PERM>
 bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm, const T* vals,
                  int64_t n_rows, const T* dense, int64_t ld_dense, int64_t n, T* out,
@@ -294,6 +338,12 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
                         const char* name, bool* rowsum_done) {
   if (rowsum_done) *rowsum_done = false;
   if (n_rows == 0 || n == 0) return SMB_OK;
+  if (n == 1 && !epi.rowsum) {  // one batch column: warp-per-row SpMV
+    row_spmv_kernel<T, EPI, PERM><<<(unsigned)ceil_div(n_rows, kSpmvWarps), kSpmvWarps * 32, 0,
+                                   st>>>(seg_ptr, idx, perm, vals, dense, ld_dense, n_rows, out,
+                                         ld_out, epi);
+    return check_launch(name);
+  }
   constexpr int VW = Vec16<T>::N;
   const bool vec_ok = aligned16(dense) && aligned16(out) && ld_dense % VW == 0 &&
                       ld_out % VW == 0 &&

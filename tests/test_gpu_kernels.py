@@ -330,3 +330,30 @@ def test_tail_step_equals_unfused_ops(dtype, n, mask):
     assert bits_equal(host(dh), host(dh_ref))
     assert abs(float(loss) - float(loss_ref)) <= 1e-12 * max(1.0, abs(float(loss_ref)))
     assert int(ws[:4].view(torch.int32)) == 0  # ticket reset for the next launch
+
+
+@pytest.mark.parametrize("relu", [True, False])
+def test_spmv_single_column_strided_with_epilogue(oracle, relu):
+    """n == 1 (batch-1 inference) through the warp-per-row SpMV, with padded
+    leading dimensions (ld 4, like the fused step at B = 1) and bias + ReLU."""
+    from paper_2407_17437_b200 import _lib
+
+    rng = np.random.default_rng(3 if relu else 4)
+    m, k, ld = 700, 500, 4
+    rp, ci, v, _ = random_csr(rng, m, k, 0.15, np.float32, empty_rows=True)
+    s = smb.CsrMatrix(m, k, rp, ci, v)
+    x = rng.standard_normal((k, 1)).astype(np.float32)
+    b = rng.standard_normal(m).astype(np.float32)
+    xp = np.zeros((k, ld), np.float32)
+    xp[:, :1] = x
+    out = torch.full((m, ld), 7.0, device="cuda")
+    tx, tb = dev(xp), dev(b)
+    _lib.call("smb_spmm", _lib.SMB_F32, tc.ptr(s.row_ptr), tc.ptr(s.col_idx), tc.ptr(s.values),
+              m, k, tc.ptr(tx), ld, 1, tc.ptr(tb), _lib.SMB_EPI_RELU if relu else _lib.SMB_EPI_NONE,
+              tc.ptr(out), ld, tc.stream_ptr())
+    want = oracle.spmm(rp, ci, v, x) + b[:, None]
+    if relu:
+        want = np.maximum(want, 0)
+    got = host(out)
+    assert bits_equal(got[:, :1], want)
+    assert np.all(got[:, 1:] == 7.0)  # padding columns untouched
