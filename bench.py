@@ -88,6 +88,13 @@ def measured_peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def large_grid(args) -> bool:
+    """Some layer has >= 2**31 grid positions (BASELINE config 5): its pattern is
+    injected with the large-grid sampler (the reference's sampler refuses it)."""
+    dims = [int(x) for x in args.layers.split(",")]
+    return any(a * b >= 2**31 for a, b in zip(dims[:-1], dims[1:]))
+
+
 def fp32_peak_tflops() -> float:
     """FFMA peak measured on a B200 by scripts/fp32_peak.cu (profiles/fp32_peak.json);
     the separately rounded mul+add the bit-exact kernels use runs at half of it."""
@@ -189,7 +196,8 @@ def cpu_step_sample(args, global_batch, budget_s, min_steps=3, max_steps=200):
     threads = os.cpu_count() or 1
     O.set_threads(threads)
     chain = [int(x) for x in args.layers.split(",")]
-    ref = O.OracleMLP.build(chain, args.density, seed=args.seed, backend=args.backend)
+    ref = O.OracleMLP.build(chain, args.density, seed=args.seed, backend=args.backend,
+                            large_patterns=large_grid(args))
     rng = np.random.default_rng(args.seed + 17)
     x = rng.standard_normal((chain[0], global_batch), dtype=np.float32)
     lab = rng.integers(0, chain[-1], global_batch)
@@ -216,7 +224,8 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     O.set_threads(threads)
     chain = [int(x) for x in args.layers.split(",")]
-    ref = O.OracleMLP.build(chain, args.density, seed=args.seed, backend=args.backend)
+    ref = O.OracleMLP.build(chain, args.density, seed=args.seed, backend=args.backend,
+                            large_patterns=large_grid(args))
     rng = np.random.default_rng(args.seed + 17)
     x = rng.standard_normal((chain[0], gb), dtype=np.float32)
     lab = rng.integers(0, chain[-1], gb)
@@ -262,7 +271,7 @@ def run_ours(args):
     B, gb = args.batch, args.batch * ws
     cfg = smb.ExperimentConfig(layer_dims=chain, density=args.density, batch_size=B, lr=args.lr,
                                seed=args.seed, backend=args.backend)
-    model, plan = smb.build_model(cfg)
+    model, plan = smb.build_model(cfg, large_patterns=large_grid(args))
     data = smb.synthetic_dataset(seed=args.seed, n_samples=args.samples, features=chain[0],
                                  classes=chain[-1])
     ddata = smb.DeviceDataset(data)
@@ -455,7 +464,8 @@ def inference_latency(args, model, cpu: bool, repeats: int = 200):
         O.build()
         O.set_threads(1)
         ref = O.OracleMLP.build([int(x) for x in args.layers.split(",")], args.density,
-                                seed=args.seed, backend=args.backend)
+                                seed=args.seed, backend=args.backend,
+                                large_patterns=large_grid(args))
         x = np.random.default_rng(args.seed).standard_normal(
             (ref.layers[0].n_in, 1)).astype(np.float32)
         for _ in range(5):

@@ -206,6 +206,25 @@ def sample_pattern(n_out, n_in, nnz, rng):
     return row_ptr.astype(np.int32), col_idx
 
 
+def sample_pattern_large(n_out, n_in, nnz, rng):
+    """Injected pattern for grids >= 2**31 (config 5; the reference refuses
+    them, sparsity.py:193-195): multinomial row counts redrawn until every row
+    fits, then sorted distinct columns per row -- the same numpy call
+    sequence as the package's sample_pattern_large_host."""
+    while True:
+        counts = rng.multinomial(nnz, np.full(n_out, 1.0 / n_out))
+        if counts.max(initial=0) <= n_in:
+            break
+    row_ptr = np.zeros(n_out + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    col_idx = np.empty(nnz, dtype=np.int32)
+    for i in range(n_out):
+        if counts[i]:
+            cols = rng.choice(n_in, size=counts[i], replace=False, shuffle=False)
+            col_idx[row_ptr[i]:row_ptr[i + 1]] = np.sort(cols)
+    return row_ptr.astype(np.int32), col_idx
+
+
 def xavier(n_in, n_out, rng, nnz=None, dtype=np.float32):
     a = float(np.sqrt(6.0 / (n_in + n_out)))
     size = n_out * n_in if nnz is None else nnz
@@ -303,7 +322,7 @@ class OracleMLP:
 
     @classmethod
     def build(cls, chain, density, seed=0, momentum=0.9, nesterov=True, dtype=np.float32,
-              backend="sparse"):
+              backend="sparse", large_patterns=False):
         """bench.build_model + Sequential.compile (bench.py:127-151, train.py:136-188).
         backend "masked": the MaskedDense baseline -- the same pattern / init
         draws scattered into dense storage plus a 0/1 mask (train.py:159-170)."""
@@ -318,7 +337,10 @@ class OracleMLP:
                 layers.append(Layer(n_in, n_out, relu, False, w, mu=momentum, nesterov=nesterov,
                                     dtype=dtype))
             else:
-                rp, ci = sample_pattern(n_out, n_in, nnz[i], prng)
+                if large_patterns and n_out * n_in >= 2**31:
+                    rp, ci = sample_pattern_large(n_out, n_in, nnz[i], prng)
+                else:
+                    rp, ci = sample_pattern(n_out, n_in, nnz[i], prng)
                 v = xavier(n_in, n_out, irng, nnz=nnz[i], dtype=dtype)
                 if backend == "masked":
                     rows = np.repeat(np.arange(n_out), np.diff(rp))

@@ -85,7 +85,7 @@ class ExperimentConfig:
         return d
 
 
-def build_model(config: ExperimentConfig):
+def build_model(config: ExperimentConfig, large_patterns: bool = False):
     """ER plan -> Sequential of Sparse (backend "sparse") or MaskedDense
     (backend "masked") layers, Dense where the density saturates, compiled
     with the config's seed (bench.py:127-151).  Returns (model, plan)."""
@@ -103,7 +103,8 @@ def build_model(config: ExperimentConfig):
             model.add(Sparse(n_out, dens, activation=act, optimizer=opt, nnz=nnz))
         else:
             model.add(MaskedDense(n_out, dens, activation=act, optimizer=opt, nnz=nnz))
-    model.compile(input_size=config.layer_dims[0], batch_size=config.batch_size, seed=config.seed)
+    model.compile(input_size=config.layer_dims[0], batch_size=config.batch_size, seed=config.seed,
+                  large_patterns=large_patterns)
     return model, plan
 
 

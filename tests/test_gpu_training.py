@@ -196,3 +196,28 @@ def test_train_batch_host_buffers_equal_device_gather(backend):
     for (n1, a), (n2, b) in zip(params_host(m_dev), params_host(m_host)):
         assert n1 == n2
         assert bits_equal(a, b), n1
+
+
+def test_config5_injected_patterns_track_oracle(oracle):
+    """BASELINE config 5 shape (3072-65536-65536-10, d=0.001; the hidden-hidden
+    grid exceeds the reference sampler's 2**31 limit, so its pattern is
+    injected): initial weights bit-exact with the oracle's restatement, then
+    two fused steps within the per-step tolerance."""
+    chain, d, B, eta = [3072, 65536, 65536, 10], 0.001, 16, 0.01
+    cfg = smb.ExperimentConfig(layer_dims=chain, density=d, seed=1, batch_size=B, lr=eta)
+    with pytest.raises(smb.InvalidArgumentError):
+        smb.build_model(cfg)  # the reference behaviour without injection
+    model, plan = smb.build_model(cfg, large_patterns=True)
+    assert plan.layer_nnz == [1319931, 2521658, 655360]
+    ref = oracle.OracleMLP.build(chain, d, seed=1, large_patterns=True)
+    for (n1, a), (n2, b) in zip(params_host(model), oracle_params(ref)):
+        assert n1 == n2 and bits_equal(a, b), n1
+    data = smb.synthetic_dataset(seed=3, n_samples=2 * B, features=chain[0])
+    step = smb.FusedTrainStep(model, B)
+    step.attach_dataset(smb.DeviceDataset(data))
+    step.set_epoch(np.arange(2 * B))
+    for k in range(2):
+        step.step(eta)
+        ref_loss = ref.step(data.Xtrain[:, k * B:(k + 1) * B], data.Ttrain[:, k * B:(k + 1) * B], eta)
+        assert abs(step.loss_value() - ref_loss) <= 1e-4 * abs(ref_loss)
+    assert max_rel(model, ref) <= 1e-4

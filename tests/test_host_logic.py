@@ -130,3 +130,21 @@ def test_shard_epoch_covers_every_sample_once():
 def test_flat_layout():
     layout, total = flat_layout([(4, 10), (3, 12)])
     assert layout == [(0, 10), (14, 26)] and total == 29
+
+
+def test_large_grid_pattern_sampler_matches_oracle(oracle):
+    """Config-5 injection sampler (grids >= 2**31, which the reference
+    refuses): exact nnz, sorted distinct columns, deterministic, and the
+    oracle's restatement draws the identical pattern from the same stream."""
+    from paper_2407_17437_b200.sparsity import sample_pattern_host, sample_pattern_large_host
+
+    n_out, n_in, nnz = 65536, 65536, 40_000
+    with pytest.raises(smb.InvalidArgumentError):
+        sample_pattern_host(n_out, n_in, nnz, np.random.default_rng(0))
+    rp, ci = sample_pattern_large_host(n_out, n_in, nnz, smb.Rng(5).stream("pattern"))
+    assert rp[0] == 0 and rp[-1] == nnz and np.all(np.diff(rp) >= 0)
+    for i in np.flatnonzero(np.diff(rp))[:2000]:
+        row = ci[rp[i]:rp[i + 1]]
+        assert np.all(np.diff(row) > 0) and row[0] >= 0 and row[-1] < n_in
+    rp2, ci2 = oracle.sample_pattern_large(n_out, n_in, nnz, oracle.Streams(5)("pattern"))
+    assert np.array_equal(rp, rp2) and np.array_equal(ci, ci2)
