@@ -170,6 +170,12 @@ class FusedTrainStep:
         self.perm = None
         self.data = None
         self.steps_per_epoch = 0
+        # device-gather steps prefetch the NEXT batch into the other input
+        # slot right after the softmax step advanced the counter (side
+        # stream, overlapping the backward); _gslot is the slot the next
+        # gather step reads, _prefetched whether it already holds that batch
+        self._gslot = 0
+        self._prefetched = False
         # data-parallel flat gradient buffer: [values | bias] per layer
         self.flat = None
         if self.world > 1:
@@ -248,6 +254,7 @@ class FusedTrainStep:
             raise InvalidArgumentError("dataset shape does not match the model")
         self.data = ddata
         self._graphs.clear()
+        self._prefetched = False
 
     def set_epoch(self, perm: np.ndarray, rank_offset: int = 0) -> None:
         """Upload the epoch's sample order; this rank's batch k is
@@ -260,6 +267,15 @@ class FusedTrainStep:
         self.perm.copy_(flat)
         self.counter.zero_()
         self.steps_per_epoch = kb
+        self._prefetched = False  # the next step gathers batch 0 of this order first
+
+    def _gather_into(self, slot: int, st) -> None:
+        """xb / tb of the batch at the device step counter into input `slot`."""
+        d, B, ld, F32 = self.data, self.B, self.ld, _lib.SMB_F32
+        self._call("gather", "smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features,
+                   ptr(self.perm), ptr(self.counter), 0, B, ptr(self.x_slots[slot]), ld, st)
+        self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples, d.classes,
+                   ptr(self.perm), ptr(self.counter), 0, B, ptr(self.t_slots[slot]), ld, st)
 
     # ------------------------------------------------------------------
     def _bias_target(self, u, fuse_update: bool):
@@ -281,22 +297,8 @@ class FusedTrainStep:
         forked = False  # the side stream joins only after this step forked onto it
         main = torch.cuda.current_stream()
         side = self._side_stream() if overlap else None
-        if gather:
-            d = self.data
-            self._call("gather", "smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features,
-                       ptr(self.perm), ptr(self.counter), 0, B, ptr(x_in), ld, st)
-            if overlap:
-                # the label batch is only read by the softmax step: gather it
-                # beside the forward chain
-                side.wait_stream(main)
-                forked = True
-                with torch.cuda.stream(side):
-                    self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples,
-                               d.classes, ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in),
-                               ld, stream_ptr())
-            else:
-                self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples,
-                           d.classes, ptr(self.perm), ptr(self.counter), 0, B, ptr(t_in), ld, st)
+        # gather steps: this batch is already in x_in / t_in (prefetched by
+        # the previous step or by step()'s prologue)
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
         tail = self.fuse_tail
@@ -320,8 +322,6 @@ class FusedTrainStep:
         # applies the last layer's bias side and advances the step counter
         top = self.units[-1]
         b, vb, gb, kind, mu = self._bias_target(top, fuse_update)
-        if gather and overlap:
-            main.wait_stream(side)  # label batch gathered
         if tail:
             # one launch: logits -> softmax-CE gradient / B_global (+ loss,
             # step counter) -> d_{L-2} = (W_top^T d_top) * mask
@@ -350,6 +350,14 @@ class FusedTrainStep:
                        ld, ptr(self.loss), b, vb, gb, kind, mu, float(eta),
                        ptr(self.counter) if gather else None, int(self.steps_per_epoch),
                        ptr(self._ce_ws), st)
+        if gather:
+            # the counter now names the next batch: gather it into the other
+            # slot beside the backward chain
+            side = side if side is not None else self._side_stream()
+            side.wait_stream(main)
+            forked = True
+            with torch.cuda.stream(side):
+                self._gather_into(1 - self._slot, stream_ptr())
         # backward, last layer first: d_{l-1} (+ bias side of layer l-1) on the
         # main stream; the weight side of layer l (SDDMM + update) either
         # follows it in order, or -- single GPU -- runs on the side stream as
@@ -481,16 +489,24 @@ class FusedTrainStep:
             gather = self.data is not None
         if gather and (self.data is None or self.perm is None):
             raise InvalidArgumentError("attach_dataset() and set_epoch() before gathering steps")
-        self._slot = 0 if gather else int(slot)
+        if gather:
+            if not self._prefetched:  # prologue: the first batch of this order
+                self._gather_into(self._gslot, stream_ptr())
+                self._prefetched = True
+            self._slot = self._gslot
+        else:
+            self._slot = int(slot)
         if self.world == 1:
             self._replay_or_run(eta, gather, "all")
             self._flip_parity()
-            return
-        import torch.distributed as dist
+        else:
+            import torch.distributed as dist
 
-        self._replay_or_run(eta, gather, "fb")
-        dist.all_reduce(self.flat, group=self.pg)
-        self._replay_or_run(eta, gather, "upd")
+            self._replay_or_run(eta, gather, "fb")
+            dist.all_reduce(self.flat, group=self.pg)
+            self._replay_or_run(eta, gather, "upd")
+        if gather:
+            self._gslot ^= 1  # the next batch was prefetched into the other slot
 
     def _replay_or_run(self, eta, gather, part):
         if not self.use_graph:
