@@ -477,7 +477,8 @@ static int softmax_launch(int dtype, const void* y, int64_t ld_y, const void* t,
     const bool rows = grad_bias != nullptr || (opt_kind != SMB_OPT_NONE && bias != nullptr);
     const size_t block = sizeof(T) * (size_t)(classes * n);
     const size_t leaves1 = sizeof(T) * 32 * (size_t)warp_pairwise_leaves((int)n);
-    const bool single = !workspace || (leaves1 + block <= 180 * 1024 && n <= 64 * 1024);
+    // (without a bias side the step is a pure per-column map: many CTAs)
+    const bool single = !workspace || (rows && leaves1 + block <= 180 * 1024 && n <= 64 * 1024);
     const int threads = single ? 1024 : 128;
     const unsigned grid = single ? 1u : (unsigned)ceil_div(n > 0 ? n : 1, threads);
     unsigned* ticket = workspace ? static_cast<unsigned*>(workspace) : nullptr;

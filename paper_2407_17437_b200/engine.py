@@ -207,7 +207,7 @@ class FusedTrainStep:
         # weights (train.py:400-401); `parity` selects the current buffer.
         self.overlap = self.world == 1
         self._parity = 0
-        self._side = None
+        self._sides = {}
         for u in self.units:
             u.vals = None
             if u.sparse and self.overlap:
@@ -294,9 +294,18 @@ class FusedTrainStep:
         F32 = _lib.SMB_F32
         x_in, t_in = self.x_slots[self._slot], self.t_slots[self._slot]
         overlap = self.overlap and fuse_update
-        forked = False  # the side stream joins only after this step forked onto it
+        forked = []  # side streams this step forked onto (joined at the end)
+
+        def fork(key):
+            """A side stream (one per purpose, so the layers' updates and the
+            batch prefetch overlap each other as well as the main chain) that
+            starts after everything enqueued on main so far."""
+            s_ = self._side_stream(key)
+            s_.wait_stream(main)
+            if s_ not in forked:
+                forked.append(s_)
+            return s_
         main = torch.cuda.current_stream()
-        side = self._side_stream() if overlap else None
         # gather steps: this batch is already in x_in / t_in (prefetched by
         # the previous step or by step()'s prologue)
         # forward: a_l = act(W_l a_{l-1} + b_l)
@@ -335,15 +344,23 @@ class FusedTrainStep:
             # the bias sides of the top two layers cross columns: beside the
             # critical path when overlapping
             sides = ((top, self.dys[-1]), (below, self.dys[-2]))
-            if overlap:
-                side.wait_stream(main)
-                forked = True
-            with torch.cuda.stream(side) if overlap else _nullctx():
+            with torch.cuda.stream(fork("bias")) if overlap else _nullctx():
                 sst = stream_ptr()
                 for u, d_u in sides:
                     bb, bv, bg, bk, bmu = self._bias_target(u, fuse_update)
                     self._call(f"bias[{u.index}]", "smb_bias_grad_update", F32, ptr(d_u), ld, u.m,
                                B, bb, bv, bg, bk, bmu, float(eta), sst)
+        elif overlap:
+            # the column-parallel softmax step on the critical path; the last
+            # layer's bias row sums + update (they cross columns) beside it
+            self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
+                       ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]),
+                       ld, ptr(self.loss), None, None, None, _lib.SMB_OPT_NONE, 0.0, float(eta),
+                       ptr(self.counter) if gather else None, int(self.steps_per_epoch),
+                       ptr(self._ce_ws), st)
+            with torch.cuda.stream(fork(("weights", len(self.units) - 1))):
+                self._call(f"bias[{top.index}]", "smb_bias_grad_update", F32, ptr(self.dys[-1]),
+                           ld, top.m, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
         else:
             self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
                        ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]),
@@ -353,10 +370,7 @@ class FusedTrainStep:
         if gather:
             # the counter now names the next batch: gather it into the other
             # slot beside the backward chain
-            side = side if side is not None else self._side_stream()
-            side.wait_stream(main)
-            forked = True
-            with torch.cuda.stream(side):
+            with torch.cuda.stream(fork("prefetch")):
                 self._gather_into(1 - self._slot, stream_ptr())
         # backward, last layer first: d_{l-1} (+ bias side of layer l-1) on the
         # main stream; the weight side of layer l (SDDMM + update) either
@@ -369,9 +383,7 @@ class FusedTrainStep:
             dy = self.dys[li]
             x_prev = self.acts[li - 1] if li > 0 else x_in
             if overlap and u.sparse:
-                side.wait_stream(main)  # d_l is ready
-                forked = True
-                with torch.cuda.stream(side):
+                with torch.cuda.stream(fork(("weights", li))):  # d_l is ready
                     self._weight_side(u, dy, x_prev, eta, fuse_update, stream_ptr())
             if li > 0 and not (tail and li == L - 1):  # the tail produced d_{L-2}
                 below = self.units[li - 1]
@@ -393,13 +405,16 @@ class FusedTrainStep:
                                B, b, vb, gb, kind, mu, float(eta), st)
             if not (overlap and u.sparse):
                 self._weight_side(u, dy, x_prev, eta, fuse_update, st)
-        if forked:
-            main.wait_stream(side)  # join: the step ends when every update has
+        for s_ in forked:
+            main.wait_stream(s_)  # join: the step ends when every update has
 
-    def _side_stream(self):
-        if self._side is None:
-            self._side = torch.cuda.Stream(device=self.dev)
-        return self._side
+    def _side_stream(self, key):
+        s_ = self._sides.get(key)
+        if s_ is None:
+            # lowest priority: the main chain's CTAs are scheduled first
+            lo, _hi = torch.cuda.Stream.priority_range()
+            s_ = self._sides[key] = torch.cuda.Stream(device=self.dev, priority=lo)
+        return s_
 
     def _vals(self, u):
         """The current (pre-update) value buffer of sparse unit u."""
@@ -521,7 +536,8 @@ class FusedTrainStep:
             # does not execute, so the captured graph replays from step 2 on
             cur = torch.cuda.current_stream()
             if self._cap_stream is None:
-                self._cap_stream = torch.cuda.Stream(device=self.dev)
+                _lo, hi = torch.cuda.Stream.priority_range()
+                self._cap_stream = torch.cuda.Stream(device=self.dev, priority=hi)
             cs = self._cap_stream
             cs.wait_stream(cur)
             with torch.cuda.stream(cs):
