@@ -197,6 +197,9 @@ class FusedTrainStep:
         self.fuse_tail = bool(want and self.tail_ok)
         self._tail_ws = torch.zeros(int(_lib.load().smb_tail_step_workspace_bytes(self.B)),
                                     dtype=torch.uint8, device=dev) if self.tail_ok else None
+        # single GPU: bias row sums of transposed-SpMM outputs on a side stream
+        # instead of fused into the critical-path kernel's epilogue
+        self.split_bias = True
         self._graphs = {}
         self._cap_stream = None
         self.timer = None  # optional KernelTimer: per-launch CUDA events (eager only)
@@ -390,7 +393,16 @@ class FusedTrainStep:
                 mask = self.acts[li - 1] if below.relu else None
                 dst = self.dys[li - 1]
                 b, vb, gb, kind, mu = self._bias_target(below, fuse_update)
-                if u.sparse:
+                if u.sparse and overlap and self.split_bias:
+                    # d_{l-1} alone on the critical path; the bias side of
+                    # layer l-1 (row sums cross the batch) beside it
+                    self._call(f"spmm_t[{li}]", "smb_spmm_t", F32, lay.weights.pattern.handle,
+                               ptr(self._vals(u)), ptr(dy), ld, B, ptr(mask),
+                               ld if mask is not None else 0, ptr(dst), ld, st)
+                    with torch.cuda.stream(fork(("weights", li - 1))):
+                        self._call(f"bias[{li - 1}]", "smb_bias_grad_update", F32, ptr(dst), ld,
+                                   u.k, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
+                elif u.sparse:
                     self._call(f"spmm_t[{li}]", "smb_spmm_t_bias", F32, lay.weights.pattern.handle,
                                ptr(self._vals(u)), ptr(dy), ld, B, ptr(mask),
                                ld if mask is not None else 0, ptr(dst), ld, b, vb, gb, kind, mu,
