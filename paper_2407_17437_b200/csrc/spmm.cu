@@ -349,10 +349,10 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
                       ld_out % VW == 0 &&
                       (EPI != kEpiMask || epi.mask == nullptr ||
                        (aligned16(epi.mask) && epi.ld_mask % VW == 0));
-  // The widest lanes (2 x 16 B, then 16 B) whose warp count still fills 148
-  // SMs: wider lanes amortise the per-nonzero index / shuffle / address work
-  // over more columns.  With few rows one column per lane spreads each row
-  // over many more warps.
+  // One 16-byte vector per lane when the warp count fills 148 SMs (measured
+  // on B200 against 2 x 16 B lanes: 1.1-1.6x faster from config 2 to config 3
+  // sizes -- lower register pressure, more resident warps); with few rows one
+  // column per lane spreads each row over many more warps.
   auto enough = [&](int w) { return n >= 32 * w && n_rows * ceil_div(n, 32 * w) >= 148 * 8; };
   static const int force_w = [] {  // tuning experiments only
     const char* e = getenv("SMB_SPMM_W");
@@ -368,9 +368,9 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   else if (force_w == 8 && vec_ok)
     done = launch_rows<T, 2 * VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
                                                 n, out, ld_out, epi, st);
-  else if (vec_ok && enough(2 * VW))
-    done = launch_rows<T, 2 * VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
-                                                n, out, ld_out, epi, st);
+  else if (force_w == 5 && vec_ok)
+    done = launch_rows<T, VW, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                             out, ld_out, epi, st);
   else if (vec_ok && enough(VW))
     done = launch_rows<T, VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                             out, ld_out, epi, st);
