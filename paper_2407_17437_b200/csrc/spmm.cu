@@ -368,11 +368,26 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   else if (force_w == 8 && vec_ok)
     done = launch_rows<T, 2 * VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
                                                 n, out, ld_out, epi, st);
-  else if (force_w == 5 && vec_ok)
-    done = launch_rows<T, VW, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+  else if (force_w == 11)
+    done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                           out, ld_out, epi, st);
+  else if (force_w == 12)
+    done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                            out, ld_out, epi, st);
+  else if (force_w == 7 && vec_ok)
+    done = launch_rows<T, VW, 2, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                              out, ld_out, epi, st);
   else if (vec_ok && enough(VW))
-    done = launch_rows<T, VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+    done = launch_rows<T, VW, 4, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                            out, ld_out, epi, st);
+  // one column per lane: ring depth by shape (measured on B200: many short
+  // rows prefer a shallow ring -- more resident warps -- while a few long
+  // rows over a wide batch need the deep one)
+  else if (n_rows >= 148)
+    done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
+                                           out, ld_out, epi, st);
+  else if (n < 512)
+    done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                             out, ld_out, epi, st);
   else
     done = launch_rows<T, 1, 32, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,

@@ -1,6 +1,6 @@
 #!/bin/bash
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-for w in 0 5; do
+
+for w in 7; do
   echo "W=$w"
   SMB_SPMM_W=$w timeout 120 python scripts/probe_spmm_small.py
   SMB_SPMM_W=$w timeout 300 python -c "
@@ -11,4 +11,4 @@ for l in sys.stdin:
     if l.startswith('{'):
         j = json.loads(l); print(j['density'], j['B'], 'spmm', j['spmm']['us'], 'spmm_t', j['spmm_t']['us'], 'sddmm', j['sddmm_update']['us'])"
 done
-python scripts/probe_ablation.py 2>&1 | grep baseline
+
