@@ -267,9 +267,6 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
   if (pat->ntiles > 0) {
     constexpr int VW = 16 / sizeof(T);
     const bool vec = aligned16(x) && aligned16(d_out) && ld_x % VW == 0 && ld_d % VW == 0;
-    // 512-nonzero tiles (16 warps of chains per SM) when there are enough of
-    // them to fill the GPU; 128-nonzero tiles for small layers and fp64
-    const bool big = sizeof(T) == 4 && ceil_div(pat->nnz, 512) >= 148;
     auto go = [&](auto kernel, int tile, size_t bytes) {
       ensure_smem(kernel, bytes);
       kernel<<<(unsigned)ceil_div(pat->nnz, tile), tile, bytes, st>>>(
@@ -278,11 +275,13 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
           static_cast<const T*>(values), static_cast<T*>(values_out), static_cast<T*>(velocity),
           static_cast<T*>(grad_out), opt);
     };
-    // every tile's d_out rows staged -> fallback-free kernel (a 256-tile's
+    // every tile's d_out rows staged -> fallback-free kernel (a 256 / 512-tile's
     // span is bounded by its enclosing 512-tile's)
     auto all_for = [&](int tile, int sd) {
       return (tile == 128 ? pat->span128 : pat->span512) <= tile / sd;
     };
+    // tuning experiments only (scripts/gpu_sddmm_var2.sh): 1 = 512-nonzero
+    // tiles x 32 columns, 2 = 128 x 16 x 8 stages
     static const int variant = [] {
       const char* e = getenv("SMB_SDDMM_VARIANT");
       return e ? atoi(e) : 0;
@@ -298,25 +297,22 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     else                                                                                   \
       go(sddmm_pipe_kernel<T, TL, CHK, STG, SDV, false, false>, TL, C::smem_bytes);        \
   } while (0)
-#define SMB_GO(TL, CHK, STG) SMB_GO_SD(TL, CHK, STG, 4)
-    // Double-buffered wide chunks: 64 columns for layers below one 512-tile
-    // wave, 32 columns (184 KB) for 512-tiles.  Measured on B200 against
-    // 16/32-column chunks with 4-8 stages (env SMB_SDDMM_VARIANT): the
-    // per-chunk barrier + copy issue, not the copy latency, dominated.
-    if (sizeof(T) == 4 && !big && variant == 1) SMB_GO(128, 32, 4);
-    else if (sizeof(T) == 4 && !big && variant == 3) SMB_GO(128, 32, 2);
-    else if (sizeof(T) == 4 && !big && variant == 4) SMB_GO(128, 16, 8);
-    else if (sizeof(T) == 4 && !big && variant == 5) SMB_GO(128, 64, 4);
-    else if (sizeof(T) == 4 && big && variant == 6) SMB_GO(512, 16, 4);
-    else if (sizeof(T) == 4 && big && variant == 7) SMB_GO(256, 64, 2);
-    else if (big) SMB_GO(512, 32, 2);
-    // very sparse rows: a 128-tile spans more than 32 rows -> one staged
-    // d_out row per nonzero (139 KB, 1 CTA / SM) instead of the per-column
-    // global-load fallback
-    else if (sizeof(T) == 4 && !all_for(128, 4)) SMB_GO_SD(128, 64, 2, 1);
-    else if (sizeof(T) == 4) SMB_GO(128, 64, 2);
-    else SMB_GO(128, 16, 4);
-#undef SMB_GO
+    // Double-buffered chunks of 128-nonzero tiles: 64 columns (87 KB, 2 CTAs
+    // per SM) when every tile is resident in one wave (the per-chain critical
+    // path sets the time), 32 columns (46 KB, 4 CTAs per SM) beyond that.
+    // Measured on B200 against 256 / 512-nonzero tiles and 16-64-column
+    // chunks with 2-8 stages: more resident CTAs beat deeper per-CTA
+    // pipelines (1.3-1.4x at config 3).  Tiles spanning more than 32 rows
+    // (1-2 nonzeros per row) stage one d_out row per nonzero (SD = 1).
+    const bool wave = pat->ntiles <= 2 * 148;
+    const bool sparse_rows = !all_for(128, 4);
+    if (sizeof(T) == 4 && variant == 1) SMB_GO_SD(512, 32, 2, 4);
+    else if (sizeof(T) == 4 && variant == 2) SMB_GO_SD(128, 16, 8, 4);
+    else if (sizeof(T) == 4 && wave && sparse_rows) SMB_GO_SD(128, 64, 2, 1);
+    else if (sizeof(T) == 4 && wave) SMB_GO_SD(128, 64, 2, 4);
+    else if (sizeof(T) == 4 && sparse_rows) SMB_GO_SD(128, 32, 2, 1);
+    else if (sizeof(T) == 4) SMB_GO_SD(128, 32, 2, 4);
+    else SMB_GO_SD(128, 16, 4, 4);
 #undef SMB_GO_SD
     const int rc = check_launch(name);
     if (rc != SMB_OK) return rc;
