@@ -18,6 +18,7 @@ from paper_2407_17437_b200 import _lib
 from paper_2407_17437_b200.tensor_core import ptr, stream_ptr
 
 HBM = 6446.6  # GB/s, MEASURED_PEAKS.json hbm_gbs
+FP32_TFLOPS = 70.83  # FFMA peak, profiles/fp32_peak.json (scripts/fp32_peak.cu)
 
 
 def bytes_model(m, k, z, B):
@@ -70,8 +71,11 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
             bs = bytes_model(n, n, nnz, B)
             rec = {"density": d, "nnz": nnz, "B": B}
             for (kind, us), b in zip(res.items(), bs):
+                # t_roof = max(bytes / HBM, 2 z B / FP32 peak)
+                t_roof = max(b / (HBM * 1e9), 2 * nnz * B / (FP32_TFLOPS * 1e12))
                 rec[kind] = {"us": round(us, 2), "GB/s": round(b / us / 1e3, 1),
                              "frac_hbm": round(b / us / 1e3 / HBM, 3),
+                             "roof_frac": round(t_roof / (us * 1e-6), 3),
                              "Gpairs/s": round(nnz * B / us / 1e3, 1)}
             print(json.dumps(rec), flush=True)
 
