@@ -303,6 +303,94 @@ __global__ void __launch_bounds__(kSpmvWarps * 32)
   out[row * ld_out] = acc;
 }
 
+// Few long rows over a wide batch, one column per lane (the output layer at
+// config 2: 10 rows x ~310 nonzeros x B = 1024).  One warp per CTA; the loop
+// body consumes three 32-nonzero groups held in three register arrays, and
+// refills each array (operands, values and indices) three groups ahead right
+// after consuming it -- any move the compiler adds to rotate the registers
+// then sits three groups after its load, not one.  Order and rounding are
+// row_spmm_kernel's.  No fused row sums (the host keeps those elsewhere).
+template <typename T, int EPI, bool PERM>
+__global__ void __launch_bounds__(32)
+    row_spmm_deep_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
+                         const int32_t* __restrict__ perm, const T* __restrict__ vals,
+                         const T* __restrict__ dense, int64_t ld_dense, int64_t n,
+                         T* __restrict__ out, int64_t ld_out, EpiArgs<T> epi) {
+  const int lane = threadIdx.x;
+  const int64_t row = blockIdx.x;
+  const int64_t col = (int64_t)blockIdx.y * 32 + lane;
+  const bool valid = col < n;
+  const T* dcol = dense + (valid ? col : 0);
+  const uint32_t ldu = (uint32_t)ld_dense;
+  const int32_t s_begin = seg_ptr[row], s_end = seg_ptr[row + 1];
+  const int len = s_end - s_begin;
+  const int ngroups = (len + 31) / 32;
+  T bias_r = T(0), mk = T(0);
+  if constexpr (EPI == kEpiBiasAct) {
+    if (epi.bias != nullptr) bias_r = epi.bias[row];
+  } else {
+    if (epi.mask != nullptr && valid) mk = epi.mask[row * epi.ld_mask + col];
+  }
+  auto ld_idx = [&](int g) -> int {  // index of position (g, lane); 0 past the row
+    const int32_t s = s_begin + g * 32 + lane;
+    return s < s_end ? idx[s] : 0;
+  };
+  auto ld_val = [&](int g) -> T {
+    const int32_t s = s_begin + g * 32 + lane;
+    return s < s_end ? (PERM ? vals[perm[s]] : vals[s]) : T(0);
+  };
+  auto gather = [&](T (&x)[32], int gi) {  // operands of a group from its indices
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      x[q] = ldg_stream(dcol + (size_t)(uint32_t)__shfl_sync(0xffffffffu, gi, q) * ldu);
+  };
+  T acc = T(0);
+  auto consume = [&](const T (&x)[32], T v, int cnt) {
+    if (cnt == 32) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc = add_rn(acc, mul_rn(__shfl_sync(0xffffffffu, v, q), x[q]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const T vq = __shfl_sync(0xffffffffu, v, q);
+        if (q < cnt) acc = add_rn(acc, mul_rn(vq, x[q]));
+      }
+    }
+  };
+  T xa[32], xb[32], xc[32];
+  T va = ld_val(0), vb = ld_val(1), vc = ld_val(2);
+  gather(xa, ld_idx(0));
+  gather(xb, ld_idx(1));
+  gather(xc, ld_idx(2));
+  int ia = ld_idx(3), ib = ld_idx(4), ic = ld_idx(5);
+  int g = 0;
+  for (; g + 3 <= ngroups; g += 3) {
+    consume(xa, va, 32 * (g + 1) <= len ? 32 : len - 32 * g);
+    gather(xa, ia);
+    va = ld_val(g + 3);
+    ia = ld_idx(g + 6);
+    consume(xb, vb, 32 * (g + 2) <= len ? 32 : len - 32 * (g + 1));
+    gather(xb, ib);
+    vb = ld_val(g + 4);
+    ib = ld_idx(g + 7);
+    consume(xc, vc, 32 * (g + 3) <= len ? 32 : len - 32 * (g + 2));
+    gather(xc, ic);
+    vc = ld_val(g + 5);
+    ic = ld_idx(g + 8);
+  }
+  // up to two remaining groups, in array order
+  if (g < ngroups) consume(xa, va, min(32, len - 32 * g));
+  if (g + 1 < ngroups) consume(xb, vb, min(32, len - 32 * (g + 1)));
+  if (!valid) return;
+  if constexpr (EPI == kEpiBiasAct) {
+    if (epi.bias != nullptr) acc = add_rn(acc, bias_r);
+    if (epi.relu) acc = relu_np(acc);
+  } else {
+    if (epi.mask != nullptr) acc = mask_np(acc, mk);
+  }
+  out[row * ld_out + col] = acc;
+}
+
 template <typename T, int W, int U, int EPI, bool PERM>
 bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm, const T* vals,
                  int64_t n_rows, const T* dense, int64_t ld_dense, int64_t n, T* out,
@@ -386,7 +474,12 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   else if (n_rows >= 148)
     done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                            out, ld_out, epi, st);
-  else if (n < 512)
+  else if (!(EPI == kEpiMask && epi.rowsum) && force_w != 13) {
+    row_spmm_deep_kernel<T, EPI, PERM><<<dim3((unsigned)n_rows, (unsigned)ceil_div(n, 32)), 32, 0,
+                                         st>>>(seg_ptr, idx, perm, vals, dense, ld_dense, n, out,
+                                               ld_out, epi);
+    done = false;
+  } else if (n < 512)
     done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                             out, ld_out, epi, st);
   else

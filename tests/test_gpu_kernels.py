@@ -357,3 +357,27 @@ def test_spmv_single_column_strided_with_epilogue(oracle, relu):
     got = host(out)
     assert bits_equal(got[:, :1], want)
     assert np.all(got[:, 1:] == 7.0)  # padding columns untouched
+
+
+@pytest.mark.parametrize("shape,density", [((10, 512, 1024), 0.6), ((7, 300, 777), 0.9),
+                                           ((20, 2000, 600), 0.3), ((3, 50, 515), 0.05)])
+def test_few_long_rows_wide_batch_bit_exact(oracle, shape, density):
+    """Few output rows x wide batch (the output layer at B >= 512): the
+    three-group register-pipelined kernel, forward with bias + ReLU and
+    transposed with mask, bit-exact."""
+    m, k, n = shape
+    rng = np.random.default_rng(m * 7 + n)
+    rp, ci, v, _ = random_csr(rng, m, k, density, np.float32, empty_rows=True)
+    s = smb.CsrMatrix(m, k, rp, ci, v)
+    x = rng.standard_normal((k, n)).astype(np.float32)
+    b = rng.standard_normal(m).astype(np.float32)
+    got = smb.spmm(s, x, bias=dev(b), relu=True)
+    assert bits_equal(got, np.maximum(oracle.spmm(rp, ci, v, x) + b[:, None], 0))
+    # transposed over the CSC of a few-column matrix: few output rows again
+    st = smb.CsrMatrix(k, m, *random_csr(rng, k, m, density, np.float32)[:3])
+    d = rng.standard_normal((k, n)).astype(np.float32)
+    mk = rng.standard_normal((m, n)).astype(np.float32)
+    rp2, ci2 = tc.to_numpy(st.row_ptr), tc.to_numpy(st.col_idx)
+    want = oracle.spmm_t(rp2, ci2, tc.to_numpy(st.values), m, d)
+    want = want * (mk > 0)
+    assert bits_equal(smb.spmm_transposed(st, d, mask=dev(mk)), want)
