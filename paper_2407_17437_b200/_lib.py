@@ -16,7 +16,8 @@ from pathlib import Path
 
 from .errors import DeviceError, InvalidArgumentError, StateError
 
-LIB_PATH = Path(__file__).resolve().parent / "libsparsemlp_b200.so"
+# SMB_LIB overrides the library file (tuning experiments load alternative builds)
+LIB_PATH = Path(os.environ.get("SMB_LIB") or Path(__file__).resolve().parent / "libsparsemlp_b200.so")
 
 SMB_OK, SMB_ERR_INVALID, SMB_ERR_STATE, SMB_ERR_CUDA = 0, 1, 2, 3
 SMB_F32, SMB_F64 = 0, 1
