@@ -131,7 +131,8 @@ class _Unit:
 
 class FusedTrainStep:
     def __init__(self, model, batch_size: int, global_batch: int | None = None,
-                 process_group=None, use_graph: bool = True, fuse_tail: bool | None = None):
+                 process_group=None, use_graph: bool = True, fuse_tail: bool | None = None,
+                 force_dp: bool = False):
         self.units = self._parse(model)
         self.model = model
         self.B = int(batch_size)
@@ -144,6 +145,11 @@ class FusedTrainStep:
             import torch.distributed as dist
 
             self.world = dist.get_world_size(process_group)
+        # data-parallel structure: a forward/backward pass that only produces
+        # gradients (flat buffer), the all-reduce, then the update pass.
+        # force_dp runs that structure on one process (testing; the
+        # all-reduce is then skipped)
+        self.dp = self.world > 1 or bool(force_dp)
         self.use_graph = use_graph
         dev = self.units[0].layer.bias.device
         self.dev = dev
@@ -178,7 +184,7 @@ class FusedTrainStep:
         self._prefetched = False
         # data-parallel flat gradient buffer: [values | bias] per layer
         self.flat = None
-        if self.world > 1:
+        if self.dp:
             layout, total = flat_layout([(u.m, u.nvals) for u in self.units])
             for u, (g_off, b_off) in zip(self.units, layout):
                 u.grad_off, u.bias_off = g_off, b_off
@@ -203,17 +209,18 @@ class FusedTrainStep:
         self._graphs = {}
         self._cap_stream = None
         self.timer = None  # optional KernelTimer: per-launch CUDA events (eager only)
-        # Single-GPU steps run each sparse layer's SDDMM+update on a side
-        # stream, concurrently with the transposed-SpMM chain.  The update
+        # Each sparse layer's weight side (SDDMM + update, or SDDMM into the
+        # flat buffer when data parallel) runs on its own side stream,
+        # concurrently with the transposed-SpMM chain.  A single-GPU update
         # writes the second of two value buffers (ping-pong), so the
         # transposed SpMM of the same layer keeps reading the pre-update
         # weights (train.py:400-401); `parity` selects the current buffer.
-        self.overlap = self.world == 1
+        self.overlap = True
         self._parity = 0
         self._sides = {}
         for u in self.units:
             u.vals = None
-            if u.sparse and self.overlap:
+            if u.sparse and self.overlap and not self.dp:
                 cur = u.layer.weights.values
                 u.vals = [cur, cur.clone()]
 
@@ -296,7 +303,7 @@ class FusedTrainStep:
         B, ld = self.B, self.ld
         F32 = _lib.SMB_F32
         x_in, t_in = self.x_slots[self._slot], self.t_slots[self._slot]
-        overlap = self.overlap and fuse_update
+        overlap = self.overlap
         forked = []  # side streams this step forked onto (joined at the end)
 
         def fork(key):
@@ -500,7 +507,7 @@ class FusedTrainStep:
 
     # ------------------------------------------------------------------
     def _run_eager(self, eta: float, gather: bool, part: str) -> None:
-        if self.world == 1:
+        if not self.dp:
             self._launch_forward_backward(eta, True, gather)
         elif part == "fb":
             self._launch_forward_backward(eta, False, gather)
@@ -523,14 +530,15 @@ class FusedTrainStep:
             self._slot = self._gslot
         else:
             self._slot = int(slot)
-        if self.world == 1:
+        if not self.dp:
             self._replay_or_run(eta, gather, "all")
             self._flip_parity()
         else:
-            import torch.distributed as dist
-
             self._replay_or_run(eta, gather, "fb")
-            dist.all_reduce(self.flat, group=self.pg)
+            if self.world > 1:
+                import torch.distributed as dist
+
+                dist.all_reduce(self.flat, group=self.pg)
             self._replay_or_run(eta, gather, "upd")
         if gather:
             self._gslot ^= 1  # the next batch was prefetched into the other slot

@@ -221,3 +221,29 @@ def test_config5_injected_patterns_track_oracle(oracle):
         ref_loss = ref.step(data.Xtrain[:, k * B:(k + 1) * B], data.Ttrain[:, k * B:(k + 1) * B], eta)
         assert abs(step.loss_value() - ref_loss) <= 1e-4 * abs(ref_loss)
     assert max_rel(model, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("density,B", [(0.01, 128), (0.1, 100)])
+def test_data_parallel_structure_on_one_gpu_equals_fused(density, B):
+    """The data-parallel step structure (gradients into the flat buffer with
+    side-stream overlap, [all-reduce], update pass from the flat buffer) run
+    on one GPU (force_dp: the all-reduce is the identity) is bit-identical to
+    the fused single-GPU step -- the update arithmetic is the same
+    sparse_combine / _step_vector sequence either way."""
+    chain, steps, eta = [3072, 1024, 512, 10], 4, 0.03
+    data = smb.synthetic_dataset(seed=9, n_samples=B * steps, features=chain[0])
+    cfg = smb.ExperimentConfig(layer_dims=chain, density=density, seed=2, batch_size=B, lr=eta)
+    models = []
+    for force_dp in (False, True):
+        model, _ = smb.build_model(cfg)
+        st = smb.FusedTrainStep(model, B, force_dp=force_dp)
+        assert st.dp == force_dp
+        st.attach_dataset(smb.DeviceDataset(data))
+        st.set_epoch(np.arange(B * steps))
+        for _ in range(steps):
+            st.step(eta)
+        models.append(model)
+    torch.cuda.synchronize()
+    for (n1, a), (n2, b) in zip(params_host(models[0]), params_host(models[1])):
+        assert n1 == n2
+        assert bits_equal(a, b), n1
