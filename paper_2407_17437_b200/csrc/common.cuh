@@ -42,6 +42,37 @@ inline void ensure_smem(K* kernel, size_t bytes) {
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+).  Every kernel is launched with
+// programmatic stream serialisation allowed: the next kernel on a stream may
+// be scheduled while the previous one drains, runs its independent prologue
+// (indices, values, bias -- never the previous kernel's output), then
+// pdl_wait()s, which returns once the previous grid has completed and its
+// writes are visible.  Producers pdl_trigger() when their main loop is done.
+// Both are no-ops when the launch carries no programmatic dependency (first
+// kernel after an event wait, eager launches on other streams, ...).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// ---------------------------------------------------------------------------
 // exact arithmetic: multiply and add rounded separately, never contracted.
 // (The library is also compiled with --fmad=false as a second guard.)
 // ---------------------------------------------------------------------------

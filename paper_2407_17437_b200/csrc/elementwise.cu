@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     bias_rows_kernel(const T* __restrict__ d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias,
                      T* grad, OptConsts<T> opt) {
   __shared__ T leaf[kRowWarps][kWarpLeafCap];
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + warp;
   if (row >= m) return;
@@ -111,8 +112,8 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 // The per-column loss log(s) - sum_c z*t is reduced per CTA in a fixed tree
 // and across CTAs by the last CTA to finish (ticket), which then also runs
 // the last layer's bias row sums / update and advances the step counter.
-template <typename T>
-__global__ void __launch_bounds__(1024)
+template <typename T, bool ROWS>
+__global__ void __launch_bounds__(ROWS ? 1024 : 128)
     softmax_step_kernel(const T* __restrict__ y, int64_t ld_y, const T* __restrict__ t,
                         int64_t ld_t, int64_t classes, int64_t n, T divisor, T* dy, int64_t ld_dy,
                         double* loss_out, double* loss_parts, unsigned* ticket, T* bias, T* vbias,
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(1024)
   // dynamic smem: [warps x pairwise leaves][classes x n staged d_y block]
   T* stage_dst =
       reinterpret_cast<T*>(smem_raw) + (blockDim.x >> 5) * warp_pairwise_leaves((int)n);
+  pdl_wait();  // y is the previous kernel's output
   double local = 0.0;
   // bias state of row `warp` (the first row this warp sums), loaded now
   T pb_w = T(0), pb_v = T(0);
@@ -186,6 +188,7 @@ __global__ void __launch_bounds__(1024)
     }
     local += static_cast<double>(sub_rn(log_full(s), zt));
   }
+  pdl_trigger();
   // fixed-order block reduction of the loss
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
@@ -215,6 +218,9 @@ __global__ void __launch_bounds__(1024)
   if (counter && threadIdx.x == 0) {
     const int32_t v = *counter + 1;
     *counter = (modulo > 0 && v >= modulo) ? 0 : v;
+  }
+  if constexpr (!ROWS) {
+    return;  // column-only variant: no bias side compiled in
   }
   if (grad_bias == nullptr && !(opt.kind != SMB_OPT_NONE && bias)) return;
   // stage_rows: the whole classes x n block of d_y fits the dynamic smem the
@@ -292,6 +298,7 @@ __global__ void __launch_bounds__(256)
   constexpr int FT = 128;  // features per tile
   __shared__ T tile[32][FT + 1];
   __shared__ int32_t s_idx[32];
+  pdl_wait();  // the step counter is written by the softmax step
   const int64_t b0 = step_counter ? (int64_t)(*step_counter) * batch : base;
   const int64_t j0 = (int64_t)blockIdx.x * 32;
   const int64_t f0 = (int64_t)blockIdx.y * FT;
@@ -344,7 +351,7 @@ template <typename T>
 int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias, T* grad,
                      const OptConsts<T>& opt, cudaStream_t st) {
   if (m == 0) return SMB_OK;
-  bias_rows_kernel<T><<<(unsigned)ceil_div(m, kRowWarps), kRowWarps * 32, 0, st>>>(
+  launch_k(bias_rows_kernel<T>, dim3((unsigned)ceil_div(m, kRowWarps)), dim3(kRowWarps * 32), 0, st,
       d, ld, m, n, bias, vbias, grad, opt);
   return check_launch("bias_rows");
 }
@@ -487,13 +494,14 @@ static int softmax_launch(int dtype, const void* y, int64_t ld_y, const void* t,
     size_t dyn = rows ? sizeof(T) * (threads / 32) * (size_t)warp_pairwise_leaves((int)n) : 0;
     const int stage = rows && dyn + block <= 180 * 1024;
     if (stage) dyn += block;
-    auto kern = softmax_step_kernel<T>;
+    // column-only instance (128-thread bound: no spills) for multi-CTA launches
+    auto kern = (rows || single) ? softmax_step_kernel<T, true> : softmax_step_kernel<T, false>;
     if (dyn > 40 * 1024) ensure_smem(kern, dyn);
-    kern<<<grid, threads, dyn, as_stream(stream)>>>(
-        static_cast<const T*>(y), ld_y, static_cast<const T*>(t), ld_t, classes, n,
-        static_cast<T>(divisor), static_cast<T*>(d_y), ld_dy, loss_out, parts, ticket,
-        static_cast<T*>(bias), static_cast<T*>(vbias), static_cast<T*>(grad_bias),
-        make_opt<T>(opt_kind, mu, eta), counter, modulo, stage);
+    launch_k(kern, dim3(grid), dim3(threads), dyn, as_stream(stream), static_cast<const T*>(y),
+             ld_y, static_cast<const T*>(t), ld_t, classes, n, static_cast<T>(divisor),
+             static_cast<T*>(d_y), ld_dy, loss_out, parts, ticket, static_cast<T*>(bias),
+             static_cast<T*>(vbias), static_cast<T*>(grad_bias), make_opt<T>(opt_kind, mu, eta),
+             counter, modulo, stage);
     return check_launch("smb_softmax_ce");
   });
 }
@@ -568,13 +576,13 @@ extern "C" int smb_gather_columns(int dtype, const void* src, int64_t n_samples,
     dim3 grid((unsigned)ceil_div(batch, 32), (unsigned)ceil_div(features, 128));
     const bool vec = aligned16(src) && (features * (int64_t)sizeof(T)) % 16 == 0;
     if (vec)
-      gather_columns_kernel<T, true><<<grid, 256, 0, as_stream(stream)>>>(
-          static_cast<const T*>(src), features, perm, step_counter, base, batch,
-          static_cast<T*>(dst), ld_dst);
+      launch_k(gather_columns_kernel<T, true>, grid, dim3(256), 0, as_stream(stream),
+               static_cast<const T*>(src), features, perm, step_counter, base, batch,
+               static_cast<T*>(dst), ld_dst);
     else
-      gather_columns_kernel<T, false><<<grid, 256, 0, as_stream(stream)>>>(
-          static_cast<const T*>(src), features, perm, step_counter, base, batch,
-          static_cast<T*>(dst), ld_dst);
+      launch_k(gather_columns_kernel<T, false>, grid, dim3(256), 0, as_stream(stream),
+               static_cast<const T*>(src), features, perm, step_counter, base, batch,
+               static_cast<T*>(dst), ld_dst);
     return check_launch("smb_gather_columns");
   });
 }

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(TILE)
   }
   const unsigned sbase = smem_u32(smem);
   constexpr unsigned kStageBytes = (unsigned)(C::stage_elems * sizeof(T));
+  pdl_wait();  // d_out / x are earlier kernels' outputs
 
   auto issue = [&](int ch) {
     const unsigned st = sbase + (unsigned)(ch & (S - 1)) * kStageBytes;
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(TILE)
     }
   }
   cp_async_wait<0>();
+  pdl_trigger();
   if (!active) return;
   const T g = (n == 0) ? T(0) : acc;  // tensor_core.py:283-284: zero batch -> zeros
   if (grad_out) grad_out[p] = g;
@@ -269,11 +271,11 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     const bool vec = aligned16(x) && aligned16(d_out) && ld_x % VW == 0 && ld_d % VW == 0;
     auto go = [&](auto kernel, int tile, size_t bytes) {
       ensure_smem(kernel, bytes);
-      kernel<<<(unsigned)ceil_div(pat->nnz, tile), tile, bytes, st>>>(
-          pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz,
-          static_cast<const T*>(d_out), ld_d, static_cast<const T*>(x), ld_x, n,
-          static_cast<const T*>(values), static_cast<T*>(values_out), static_cast<T*>(velocity),
-          static_cast<T*>(grad_out), opt);
+      launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, tile)), dim3(tile), bytes, st,
+               pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz,
+               static_cast<const T*>(d_out), ld_d, static_cast<const T*>(x), ld_x, n,
+               static_cast<const T*>(values), static_cast<T*>(values_out),
+               static_cast<T*>(velocity), static_cast<T*>(grad_out), opt);
     };
     // every tile's d_out rows staged -> fallback-free kernel (a 256 / 512-tile's
     // span is bounded by its enclosing 512-tile's)

@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(max_threads_for<W>())
       if (epi.rb_vbias) rb_v = epi.rb_vbias[row];
     }
   }
+  // everything above reads data older than the previous kernel on this
+  // stream; the dense operand below is that kernel's output
+  pdl_wait();
   // lanes with 0 < valid < W (the batch tail) need element-wise loads
   const bool lane_full = valid == W || valid == 0;
   auto refill = [&](Frag<T, W>& f, int src) {
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(max_threads_for<W>())
     val_n = val_nn;
     load_group(g + 3, idx_nn, val_nn);
   }
+  pdl_trigger();
 
   if constexpr (EPI == kEpiBiasAct) {
     if (valid == 0) return;
@@ -273,6 +277,7 @@ __global__ void __launch_bounds__(kSpmvWarps * 32)
                     const T* __restrict__ dense, int64_t ld_dense, int64_t n_rows,
                     T* __restrict__ out, int64_t ld_out, EpiArgs<T> epi) {
   __shared__ T s_p[kSpmvWarps][32];
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = (int64_t)blockIdx.x * kSpmvWarps + warp;
   if (row >= n_rows) return;
@@ -359,9 +364,11 @@ __global__ void __launch_bounds__(32)
   };
   T xa[32], xb[32], xc[32];
   T va = ld_val(0), vb = ld_val(1), vc = ld_val(2);
-  gather(xa, ld_idx(0));
-  gather(xb, ld_idx(1));
-  gather(xc, ld_idx(2));
+  const int i0 = ld_idx(0), i1 = ld_idx(1), i2 = ld_idx(2);
+  pdl_wait();  // the dense operand is the previous kernel's output
+  gather(xa, i0);
+  gather(xb, i1);
+  gather(xc, i2);
   int ia = ld_idx(3), ib = ld_idx(4), ic = ld_idx(5);
   int g = 0;
   for (; g + 3 <= ngroups; g += 3) {
@@ -381,6 +388,7 @@ __global__ void __launch_bounds__(32)
   // up to two remaining groups, in array order
   if (g < ngroups) consume(xa, va, min(32, len - 32 * g));
   if (g + 1 < ngroups) consume(xb, vb, min(32, len - 32 * (g + 1)));
+  pdl_trigger();
   if (!valid) return;
   if constexpr (EPI == kEpiBiasAct) {
     if (epi.bias != nullptr) acc = add_rn(acc, bias_r);
@@ -413,8 +421,8 @@ bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm
   auto kern = row_spmm_kernel<T, W, U, EPI, PERM>;
   if (dyn > 40 * 1024)
     ensure_smem(kern, dyn);
-  kern<<<dim3((unsigned)n_rows, (unsigned)gy), warps * 32, dyn, st>>>(
-      seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out, epi);
+  launch_k(kern, dim3((unsigned)n_rows, (unsigned)gy), dim3(warps * 32), dyn, st, seg_ptr, idx,
+           perm, vals, dense, ld_dense, n, out, ld_out, epi);
   return epi.rowsum != 0;
 }
 
@@ -427,9 +435,9 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   if (rowsum_done) *rowsum_done = false;
   if (n_rows == 0 || n == 0) return SMB_OK;
   if (n == 1 && !epi.rowsum) {  // one batch column: warp-per-row SpMV
-    row_spmv_kernel<T, EPI, PERM><<<(unsigned)ceil_div(n_rows, kSpmvWarps), kSpmvWarps * 32, 0,
-                                   st>>>(seg_ptr, idx, perm, vals, dense, ld_dense, n_rows, out,
-                                         ld_out, epi);
+    launch_k(row_spmv_kernel<T, EPI, PERM>, dim3((unsigned)ceil_div(n_rows, kSpmvWarps)),
+             dim3(kSpmvWarps * 32), 0, st, seg_ptr, idx, perm, vals, dense, ld_dense, n_rows, out,
+             ld_out, epi);
     return check_launch(name);
   }
   constexpr int VW = Vec16<T>::N;
@@ -475,9 +483,8 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
     done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                            out, ld_out, epi, st);
   else if (!(EPI == kEpiMask && epi.rowsum) && force_w != 13) {
-    row_spmm_deep_kernel<T, EPI, PERM><<<dim3((unsigned)n_rows, (unsigned)ceil_div(n, 32)), 32, 0,
-                                         st>>>(seg_ptr, idx, perm, vals, dense, ld_dense, n, out,
-                                               ld_out, epi);
+    launch_k(row_spmm_deep_kernel<T, EPI, PERM>, dim3((unsigned)n_rows, (unsigned)ceil_div(n, 32)),
+             dim3(32), 0, st, seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out, epi);
     done = false;
   } else if (n < 512)
     done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
