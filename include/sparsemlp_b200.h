@@ -267,6 +267,15 @@ SMB_API int smb_gather_columns(int dtype, const void* src, int64_t n_samples, in
                        const int32_t* perm, const int32_t* step_counter, int64_t base,
                        int64_t batch, void* dst, int64_t ld_dst, void* stream);
 
+/* The same gather for the batch `step_offset` steps ahead of the device step
+ * counter: batch index ((*step_counter + step_offset) mod modulo) (modulo 0:
+ * no wrap).  Lets the next batch be gathered while the current step runs. */
+SMB_API int smb_gather_columns_ahead(int dtype, const void* src, int64_t n_samples,
+                                     int64_t features, const int32_t* perm,
+                                     const int32_t* step_counter, int32_t step_offset,
+                                     int32_t modulo, int64_t batch, void* dst, int64_t ld_dst,
+                                     void* stream);
+
 /* *counter = (*counter + 1) % modulo  (device-side step index for CUDA-graph
  * replays of the training step). */
 SMB_API int smb_step_counter_advance(int32_t* counter, int32_t modulo, void* stream);

@@ -79,6 +79,8 @@ SIGNATURES = {
     "smb_relu_backward": (_i32, [_i32, _p, _i64, _p, _i64, _i64, _i64, _p, _i64, _p]),
     "smb_gather_columns": (_i32, [_i32, _p, _i64, _i64, _p, _p, _i64, _i64, _p, _i64, _p]),
     "smb_step_counter_advance": (_i32, [_p, _i32, _p]),
+    "smb_gather_columns_ahead": (_i32, [_i32, _p, _i64, _i64, _p, _p, _i32, _i32, _i64, _p, _i64,
+                                        _p]),
     "smb_xavier_pcg64": (_i32, [_i32, _u64, _u64, _u64, _u64, _u64, _i64, _f64, _p, _p]),
 }
 

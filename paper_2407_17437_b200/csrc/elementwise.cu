@@ -294,12 +294,18 @@ template <typename T, bool VEC>
 __global__ void __launch_bounds__(256)
     gather_columns_kernel(const T* __restrict__ src, int64_t features,
                           const int32_t* __restrict__ perm, const int32_t* __restrict__ step_counter,
-                          int64_t base, int64_t batch, T* __restrict__ dst, int64_t ld_dst) {
+                          int64_t base, int32_t step_offset, int32_t modulo, int64_t batch,
+                          T* __restrict__ dst, int64_t ld_dst) {
   constexpr int FT = 128;  // features per tile
   __shared__ T tile[32][FT + 1];
   __shared__ int32_t s_idx[32];
-  pdl_wait();  // the step counter is written by the softmax step
-  const int64_t b0 = step_counter ? (int64_t)(*step_counter) * batch : base;
+  pdl_wait();  // the step counter may be the previous kernel's output
+  int64_t b0 = base;
+  if (step_counter) {
+    int64_t k = (int64_t)(*step_counter) + step_offset;
+    if (modulo > 0) k %= modulo;
+    b0 = k * batch;
+  }
   const int64_t j0 = (int64_t)blockIdx.x * 32;
   const int64_t f0 = (int64_t)blockIdx.y * FT;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -561,9 +567,34 @@ extern "C" int smb_relu_backward(int dtype, const void* d_out, int64_t ld_d, con
   });
 }
 
+static int gather_launch(int dtype, const void* src, int64_t n_samples, int64_t features,
+                         const int32_t* perm, const int32_t* step_counter, int64_t base,
+                         int32_t step_offset, int32_t modulo, int64_t batch, void* dst,
+                         int64_t ld_dst, void* stream);
+
 extern "C" int smb_gather_columns(int dtype, const void* src, int64_t n_samples, int64_t features,
                                   const int32_t* perm, const int32_t* step_counter, int64_t base,
                                   int64_t batch, void* dst, int64_t ld_dst, void* stream) {
+  return gather_launch(dtype, src, n_samples, features, perm, step_counter, base, 0, 0, batch,
+                       dst, ld_dst, stream);
+}
+
+extern "C" int smb_gather_columns_ahead(int dtype, const void* src, int64_t n_samples,
+                                        int64_t features, const int32_t* perm,
+                                        const int32_t* step_counter, int32_t step_offset,
+                                        int32_t modulo, int64_t batch, void* dst, int64_t ld_dst,
+                                        void* stream) {
+  clear_error();
+  SMB_REQUIRE(step_counter != nullptr, "smb_gather_columns_ahead: null step counter");
+  SMB_REQUIRE(step_offset >= 0 && modulo >= 0, "smb_gather_columns_ahead: bad offset / modulo");
+  return gather_launch(dtype, src, n_samples, features, perm, step_counter, 0, step_offset,
+                       modulo, batch, dst, ld_dst, stream);
+}
+
+static int gather_launch(int dtype, const void* src, int64_t n_samples, int64_t features,
+                         const int32_t* perm, const int32_t* step_counter, int64_t base,
+                         int32_t step_offset, int32_t modulo, int64_t batch, void* dst,
+                         int64_t ld_dst, void* stream) {
   clear_error();
   SMB_REQUIRE(n_samples >= 0 && features >= 0 && batch >= 0 && ld_dst >= batch,
               "smb_gather_columns: bad shape");
@@ -577,12 +608,12 @@ extern "C" int smb_gather_columns(int dtype, const void* src, int64_t n_samples,
     const bool vec = aligned16(src) && (features * (int64_t)sizeof(T)) % 16 == 0;
     if (vec)
       launch_k(gather_columns_kernel<T, true>, grid, dim3(256), 0, as_stream(stream),
-               static_cast<const T*>(src), features, perm, step_counter, base, batch,
-               static_cast<T*>(dst), ld_dst);
+               static_cast<const T*>(src), features, perm, step_counter, base, step_offset,
+               modulo, batch, static_cast<T*>(dst), ld_dst);
     else
       launch_k(gather_columns_kernel<T, false>, grid, dim3(256), 0, as_stream(stream),
-               static_cast<const T*>(src), features, perm, step_counter, base, batch,
-               static_cast<T*>(dst), ld_dst);
+               static_cast<const T*>(src), features, perm, step_counter, base, step_offset,
+               modulo, batch, static_cast<T*>(dst), ld_dst);
     return check_launch("smb_gather_columns");
   });
 }

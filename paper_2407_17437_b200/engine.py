@@ -9,7 +9,8 @@ of the reference's per-batch loop (train.py:389-402):
     backward    d_{l-1} = (W_l^T d_l) * (a_{l-1} > 0)           smb_spmm_t_bias (mask fused,
                 + row_sums(d_{l-1}), update b_{l-1}              + bias side of layer l-1)
                 grad_l = sddmm(d_l, a_{l-1}); update W_l        smb_sddmm_update (fused)
-    next batch  step counter += 1                               (softmax kernel's last CTA)
+    next batch  gathered ahead into the other input slot, step  smb_gather_columns_ahead +
+                counter += 1 (own stream, beside the forward)   smb_step_counter_advance
 
 spmm_t of layer l runs before the update of layer l (pre-update weights,
 train.py:400-401).  The layer-1 input gradient is never computed: the
@@ -279,13 +280,25 @@ class FusedTrainStep:
         self.steps_per_epoch = kb
         self._prefetched = False  # the next step gathers batch 0 of this order first
 
-    def _gather_into(self, slot: int, st) -> None:
-        """xb / tb of the batch at the device step counter into input `slot`."""
+    def _gather_into(self, slot: int, st, ahead: bool = False) -> None:
+        """xb / tb of the batch at the device step counter (ahead: the next
+        batch, then advance the counter) into input `slot`.  The counter
+        names the batch in the slot the current step reads; only this
+        gather stream reads or writes it during a step."""
         d, B, ld, F32 = self.data, self.B, self.ld, _lib.SMB_F32
-        self._call("gather", "smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features,
-                   ptr(self.perm), ptr(self.counter), 0, B, ptr(self.x_slots[slot]), ld, st)
-        self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples, d.classes,
-                   ptr(self.perm), ptr(self.counter), 0, B, ptr(self.t_slots[slot]), ld, st)
+        if not ahead:
+            self._call("gather", "smb_gather_columns", F32, ptr(d.X), d.n_samples, d.features,
+                       ptr(self.perm), ptr(self.counter), 0, B, ptr(self.x_slots[slot]), ld, st)
+            self._call("gather_t", "smb_gather_columns", F32, ptr(d.T), d.n_samples, d.classes,
+                       ptr(self.perm), ptr(self.counter), 0, B, ptr(self.t_slots[slot]), ld, st)
+            return
+        kb = int(self.steps_per_epoch)
+        self._call("gather", "smb_gather_columns_ahead", F32, ptr(d.X), d.n_samples, d.features,
+                   ptr(self.perm), ptr(self.counter), 1, kb, B, ptr(self.x_slots[slot]), ld, st)
+        self._call("gather_t", "smb_gather_columns_ahead", F32, ptr(d.T), d.n_samples,
+                   d.classes, ptr(self.perm), ptr(self.counter), 1, kb, B,
+                   ptr(self.t_slots[slot]), ld, st)
+        self._call("counter", "smb_step_counter_advance", ptr(self.counter), kb, st)
 
     # ------------------------------------------------------------------
     def _bias_target(self, u, fuse_update: bool):
@@ -317,7 +330,11 @@ class FusedTrainStep:
             return s_
         main = torch.cuda.current_stream()
         # gather steps: this batch is already in x_in / t_in (prefetched by
-        # the previous step or by step()'s prologue)
+        # the previous step or by step()'s prologue); the next one is
+        # gathered into the other slot beside the (latency-bound) forward
+        if gather:
+            with torch.cuda.stream(fork("prefetch")):
+                self._gather_into(1 - self._slot, stream_ptr(), ahead=True)
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
         tail = self.fuse_tail
@@ -349,8 +366,7 @@ class FusedTrainStep:
                        ptr(self._vals(top)), ptr(self.acts[-2]), ld, 1 if below.relu else 0,
                        ptr(top.layer.bias), ptr(t_in), ld, B, float(self.B_global),
                        ptr(self.acts[-1]), ld, ptr(self.dys[-1]), ld, ptr(self.dys[-2]), ld,
-                       ptr(self.loss), ptr(self.counter) if gather else None,
-                       int(self.steps_per_epoch), ptr(self._tail_ws), st)
+                       ptr(self.loss), None, 0, ptr(self._tail_ws), st)
             # the bias sides of the top two layers cross columns: beside the
             # critical path when overlapping
             sides = ((top, self.dys[-1]), (below, self.dys[-2]))
@@ -366,22 +382,15 @@ class FusedTrainStep:
             self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
                        ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]),
                        ld, ptr(self.loss), None, None, None, _lib.SMB_OPT_NONE, 0.0, float(eta),
-                       ptr(self.counter) if gather else None, int(self.steps_per_epoch),
-                       ptr(self._ce_ws), st)
+                       None, 0, ptr(self._ce_ws), st)
             with torch.cuda.stream(fork(("weights", len(self.units) - 1))):
                 self._call(f"bias[{top.index}]", "smb_bias_grad_update", F32, ptr(self.dys[-1]),
                            ld, top.m, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
         else:
             self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
                        ptr(t_in), ld, self.classes, B, float(self.B_global), ptr(self.dys[-1]),
-                       ld, ptr(self.loss), b, vb, gb, kind, mu, float(eta),
-                       ptr(self.counter) if gather else None, int(self.steps_per_epoch),
+                       ld, ptr(self.loss), b, vb, gb, kind, mu, float(eta), None, 0,
                        ptr(self._ce_ws), st)
-        if gather:
-            # the counter now names the next batch: gather it into the other
-            # slot beside the backward chain
-            with torch.cuda.stream(fork("prefetch")):
-                self._gather_into(1 - self._slot, stream_ptr())
         # backward, last layer first: d_{l-1} (+ bias side of layer l-1) on the
         # main stream; the weight side of layer l (SDDMM + update) either
         # follows it in order, or -- single GPU -- runs on the side stream as
