@@ -212,6 +212,22 @@ SMB_API int smb_tail_step(int dtype, const smb_pattern* pattern, const void* val
                           void* d_y, int64_t ld_dy, void* d_h, int64_t ld_dh, double* loss_out,
                           int32_t* step_counter, int32_t modulo, void* workspace, void* stream);
 
+/* Output layer fused with the softmax-CE step, for m <= 12 output rows:
+ * y = W h + bias (SparseLinearLayer.forward, nn.py:169-176; row order and
+ * rounding of smb_spmm), d_y = (softmax(y) - t) / divisor and the summed loss
+ * (nn.py:397-417, train.py:399; arithmetic of smb_softmax_ce_grad).  W in CSR
+ * (row_ptr, col_idx, values), m x k.  y may be NULL.  The bias row sums of
+ * d_y are not computed (smb_bias_grad_update).  workspace:
+ * smb_logits_softmax_workspace_bytes(n) zero-initialised bytes (ticket +
+ * per-CTA loss partials). */
+SMB_API size_t smb_logits_softmax_workspace_bytes(int64_t n);
+SMB_API int smb_logits_softmax_step(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
+                                    const void* values, int64_t m, int64_t k, const void* h,
+                                    int64_t ld_h, const void* bias, const void* t, int64_t ld_t,
+                                    int64_t n, double divisor, void* y, int64_t ld_y, void* d_y,
+                                    int64_t ld_dy, double* loss_out, void* workspace,
+                                    void* stream);
+
 /* Masked-dense baseline update, DenseLinearLayer.optimize with a mask
  * (nn.py:258-264, gradient masked as in backward nn.py:255-256):
  * g' = grad*mask, velocity *= mask, _step_vector(param, g', velocity),

@@ -133,7 +133,7 @@ class _Unit:
 class FusedTrainStep:
     def __init__(self, model, batch_size: int, global_batch: int | None = None,
                  process_group=None, use_graph: bool = True, fuse_tail: bool | None = None,
-                 force_dp: bool = False):
+                 force_dp: bool = False, fuse_logits: bool = False):
         self.units = self._parse(model)
         self.model = model
         self.B = int(batch_size)
@@ -204,6 +204,16 @@ class FusedTrainStep:
         self.fuse_tail = bool(want and self.tail_ok)
         self._tail_ws = torch.zeros(int(_lib.load().smb_tail_step_workspace_bytes(self.B)),
                                     dtype=torch.uint8, device=dev) if self.tail_ok else None
+        # output layer fused with the softmax step (smb_logits_softmax_step:
+        # last layer sparse, no activation, <= 12 outputs, after >= 1 layer).
+        # Off by default: at config 2 it measured ~1 us/step slower than the
+        # separate deep kernel (320 one-warp CTAs) + softmax step -- the fused
+        # CTAs put all ten row chains of 32 columns on one SM.
+        self.logits_ok = bool(len(self.units) >= 2 and top.sparse and not top.relu
+                              and top.m <= 12)
+        self.fuse_logits = bool(fuse_logits and self.logits_ok)
+        self._ls_ws = torch.zeros(int(_lib.load().smb_logits_softmax_workspace_bytes(self.B)),
+                                  dtype=torch.uint8, device=dev) if self.logits_ok else None
         # single GPU: bias row sums of transposed-SpMM outputs on a side stream
         # instead of fused into the critical-path kernel's epilogue
         self.split_bias = True
@@ -338,10 +348,11 @@ class FusedTrainStep:
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
         tail = self.fuse_tail
+        logits = self.fuse_logits and not tail
         L = len(self.units)
         for li, (u, a) in enumerate(zip(self.units, self.acts)):
             lay = u.layer
-            if tail and li == L - 1:
+            if (tail or logits) and li == L - 1:
                 break
             if u.sparse:
                 self._call(f"spmm[{li}]", "smb_spmm", F32, ptr(lay.weights.row_ptr),
@@ -376,6 +387,18 @@ class FusedTrainStep:
                     bb, bv, bg, bk, bmu = self._bias_target(u, fuse_update)
                     self._call(f"bias[{u.index}]", "smb_bias_grad_update", F32, ptr(d_u), ld, u.m,
                                B, bb, bv, bg, bk, bmu, float(eta), sst)
+        elif logits:
+            # output layer + softmax-CE step in one launch; the bias row sums
+            # of d_y (they cross columns) beside the critical path
+            lw = top.layer.weights
+            self._call("logits_softmax", "smb_logits_softmax_step", F32, ptr(lw.row_ptr),
+                       ptr(lw.col_idx), ptr(lw.values), top.m, top.k, ptr(self.acts[-2]), ld,
+                       ptr(top.layer.bias), ptr(t_in), ld, B, float(self.B_global),
+                       ptr(self.acts[-1]), ld, ptr(self.dys[-1]), ld, ptr(self.loss),
+                       ptr(self._ls_ws), st)
+            with torch.cuda.stream(fork(("weights", L - 1))) if overlap else _nullctx():
+                self._call(f"bias[{top.index}]", "smb_bias_grad_update", F32, ptr(self.dys[-1]),
+                           ld, top.m, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
         elif overlap:
             # the column-parallel softmax step on the critical path; the last
             # layer's bias row sums + update (they cross columns) beside it

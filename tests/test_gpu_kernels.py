@@ -381,3 +381,38 @@ def test_few_long_rows_wide_batch_bit_exact(oracle, shape, density):
     want = oracle.spmm_t(rp2, ci2, tc.to_numpy(st.values), m, d)
     want = want * (mk > 0)
     assert bits_equal(smb.spmm_transposed(st, d, mask=dev(mk)), want)
+
+
+@pytest.mark.parametrize("m,k,n", [(10, 512, 1024), (12, 300, 37), (3, 100, 1), (10, 2000, 100)])
+def test_logits_softmax_step_equals_unfused(m, k, n):
+    """smb_logits_softmax_step == smb_spmm (+bias) -> smb_softmax_ce_grad
+    (/divisor), bit for bit; loss within fp64 summation-order noise."""
+    from paper_2407_17437_b200 import _lib
+
+    rng = np.random.default_rng(m * 1000 + n)
+    rp, ci, v, _ = random_csr(rng, m, k, 0.5, np.float32, empty_rows=True)
+    s = smb.CsrMatrix(m, k, rp, ci, v)
+    h = dev(np.maximum(rng.standard_normal((k, n)), 0).astype(np.float32))
+    bias = dev(rng.standard_normal(m).astype(np.float32))
+    t = np.zeros((m, n), np.float32)
+    t[rng.integers(0, m, n), np.arange(n)] = 1
+    t = dev(t)
+    divisor = float(n + 5)
+    y_ref = smb.spmm(s, h, bias=bias)
+    dy_ref, loss_ref = smb.nn._ce_call(y_ref, t, divisor)
+    y = torch.empty((m, n), device="cuda")
+    dy = torch.empty_like(y)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = torch.zeros(int(_lib.load().smb_logits_softmax_workspace_bytes(n)), dtype=torch.uint8,
+                     device="cuda")
+    _lib.call("smb_logits_softmax_step", _lib.SMB_F32, tc.ptr(s.row_ptr), tc.ptr(s.col_idx),
+              tc.ptr(s.values), m, k, tc.ptr(h), n, tc.ptr(bias), tc.ptr(t), n, n, divisor,
+              tc.ptr(y), n, tc.ptr(dy), n, tc.ptr(loss), tc.ptr(ws), tc.stream_ptr())
+    assert bits_equal(host(y), host(y_ref))
+    assert bits_equal(host(dy), host(dy_ref))
+    assert abs(float(loss) - float(loss_ref)) <= 1e-12 * max(1.0, abs(float(loss_ref)))
+    assert int(ws[:4].view(torch.int32)) == 0
+    with pytest.raises(smb.InvalidArgumentError):  # > 12 output rows
+        _lib.call("smb_logits_softmax_step", _lib.SMB_F32, tc.ptr(s.row_ptr), tc.ptr(s.col_idx),
+                  tc.ptr(s.values), 13, k, tc.ptr(h), n, None, tc.ptr(t), n, n, divisor, None, 0,
+                  tc.ptr(dy), n, tc.ptr(loss), tc.ptr(ws), tc.stream_ptr())
