@@ -252,6 +252,149 @@ __global__ void __launch_bounds__(TILE)
   }
 }
 
+// Warp-independent variant for many-wave layers: each warp owns 32
+// consecutive nonzeros of a 128-nonzero tile and stages, in its own
+// shared-memory ring, their x rows and the (<= kWarpDSlots) d_out rows they
+// span; it waits on its own cp.async groups + __syncwarp, so warps never
+// meet at a CTA barrier.  Warps whose 32 nonzeros span more rows read d_out
+// from global memory.  Same per-chain order / rounding as sddmm_pipe_kernel.
+constexpr int kWarpDSlots = 4;
+
+template <typename T, int CH, int S>
+struct SddmmWarpCfg {
+  static constexpr int VW = 16 / sizeof(T);
+  static constexpr int LDS = CH + VW;  // padded row (conflict-free 16-byte reads)
+  static constexpr int VPR = CH / VW;
+  static constexpr size_t warp_elems = size_t(S) * (32 + kWarpDSlots) * LDS;
+  static constexpr size_t smem_bytes = 4 * warp_elems * sizeof(T);  // 4 warps per CTA
+};
+
+template <typename T, int CH, int S>
+__global__ void __launch_bounds__(128)
+    sddmm_warp_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                      const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
+                      const T* __restrict__ d_out, int64_t ld_d, const T* __restrict__ x,
+                      int64_t ld_x, int64_t n, const T* values, T* values_out, T* velocity,
+                      T* grad_out, OptConsts<T> opt) {
+  using C = SddmmWarpCfg<T, CH, S>;
+  constexpr int VW = C::VW, LDS = C::LDS, VPR = C::VPR;
+  static_assert(kWarpDSlots * VPR <= 32, "one d_out copy per lane");
+  constexpr unsigned kStageBytes = (unsigned)((32 + kWarpDSlots) * LDS * sizeof(T));
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int32_t s_rp[kSddmmTile + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* wsm = reinterpret_cast<T*>(smem_raw) + warp * C::warp_elems;
+  const int64_t p0 = (int64_t)blockIdx.x * kSddmmTile;
+  const int64_t pw = p0 + warp * 32;             // first nonzero of this warp
+  const int nw = (int)imax(0, imin(32, nnz - pw));  // nonzeros of this warp
+  const int64_t p = pw + lane;
+  const bool active = lane < nw;
+  const int32_t r0 = tile_row0[blockIdx.x];
+  s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
+  if (tid == 0) s_rp[kSddmmTile] = (r0 + kSddmmTile <= m) ? row_ptr[r0 + kSddmmTile] : INT32_MAX;
+  const int32_t my_col = active ? col_idx[p] : 0;
+  __syncthreads();  // the only CTA-wide barrier (row window)
+  if (nw == 0) return;
+  const int64_t row = tile_row_of<kSddmmTile>(active ? p : pw, r0, s_rp, row_ptr, m);
+  const int64_t row_first = __shfl_sync(0xffffffffu, row, 0);
+  const int64_t row_last = __shfl_sync(0xffffffffu, row, nw - 1);
+  const int span = (int)(row_last - row_first + 1);
+  const bool staged = span <= kWarpDSlots;  // warp-uniform
+  const int slot = (int)(row - row_first);
+  const int n32 = (int)n;
+  const int n_chunks = (n32 + CH - 1) / CH;
+  // copy slots: x vectors e = lane + 32 k (k < VPR): row e / VPR, part e % VPR
+  const T* xsrc[VPR];
+  unsigned xdst[VPR];
+  int xok[VPR];
+#pragma unroll
+  for (int k = 0; k < VPR; ++k) {
+    const int e = lane + 32 * k, r = e / VPR, v = e % VPR;
+    const int32_t c = __shfl_sync(0xffffffffu, my_col, r);
+    xok[k] = r < nw ? 16 : 0;
+    xsrc[k] = x + (int64_t)c * ld_x + v * VW;
+    xdst[k] = (unsigned)((r * LDS + v * VW) * sizeof(T));
+  }
+  // d_out rows: vector e = lane (kWarpDSlots * VPR <= 32 for CH <= 32 fp32)
+  const bool dcopy = staged && lane < span * VPR;
+  const T* dsrc = d_out + (row_first + (dcopy ? lane / VPR : 0)) * ld_d + (lane % VPR) * VW;
+  const unsigned ddst = (unsigned)(((32 + lane / VPR) * LDS + (lane % VPR) * VW) * sizeof(T));
+  const unsigned sbase = smem_u32(wsm);
+  pdl_wait();  // d_out / x are earlier kernels' outputs
+  auto issue = [&](int ch) {
+    const unsigned st = sbase + (unsigned)(ch % S) * kStageBytes;
+    const int t0 = ch * CH;
+    if (t0 + CH <= n32) {
+#pragma unroll
+      for (int k = 0; k < VPR; ++k) cp_async16(st + xdst[k], xsrc[k] + t0, xok[k]);
+      if (dcopy) cp_async16(st + ddst, dsrc + t0, 16);
+      return;
+    }
+    const int valid = max(0, min(VW, n32 - (t0 + (lane % VPR) * VW)));
+#pragma unroll
+    for (int k = 0; k < VPR; ++k) {
+      const int vk = max(0, min(VW, n32 - (t0 + ((lane + 32 * k) % VPR) * VW)));
+      cp_async16(st + xdst[k], xsrc[k] + t0, xok[k] ? vk * (int)sizeof(T) : 0);
+    }
+    if (dcopy) cp_async16(st + ddst, dsrc + t0, valid * (int)sizeof(T));
+  };
+#pragma unroll
+  for (int c = 0; c < S - 1; ++c) {
+    if (c < n_chunks) issue(c);
+    cp_async_commit();
+  }
+  T acc = T(-0.0);
+  const T* drow = d_out + row * ld_d;
+  using V = typename Vec16<T>::type;
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    cp_async_wait<S - 2>();
+    __syncwarp();  // chunk ch landed for the whole warp; stage (ch-1) % S is free
+    if (ch + S - 1 < n_chunks) issue(ch + S - 1);
+    cp_async_commit();
+    if (active) {
+      const T* xs = wsm + (ch % S) * (kStageBytes / sizeof(T));
+      const T* xr = xs + lane * LDS;
+      const T* dr = xs + (32 + slot) * LDS;
+      const int t0 = ch * CH;
+      const int cnt = min(CH, n32 - t0);
+      if (cnt == CH) {
+#pragma unroll
+        for (int u = 0; u < VPR; ++u) {
+          const V xv = *reinterpret_cast<const V*>(xr + u * VW);
+          V dv;
+          if (staged) {
+            dv = *reinterpret_cast<const V*>(dr + u * VW);
+          } else {
+#pragma unroll
+            for (int j = 0; j < VW; ++j) VecOps<T>::set(dv, j, drow[t0 + u * VW + j]);
+          }
+#pragma unroll
+          for (int j = 0; j < VW; ++j)
+            acc = add_rn(acc, mul_rn(VecOps<T>::get(dv, j), VecOps<T>::get(xv, j)));
+        }
+      } else {
+        for (int j = 0; j < cnt; ++j) {
+          const T dv = staged ? dr[j] : drow[t0 + j];
+          acc = add_rn(acc, mul_rn(dv, xr[j]));
+        }
+      }
+    }
+    __syncwarp();  // every lane done reading this stage before it is refilled
+  }
+  cp_async_wait<0>();
+  pdl_trigger();
+  if (!active) return;
+  const T g = (n == 0) ? T(0) : acc;  // tensor_core.py:283-284: zero batch -> zeros
+  if (grad_out) grad_out[p] = g;
+  if (opt.kind != SMB_OPT_NONE) {
+    T w = values[p];
+    T v = velocity ? velocity[p] : T(0);
+    apply_update(opt, g, &w, &v);
+    values_out[p] = w;
+    if (velocity) velocity[p] = v;
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -283,7 +426,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       return (tile == 128 ? pat->span128 : pat->span512) <= tile / sd;
     };
     // tuning experiments only (scripts/gpu_sddmm_var2.sh): 1 = 512-nonzero
-    // tiles x 32 columns, 2 = 128 x 16 x 8 stages
+    // tiles x 32 columns, 2 = 128 x 16 x 8 stages, 3 = warp-independent
     static const int variant = [] {
       const char* e = getenv("SMB_SDDMM_VARIANT");
       return e ? atoi(e) : 0;
@@ -308,7 +451,20 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     // (1-2 nonzeros per row) stage one d_out row per nonzero (SD = 1).
     const bool wave = pat->ntiles <= 2 * 148;
     const bool sparse_rows = !all_for(128, 4);
-    if (sizeof(T) == 4 && variant == 1) SMB_GO_SD(512, 32, 2, 4);
+    // many waves and every 128-tile within kWarpDSlots rows (>= ~10 nonzeros
+    // per row): warp-independent staging, no CTA barrier (1.1-1.2x at
+    // config 3 d >= 0.01; measured slower when rows are short)
+    const bool warp_kernel = sizeof(T) == 4 && vec && variant == 0 && !wave &&
+                             pat->span128 <= kWarpDSlots;
+    bool warp_done = false;
+    if constexpr (sizeof(T) == 4) {
+      if (warp_kernel || (vec && variant == 3)) {
+        go(sddmm_warp_kernel<T, 32, 2>, 128, SddmmWarpCfg<T, 32, 2>::smem_bytes);
+        warp_done = true;
+      }
+    }
+    if (warp_done) {
+    } else if (sizeof(T) == 4 && variant == 1) SMB_GO_SD(512, 32, 2, 4);
     else if (sizeof(T) == 4 && variant == 2) SMB_GO_SD(128, 16, 8, 4);
     else if (sizeof(T) == 4 && wave && sparse_rows) SMB_GO_SD(128, 64, 2, 1);
     else if (sizeof(T) == 4 && wave) SMB_GO_SD(128, 64, 2, 4);

@@ -416,3 +416,21 @@ def test_logits_softmax_step_equals_unfused(m, k, n):
         _lib.call("smb_logits_softmax_step", _lib.SMB_F32, tc.ptr(s.row_ptr), tc.ptr(s.col_idx),
                   tc.ptr(s.values), 13, k, tc.ptr(h), n, None, tc.ptr(t), n, n, divisor, None, 0,
                   tc.ptr(dy), n, tc.ptr(loss), tc.ptr(ws), tc.stream_ptr())
+
+
+@pytest.mark.parametrize("n", [1024, 100, 37])
+def test_sddmm_many_waves_long_rows_bit_exact(oracle, n):
+    """> 296 tiles of 128 nonzeros whose rows hold >= ~60 nonzeros: the
+    warp-independent SDDMM (per-warp staging, no CTA barrier); partial last
+    chunks for n = 100 / 37."""
+    m, k = 1000, 4000
+    rng = np.random.default_rng(n + 11)
+    counts = rng.integers(60, 100, size=m)
+    rp = np.zeros(m + 1, dtype=np.int32)
+    np.cumsum(counts, out=rp[1:])
+    ci = np.concatenate([np.sort(rng.choice(k, size=c, replace=False)) for c in counts]).astype(np.int32)
+    assert rp[-1] > 296 * 128
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float32)
+    got = host(smb.sddmm(smb.SparsityPattern(m, k, rp, ci), dev(a), dev(b)).values)
+    assert bits_equal(got, oracle.sddmm(rp, ci, a, b))
