@@ -1,5 +1,5 @@
 #!/bin/bash
-for v in 0 3 4 5; do
+for v in 3 4 5; do
   echo "variant $v"
   SMB_SDDMM_VARIANT=$v timeout 120 python scripts/probe_sddmm.py
   SMB_SDDMM_VARIANT=$v timeout 300 python -c "

@@ -89,9 +89,9 @@ def full(args):
         return v * {"ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(u, 1)
 
     tags = args.tags.split(",") if args.tags else [str(i) for i in range(len(data))]
-    lines = ["| tag | kernel | grid×block | µs | DRAM rd+wr MB | DRAM % | L1 % | "
+    lines = ["| tag | kernel | grid×block | µs | DRAM rd+wr MB | DRAM % | L2→L1 MB | L2 % | L1 % | "
              "inst % (active) | warps/SM | regs | top stalls (per issue) |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = {}
     for tag, r in zip(tags, data):
         rd = nbytes(r, "dram__bytes_read.sum")
@@ -105,6 +105,8 @@ def full(args):
         lines.append(
             f"| {tag} | `{short(r[4])}` | {r[8]}×{r[7]} | {usec(r):.2f} | "
             f"{(rd + wr) / 1e6:.2f} | {g(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
+            f"{nbytes(r, 'l1tex__m_xbar2l1tex_read_bytes.sum') / 1e6:.1f} | "
+            f"{g(r, 'lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
             f"{g(r, 'l1tex__throughput.avg.pct_of_peak_sustained_active'):.1f} | "
             f"{g(r, 'sm__instruction_throughput.avg.pct_of_peak_sustained_active'):.1f} | "
             f"{g(r, 'sm__warps_active.avg.per_cycle_active'):.1f} | "
