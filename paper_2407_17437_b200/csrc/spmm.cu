@@ -383,6 +383,100 @@ __device__ __forceinline__ T deep_row_chain(const int32_t* __restrict__ seg_ptr,
   return acc;
 }
 
+// Few long rows, one column per lane, "parallel products + serial sum": CTA
+// = one row x 32 batch columns, 8 warps.  The row is walked in segments of
+// kPpSeg nonzeros: all warps compute the segment's products
+// val(s) * x[idx(s), col] (each rounded on its own) into one of two
+// shared-memory buffers while warp 0 adds the previous segment's products in
+// ascending s -- the same separately rounded multiply-then-add sequence, but
+// the serial chain no longer waits on index -> operand loads.
+constexpr int kPpWarps = 8;
+template <typename T>
+__host__ __device__ constexpr int pp_seg() { return sizeof(T) == 4 ? 128 : 64; }  // 32 KB x2
+
+template <typename T, int EPI, bool PERM>
+__global__ void __launch_bounds__(32 * kPpWarps)
+    row_spmm_pp_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
+                       const int32_t* __restrict__ perm, const T* __restrict__ vals,
+                       const T* __restrict__ dense, int64_t ld_dense, int64_t n,
+                       T* __restrict__ out, int64_t ld_out, EpiArgs<T> epi) {
+  constexpr int kPpSeg = pp_seg<T>();
+  __shared__ T s_p[2][kPpSeg][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x;
+  const int64_t col = (int64_t)blockIdx.y * 32 + lane;
+  const bool valid = col < n;
+  const T* dcol = dense + (valid ? col : 0);
+  const uint32_t ldu = (uint32_t)ld_dense;
+  const int32_t s_begin = seg_ptr[row], s_end = seg_ptr[row + 1];
+  const int len = s_end - s_begin;
+  const int nseg = (len + kPpSeg - 1) / kPpSeg;
+  T bias_r = T(0), mk = T(0);
+  if constexpr (EPI == kEpiBiasAct) {
+    if (epi.bias != nullptr) bias_r = epi.bias[row];
+  } else {
+    if (epi.mask != nullptr && valid) mk = epi.mask[row * epi.ld_mask + col];
+  }
+  // products of segment sg: warp w takes positions w*16 .. w*16+15 (kPpSeg =
+  // 8 warps x 16); lane q < 16 holds (idx, val) of position q, broadcast by
+  // shuffles
+  constexpr int PW = kPpSeg / kPpWarps;
+  auto load_iv = [&](int sg, int& gi, T& gv) {
+    const int q = lane % PW;
+    const int32_t s = s_begin + sg * kPpSeg + warp * PW + q;
+    gi = 0;
+    gv = T(0);
+    if (s < s_end) {
+      gi = idx[s];
+      gv = PERM ? vals[perm[s]] : vals[s];
+    }
+  };
+  auto products = [&](int sg, int gi, T gv) {
+    T (*buf)[32] = s_p[sg & 1];
+    T xv[PW];
+#pragma unroll
+    for (int q = 0; q < PW; ++q)
+      xv[q] = ldg_stream(dcol + (size_t)(uint32_t)__shfl_sync(0xffffffffu, gi, q) * ldu);
+#pragma unroll
+    for (int q = 0; q < PW; ++q) buf[warp * PW + q][lane] = mul_rn(__shfl_sync(0xffffffffu, gv, q), xv[q]);
+  };
+  int gi;
+  T gv;
+  load_iv(0, gi, gv);
+  pdl_wait();  // the dense operand is the previous kernel's output
+  if (nseg > 0) products(0, gi, gv);
+  if (nseg > 1) load_iv(1, gi, gv);
+  __syncthreads();
+  T acc = T(0);
+  for (int sg = 0; sg < nseg; ++sg) {
+    // warps 1..7 (and warp 0 first) produce segment sg + 1 while warp 0 sums sg
+    if (sg + 1 < nseg) {
+      products(sg + 1, gi, gv);
+      if (sg + 2 < nseg) load_iv(sg + 2, gi, gv);
+    }
+    if (warp == 0) {
+      const T (*buf)[32] = s_p[sg & 1];
+      const int cnt = min(kPpSeg, len - sg * kPpSeg);
+      if (cnt == kPpSeg) {
+#pragma unroll 16
+        for (int q = 0; q < kPpSeg; ++q) acc = add_rn(acc, buf[q][lane]);
+      } else {
+        for (int q = 0; q < cnt; ++q) acc = add_rn(acc, buf[q][lane]);
+      }
+    }
+    __syncthreads();  // segment sg consumed, sg + 1 produced
+  }
+  pdl_trigger();
+  if (warp != 0 || !valid) return;
+  if constexpr (EPI == kEpiBiasAct) {
+    if (epi.bias != nullptr) acc = add_rn(acc, bias_r);
+    if (epi.relu) acc = relu_np(acc);
+  } else {
+    if (epi.mask != nullptr) acc = mask_np(acc, mk);
+  }
+  out[row * ld_out + col] = acc;
+}
+
 template <typename T, int EPI, bool PERM>
 __global__ void __launch_bounds__(32)
     row_spmm_deep_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
@@ -564,7 +658,13 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   else if (n_rows >= 148)
     done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                            out, ld_out, epi, st);
-  else if (!(EPI == kEpiMask && epi.rowsum) && force_w != 13) {
+  else if (!(EPI == kEpiMask && epi.rowsum) && (n < 512 || force_w == 14) && force_w != 13) {
+    // few long rows, narrow batch: parallel products + serial sum
+    launch_k(row_spmm_pp_kernel<T, EPI, PERM>, dim3((unsigned)n_rows, (unsigned)ceil_div(n, 32)),
+             dim3(32 * kPpWarps), 0, st, seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out,
+             epi);
+    done = false;
+  } else if (!(EPI == kEpiMask && epi.rowsum) && force_w != 13) {
     launch_k(row_spmm_deep_kernel<T, EPI, PERM>, dim3((unsigned)n_rows, (unsigned)ceil_div(n, 32)),
              dim3(32), 0, st, seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out, epi);
     done = false;

@@ -4,8 +4,9 @@ skipped step computes are meaningless)."""
 import sys; sys.path.insert(0, '.')
 import numpy as np, torch, paper_2407_17437_b200 as smb
 from paper_2407_17437_b200 import engine
-B = 1024
-data = smb.synthetic_dataset(seed=0, n_samples=16384, features=3072)
+import os
+B = int(os.environ.get("ABL_B", "1024"))
+data = smb.synthetic_dataset(seed=0, n_samples=16384 if B >= 1024 else 4096, features=3072)
 ddata = smb.DeviceDataset(data)
 orig = engine.FusedTrainStep._call
 
@@ -20,7 +21,7 @@ def time_with(skip):
                                                         density=0.01, batch_size=B, lr=0.01))
         st = smb.FusedTrainStep(model, B)
         st.attach_dataset(ddata)
-        st.set_epoch(np.arange(16384))
+        st.set_epoch(np.arange(data.Xtrain.shape[1]))
         for _ in range(6): st.step(0.01)
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

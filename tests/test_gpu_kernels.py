@@ -360,11 +360,14 @@ def test_spmv_single_column_strided_with_epilogue(oracle, relu):
 
 
 @pytest.mark.parametrize("shape,density", [((10, 512, 1024), 0.6), ((7, 300, 777), 0.9),
-                                           ((20, 2000, 600), 0.3), ((3, 50, 515), 0.05)])
+                                           ((20, 2000, 600), 0.3), ((3, 50, 515), 0.05),
+                                           ((10, 512, 100), 0.6), ((5, 1000, 37), 0.4),
+                                           ((12, 64, 300), 0.9)])
 def test_few_long_rows_wide_batch_bit_exact(oracle, shape, density):
-    """Few output rows x wide batch (the output layer at B >= 512): the
-    three-group register-pipelined kernel, forward with bias + ReLU and
-    transposed with mask, bit-exact."""
+    """Few output rows (the output layer): the three-group register-pipelined
+    kernel (batch >= 512) and the parallel-products kernel (narrower
+    batches, rows of several 128-nonzero segments), forward with bias + ReLU
+    and transposed with mask, bit-exact."""
     m, k, n = shape
     rng = np.random.default_rng(m * 7 + n)
     rp, ci, v, _ = random_csr(rng, m, k, density, np.float32, empty_rows=True)
