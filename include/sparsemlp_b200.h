@@ -112,6 +112,14 @@ SMB_API int smb_pattern_destroy(smb_pattern* pattern);
 SMB_API int smb_pattern_csc(const smb_pattern* pattern, int32_t* col_ptr, int32_t* row_idx,
                             int32_t* perm, void* stream);
 
+/* smb_spmm through a pattern handle: the same product, order and epilogue
+ * (tensor_core.spmm, tensor_core.py:227-240; nn.py:169-176, 86-87); the
+ * handle's nonzero count selects the lane width (short rows: 2 x 16 bytes
+ * per lane, long rows: 16 bytes). */
+SMB_API int smb_spmm_p(int dtype, const smb_pattern* pattern, const void* values,
+                       const void* dense, int64_t ld_dense, int64_t n, const void* bias,
+                       int epilogue, void* out, int64_t ld_out, void* stream);
+
 /* out[c,:] = sum_{i ascending} values[perm[q]] * dense[i,:] over the column-c
  * slots q of the CSC index, then out *= (mask[c,:] > 0) when mask != NULL.
  * Replaces _kernels.spmm_t_kernel (_kernels.py:40-59) via

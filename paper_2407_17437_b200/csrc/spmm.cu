@@ -607,7 +607,7 @@ template <typename T, int EPI, bool PERM>
 int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm,
                         const T* vals, int64_t n_rows, const T* dense, int64_t ld_dense,
                         int64_t n, T* out, int64_t ld_out, EpiArgs<T> epi, cudaStream_t st,
-                        const char* name, bool* rowsum_done) {
+                        const char* name, bool* rowsum_done, double avg_len = -1.0) {
   if (rowsum_done) *rowsum_done = false;
   if (n_rows == 0 || n == 0) return SMB_OK;
   if (n == 1 && !epi.rowsum) {  // one batch column: warp-per-row SpMV
@@ -646,6 +646,14 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   else if (force_w == 12)
     done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                             out, ld_out, epi, st);
+  else if ((force_w == 9 || (force_w == 0 && avg_len >= 0 && avg_len <= 32)) && vec_ok &&
+           enough(2 * VW))
+    // short segments (<= 32 nonzeros on average; known when the pattern is):
+    // two vectors per lane with a 2-deep ring halve the warps per row and
+    // the per-column index / shuffle work (config 2: 1.2-1.3x); long
+    // segments keep one vector and a 4-deep ring (1.2-1.5x better there)
+    done = launch_rows<T, 2 * VW, 2, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
+                                                n, out, ld_out, epi, st);
   else if (force_w == 7 && vec_ok)
     done = launch_rows<T, VW, 2, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
                                              out, ld_out, epi, st);
@@ -706,7 +714,7 @@ int spmm_t_fused_impl(const smb_pattern* pat, const void* values, const void* de
   int rc = launch_segment_spmm<T, kEpiMask, true>(
       pat->col_ptr, pat->row_idx, pat->perm, static_cast<const T*>(values), pat->k,
       static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi, st,
-      "smb_spmm_t", &done);
+      "smb_spmm_t", &done, pat->k > 0 ? (double)pat->nnz / (double)pat->k : -1.0);
   if (rc != SMB_OK || !want_rows || done) return rc;
   return launch_bias_rows<T>(static_cast<const T*>(out), ld_out, pat->k, n, epi.rb_bias,
                              epi.rb_vbias, epi.rb_grad, epi.opt, st);
@@ -720,13 +728,14 @@ namespace {
 template <typename T>
 int spmm_impl(const int32_t* row_ptr, const int32_t* col_idx, const void* values, int64_t m,
               const void* dense, int64_t ld_dense, int64_t n, const void* bias, int epilogue,
-              void* out, int64_t ld_out, void* stream) {
+              void* out, int64_t ld_out, void* stream, double avg_len = -1.0) {
   EpiArgs<T> epi{};
   epi.bias = static_cast<const T*>(bias);
   epi.relu = epilogue == SMB_EPI_RELU;
   return launch_segment_spmm<T, kEpiBiasAct, false>(
       row_ptr, col_idx, nullptr, static_cast<const T*>(values), m, static_cast<const T*>(dense),
-      ld_dense, n, static_cast<T*>(out), ld_out, epi, as_stream(stream), "smb_spmm", nullptr);
+      ld_dense, n, static_cast<T*>(out), ld_out, epi, as_stream(stream), "smb_spmm", nullptr,
+      avg_len);
 }
 
 int spmm_t_checks(const smb_pattern* pat, int64_t ld_dense, int64_t n, const void* mask,
@@ -760,6 +769,27 @@ extern "C" int smb_spmm(int dtype, const int32_t* row_ptr, const int32_t* col_id
     return spmm_impl<double>(row_ptr, col_idx, values, m, dense, ld_dense, n, bias, epilogue,
                              out, ld_out, stream);
   set_error("smb_spmm: unsupported dtype %d", dtype);
+  return SMB_ERR_INVALID;
+}
+
+extern "C" int smb_spmm_p(int dtype, const smb_pattern* pat, const void* values,
+                          const void* dense, int64_t ld_dense, int64_t n, const void* bias,
+                          int epilogue, void* out, int64_t ld_out, void* stream) {
+  clear_error();
+  SMB_REQUIRE(pat != nullptr, "smb_spmm_p: null pattern");
+  SMB_REQUIRE(n >= 0, "smb_spmm_p: negative dimension");
+  SMB_REQUIRE(ld_dense >= n && ld_out >= n, "smb_spmm_p: leading dimension smaller than n");
+  SMB_REQUIRE(epilogue == SMB_EPI_NONE || epilogue == SMB_EPI_RELU, "smb_spmm_p: bad epilogue %d",
+              epilogue);
+  SMB_REQUIRE(pat->m == 0 || out != nullptr, "smb_spmm_p: null output");
+  const double avg = pat->m > 0 ? (double)pat->nnz / (double)pat->m : -1.0;
+  if (dtype == SMB_F32)
+    return spmm_impl<float>(pat->row_ptr, pat->col_idx, values, pat->m, dense, ld_dense, n, bias,
+                            epilogue, out, ld_out, stream, avg);
+  if (dtype == SMB_F64)
+    return spmm_impl<double>(pat->row_ptr, pat->col_idx, values, pat->m, dense, ld_dense, n,
+                             bias, epilogue, out, ld_out, stream, avg);
+  set_error("smb_spmm_p: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
 }
 

@@ -355,10 +355,9 @@ class FusedTrainStep:
             if (tail or logits) and li == L - 1:
                 break
             if u.sparse:
-                self._call(f"spmm[{li}]", "smb_spmm", F32, ptr(lay.weights.row_ptr),
-                           ptr(lay.weights.col_idx), ptr(lay.weights.values), u.m, u.k, ptr(x), ld,
-                           B, ptr(lay.bias), _lib.SMB_EPI_RELU if u.relu else _lib.SMB_EPI_NONE,
-                           ptr(a), ld, st)
+                self._call(f"spmm[{li}]", "smb_spmm_p", F32, lay.weights.pattern.handle,
+                           ptr(lay.weights.values), ptr(x), ld, B, ptr(lay.bias),
+                           _lib.SMB_EPI_RELU if u.relu else _lib.SMB_EPI_NONE, ptr(a), ld, st)
             else:
                 with _no_tf32():
                     torch.addmm(lay.bias[:, None], lay.weights, x[:, :B], out=a[:, :B])

@@ -364,9 +364,9 @@ def spmm(s: CsrMatrix, dense, bias=None, relu: bool = False):
     out = torch.empty((s.nrows, n), dtype=s.values.dtype, device=d.device)
     if s.nrows and n:
         _lib.call(
-            "smb_spmm", dtype_code(s.dtype), ptr(s.row_ptr), ptr(s.col_idx), ptr(s.values),
-            s.nrows, s.ncols, ptr(d), _ld(d), n, ptr(b),
-            _lib.SMB_EPI_RELU if relu else _lib.SMB_EPI_NONE, ptr(out), _ld(out), stream_ptr(),
+            "smb_spmm_p", dtype_code(s.dtype), s.pattern.handle, ptr(s.values), ptr(d), _ld(d),
+            n, ptr(b), _lib.SMB_EPI_RELU if relu else _lib.SMB_EPI_NONE, ptr(out), _ld(out),
+            stream_ptr(),
         )
     return _ret(out, host)
 

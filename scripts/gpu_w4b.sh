@@ -1,6 +1,6 @@
 #!/bin/bash
 
-for w in 0 9; do
+for w in 9; do
   echo "W=$w"
   SMB_SPMM_W=$w timeout 120 python scripts/probe_spmm_small.py
   SMB_SPMM_W=$w timeout 300 python -c "

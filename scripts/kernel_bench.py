@@ -47,8 +47,8 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
             def launch(kind):
                 st = stream_ptr()
                 if kind == "spmm":
-                    _lib.call("smb_spmm", 0, ptr(pat.row_ptr), ptr(pat.col_idx), ptr(vals), n, n,
-                              ptr(X), B, B, None, 0, ptr(out), B, st)
+                    _lib.call("smb_spmm_p", 0, pat.handle, ptr(vals), ptr(X), B, B, None, 0,
+                              ptr(out), B, st)
                 elif kind == "spmm_t":
                     _lib.call("smb_spmm_t", 0, pat.handle, ptr(vals), ptr(dY), B, B, None, 0,
                               ptr(out), B, st)

@@ -19,7 +19,7 @@ def time_with(skip):
     try:
         model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=[3072, 1024, 512, 10],
                                                         density=0.01, batch_size=B, lr=0.01))
-        st = smb.FusedTrainStep(model, B)
+        st = smb.FusedTrainStep(model, B, fuse_logits=os.environ.get("ABL_FUSE_LOGITS") == "1")
         st.attach_dataset(ddata)
         st.set_epoch(np.arange(data.Xtrain.shape[1]))
         for _ in range(6): st.step(0.01)
