@@ -59,6 +59,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", default="sparse", choices=["sparse", "masked"],
                     help="masked = the masked-dense baseline (MaskedDense, cuBLAS FP32)")
+    ap.add_argument("--force-dp", action="store_true",
+                    help="one process: run the data-parallel step structure (flat gradient "
+                         "buffer, NCCL all-reduce over a world of 1, update pass)")
     ap.add_argument("--sweep", action="store_true",
                     help="also report the config-2 density sweep (B=100 and 1024)")
     return ap.parse_args()
@@ -183,7 +186,8 @@ def config_dict(args, ws):
                         + ("" if args.backend == "sparse" else f" backend={args.backend}"),
             "layers": [int(x) for x in args.layers.split(",")], "density": args.density,
             "batch_per_gpu": args.batch, "global_batch": args.batch * ws,
-            "train_samples": args.samples, "parallelism": f"dp{ws}",
+            "train_samples": args.samples,
+            "parallelism": f"dp{ws}" + (" (data-parallel step structure, forced)" if args.force_dp else ""),
             "l2": "flushed (512 MB write) before every timed step; dataset 614 MB > L2"}
 
 
@@ -258,9 +262,13 @@ def run_ours(args):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     pg = None
-    if ws > 1:
+    if ws > 1 or args.force_dp:
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(ws))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist.group.WORLD
     import paper_2407_17437_b200 as smb
@@ -275,7 +283,8 @@ def run_ours(args):
     data = smb.synthetic_dataset(seed=args.seed, n_samples=args.samples, features=chain[0],
                                  classes=chain[-1])
     ddata = smb.DeviceDataset(data)
-    step = smb.FusedTrainStep(model, B, global_batch=gb, process_group=pg)
+    step = smb.FusedTrainStep(model, B, global_batch=gb, process_group=pg,
+                              force_dp=args.force_dp)
     step.attach_dataset(ddata)
     perm = np.random.default_rng(args.seed).permutation(args.samples)
     step.set_epoch(perm, rank_offset=rank * B)

@@ -236,6 +236,16 @@ SMB_API int smb_logits_softmax_step(int dtype, const int32_t* row_ptr, const int
                                     int64_t ld_dy, double* loss_out, void* workspace,
                                     void* stream);
 
+/* The data-parallel update pass in one launch: `segments` is a DEVICE array of
+ * n_segments (<= 32) records {void* param; void* velocity; const void* grad;
+ * const void* mask; int64_t start;} -- element e of the concatenation
+ * (start[i] <= e < start[i+1], the last segment ends at `total`) is updated
+ * exactly like smb_optimizer_step (mask == NULL) or
+ * smb_masked_optimizer_step (nn.py:118-131, 187-198, 255-263). */
+SMB_API int smb_optimizer_step_multi(int dtype, const void* segments, int n_segments,
+                                     int64_t total, int opt_kind, double mu, double eta,
+                                     void* stream);
+
 /* Masked-dense baseline update, DenseLinearLayer.optimize with a mask
  * (nn.py:258-264, gradient masked as in backward nn.py:255-256):
  * g' = grad*mask, velocity *= mask, _step_vector(param, g', velocity),

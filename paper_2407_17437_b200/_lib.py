@@ -76,6 +76,7 @@ SIGNATURES = {
         [_i32, _p, _p, _p, _i64, _i64, _p, _i64, _p, _p, _i64, _i64, _f64, _p, _i64, _p, _i64,
          _p, _p, _p],
     ),
+    "smb_optimizer_step_multi": (_i32, [_i32, _p, _i32, _i64, _i32, _f64, _f64, _p]),
     "smb_masked_optimizer_step": (_i32, [_i32, _p, _p, _p, _p, _i64, _i32, _f64, _f64, _p]),
     "smb_row_sums": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p]),
     "smb_softmax_ce_grad": (

@@ -78,6 +78,46 @@ __global__ void masked_optimizer_kernel(T* __restrict__ w, T* __restrict__ v,
   }
 }
 
+// ---- several (param, velocity, grad, mask) segments in one launch: the
+// data-parallel update pass after the gradient all-reduce.  Segment i covers
+// elements [start[i], start[i+1]) of the concatenation (up to 32 segments).
+// Same arithmetic as optimizer_kernel / masked_optimizer_kernel per element.
+struct OptSegment {
+  void* param;
+  void* velocity;      // may be null (GD)
+  const void* grad;
+  const void* mask;    // may be null (no mask)
+  int64_t start;       // first element in the concatenation
+};
+
+template <typename T>
+__global__ void multi_optimizer_kernel(const OptSegment* __restrict__ segs, int nseg, int64_t total,
+                                       OptConsts<T> o) {
+  __shared__ OptSegment s_seg[32];
+  __shared__ int64_t s_end[32];
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    s_seg[i] = segs[i];
+    s_end[i] = (i + 1 < nseg) ? segs[i + 1].start : total;
+  }
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int si = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    while (e >= s_end[si]) ++si;  // segments ascend with e
+    const OptSegment& sg = s_seg[si];
+    const int64_t j = e - sg.start;
+    T* w = static_cast<T*>(sg.param) + j;
+    T* v = sg.velocity ? static_cast<T*>(sg.velocity) + j : nullptr;
+    const T g = static_cast<const T*>(sg.grad)[j];
+    if (sg.mask) {
+      masked_update_one(o, w, v, g, static_cast<const T*>(sg.mask)[j]);
+    } else {
+      T dummy = T(0);
+      apply_update(o, g, w, v ? v : &dummy);
+    }
+  }
+}
+
 // ---- warp per row: pairwise row sum (tensor_core.py:353-356) and the bias
 // optimizer update (_step_vector, nn.py:118-131) --------------------------
 constexpr int kRowWarps = 8;
@@ -431,6 +471,25 @@ extern "C" int smb_masked_optimizer_step(int dtype, void* param, void* velocity,
           static_cast<T*>(param), static_cast<T*>(velocity), static_cast<const T*>(grad),
           static_cast<const T*>(mask), count, o);
     return check_launch("smb_masked_optimizer_step");
+  });
+}
+
+extern "C" int smb_optimizer_step_multi(int dtype, const void* segments, int n_segments,
+                                        int64_t total, int opt_kind, double mu, double eta,
+                                        void* stream) {
+  clear_error();
+  SMB_REQUIRE(n_segments >= 0 && n_segments <= 32, "smb_optimizer_step_multi: 0..32 segments");
+  SMB_REQUIRE(total >= 0, "smb_optimizer_step_multi: negative total");
+  SMB_REQUIRE(opt_kind >= SMB_OPT_NONE && opt_kind <= SMB_OPT_NESTEROV,
+              "smb_optimizer_step_multi: bad optimizer kind %d", opt_kind);
+  if (total == 0 || n_segments == 0 || opt_kind == SMB_OPT_NONE) return SMB_OK;
+  SMB_REQUIRE(segments != nullptr, "smb_optimizer_step_multi: null segment table");
+  return dispatch_dtype(dtype, "smb_optimizer_step_multi", [&](auto tag) {
+    using T = decltype(tag);
+    multi_optimizer_kernel<T><<<grid_1d(total, 256), 256, 0, as_stream(stream)>>>(
+        static_cast<const OptSegment*>(segments), n_segments, total,
+        make_opt<T>(opt_kind, mu, eta));
+    return check_launch("smb_optimizer_step_multi");
   });
 }
 

@@ -217,6 +217,7 @@ class FusedTrainStep:
         # single GPU: bias row sums of transposed-SpMM outputs on a side stream
         # instead of fused into the critical-path kernel's epilogue
         self.split_bias = True
+        self._segs = None  # data-parallel update segment table (built on first use)
         self._graphs = {}
         self._cap_stream = None
         self.timer = None  # optional KernelTimer: per-launch CUDA events (eager only)
@@ -511,8 +512,45 @@ class FusedTrainStep:
                            ptr(vel), ptr(gw), u.nvals, optimizer_kind(opt), float(opt.mu),
                            float(eta), st)
 
+    def _segment_table(self):
+        """Device table for smb_optimizer_step_multi: one record per
+        parameter (values or dense weights, then bias) in flat-buffer order,
+        or None when the layers' optimizers differ."""
+        if self._segs is not None:
+            return self._segs if self._segs is not False else None
+        opts = {(optimizer_kind(u.layer.optimizer), float(u.layer.optimizer.mu)) for u in self.units}
+        if len(opts) != 1 or 2 * len(self.units) > 32:
+            self._segs = False
+            return None
+        rec = np.zeros((2 * len(self.units), 5), dtype=np.int64)
+        fp = self.flat.data_ptr()
+        for i, u in enumerate(self.units):
+            lay = u.layer
+            if u.sparse:
+                w = lay.weights.values
+                vel = lay.velocity.values if lay.velocity is not None else None
+                mk = None
+            else:
+                w = lay.weights
+                vel = lay.velocity
+                mk = lay.mask
+            rec[2 * i] = [w.data_ptr(), vel.data_ptr() if vel is not None else 0,
+                          fp + 4 * u.grad_off, mk.data_ptr() if mk is not None else 0, u.grad_off]
+            vb = lay.velocity_bias
+            rec[2 * i + 1] = [lay.bias.data_ptr(), vb.data_ptr() if vb is not None else 0,
+                              fp + 4 * u.bias_off, 0, u.bias_off]
+        self._segs = torch.from_numpy(rec.view(np.uint8).reshape(-1)).to(self.dev)
+        self._seg_kind = opts.pop()
+        return self._segs
+
     def _launch_updates_from_flat(self, eta: float) -> None:
         st = stream_ptr()
+        segs = self._segment_table()
+        if segs is not None:
+            kind, mu = self._seg_kind
+            self._call("update", "smb_optimizer_step_multi", _lib.SMB_F32, ptr(segs),
+                       2 * len(self.units), self.flat.numel(), kind, mu, float(eta), st)
+            return
         for u in self.units:
             lay = u.layer
             opt = lay.optimizer
@@ -566,7 +604,7 @@ class FusedTrainStep:
             self._flip_parity()
         else:
             self._replay_or_run(eta, gather, "fb")
-            if self.world > 1:
+            if self.pg is not None:  # (a world of 1 is the identity)
                 import torch.distributed as dist
 
                 dist.all_reduce(self.flat, group=self.pg)
