@@ -108,11 +108,11 @@ __global__ void rank_sort_columns_kernel(const int32_t* col_ptr, int64_t k, cons
   }
 }
 
-__global__ void tile_rows_kernel(const int32_t* row_ptr, int64_t m, int64_t ntiles,
+__global__ void tile_rows_kernel(const int32_t* row_ptr, int64_t m, int64_t ngrains,
                                  int32_t* tile_row0) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ntiles) return;
-  const int64_t p = t * kSddmmTile;
+  if (t >= ngrains) return;
+  const int64_t p = t * kTileGrain;
   // last row i with row_ptr[i] <= p (skips empty rows)
   int64_t lo = 0, hi = m;  // invariant: row_ptr[lo] <= p < row_ptr[hi] (row_ptr[m] = nnz > p)
   while (hi - lo > 1) {
@@ -162,6 +162,7 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
   p->row_ptr = row_ptr;
   p->col_idx = col_idx;
   p->ntiles = ceil_div(nnz, kSddmmTile);
+  p->ngrains = ceil_div(nnz, kTileGrain);
 
   auto fail_cuda = [&](const char* what) {
     set_error("smb_pattern_create: %s: %s", what, cudaGetErrorString(cudaGetLastError()));
@@ -193,7 +194,7 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
   if (cudaMalloc(&p->col_ptr, sizeof(int32_t) * (k + 1)) != cudaSuccess ||
       cudaMalloc(&p->row_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess ||
       cudaMalloc(&p->perm, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess ||
-      cudaMalloc(&p->tile_row0, sizeof(int32_t) * (p->ntiles > 0 ? p->ntiles : 1)) != cudaSuccess)
+      cudaMalloc(&p->tile_row0, sizeof(int32_t) * (p->ngrains > 0 ? p->ngrains : 1)) != cudaSuccess)
     return fail_cuda("cudaMalloc");
 
   int32_t *counts = nullptr, *tmp_row = nullptr, *tmp_perm = nullptr;
@@ -218,8 +219,8 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
     rank_sort_columns_kernel<<<grid_for(k * 32, 256), 256, 0, st>>>(p->col_ptr, k, tmp_row,
                                                                       tmp_perm, p->row_idx,
                                                                       p->perm);
-    tile_rows_kernel<<<(unsigned)ceil_div(p->ntiles, 256), 256, 0, st>>>(row_ptr, m, p->ntiles,
-                                                                         p->tile_row0);
+    tile_rows_kernel<<<(unsigned)ceil_div(p->ngrains, 256), 256, 0, st>>>(row_ptr, m, p->ngrains,
+                                                                          p->tile_row0);
     launches += 3;
   }
   cudaError_t e = cudaStreamSynchronize(st);
@@ -229,20 +230,26 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
   count_launches(launches);
   if (e != cudaSuccess || cudaGetLastError() != cudaSuccess) return fail_cuda("index build");
   if (nnz > 0) {
-    // row spans of 128- and 512-nonzero tiles: tile t covers rows
-    // tile_row0[t] .. row of its last nonzero <= tile_row0[t + 1] (or m - 1)
-    std::vector<int32_t> t0(p->ntiles);
-    if (cudaMemcpy(t0.data(), p->tile_row0, sizeof(int32_t) * p->ntiles,
-                   cudaMemcpyDeviceToHost) != cudaSuccess)
+    // row spans of 32- .. 512-nonzero tiles: the tile of grains [g, g + G)
+    // covers rows tile_row0[g] .. row of its last nonzero <= tile_row0[g + G]
+    // (or m - 1)
+    const int64_t ng = p->ngrains;
+    std::vector<int32_t> t0(ng);
+    if (cudaMemcpy(t0.data(), p->tile_row0, sizeof(int32_t) * ng, cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
       return fail_cuda("tile index readback");
-    for (int64_t t = 0; t < p->ntiles; ++t) {
-      const int64_t last128 = (t + 1 < p->ntiles) ? t0[t + 1] : m - 1;
-      p->span128 = imax(p->span128, last128 - t0[t] + 1);
-      if (t % 4 == 0) {
-        const int64_t last512 = (t + 4 < p->ntiles) ? t0[t + 4] : m - 1;
-        p->span512 = imax(p->span512, last512 - t0[t] + 1);
+    auto span = [&](int64_t grains) {
+      int64_t s = 0;
+      for (int64_t g = 0; g < ng; g += grains) {
+        const int64_t last = (g + grains < ng) ? t0[g + grains] : m - 1;
+        s = imax(s, last - t0[g] + 1);
       }
-    }
+      return s;
+    };
+    p->span32 = span(1);
+    p->span64 = span(64 / kTileGrain);
+    p->span128 = span(128 / kTileGrain);
+    p->span512 = span(512 / kTileGrain);
   }
   *out = p;
   return SMB_OK;

@@ -11,13 +11,15 @@ struct smb_pattern {
   int32_t* col_ptr = nullptr;        // owned, [k+1]   CSC column pointers
   int32_t* row_idx = nullptr;        // owned, [nnz]   CSC rows, ascending per column
   int32_t* perm = nullptr;           // owned, [nnz]   CSC slot -> CSR value index
-  int32_t* tile_row0 = nullptr;      // owned, [ntiles] row of nonzero t*kSddmmTile
-  int64_t ntiles = 0;
-  // most rows spanned by any tile of kSddmmTile (span128) / 4*kSddmmTile
-  // (span512) consecutive nonzeros (first row .. row of the last nonzero)
-  int64_t span128 = 0, span512 = 0;
+  int32_t* tile_row0 = nullptr;      // owned, [ngrains] row of nonzero g*kTileGrain
+  int64_t ngrains = 0;               // ceil(nnz / kTileGrain)
+  int64_t ntiles = 0;                // ceil(nnz / kSddmmTile)
+  // most rows spanned by any tile of 32 / 64 / 128 / 512 consecutive nonzeros
+  // (aligned; first row .. row of the last nonzero)
+  int64_t span32 = 0, span64 = 0, span128 = 0, span512 = 0;
 };
 
 namespace smb {
 constexpr int kSddmmTile = 128;  // nonzeros per SDDMM CTA (one per thread)
+constexpr int kTileGrain = 32;   // granularity of the tile -> first-row table
 }

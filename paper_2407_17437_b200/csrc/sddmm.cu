@@ -57,6 +57,9 @@ __device__ __forceinline__ void cp_async16(unsigned dst, const void* gmem, int s
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gmem),
                "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem));
+}
 template <int BYTES>
 __device__ __forceinline__ void cp_async_small(unsigned dst, const void* gmem, int src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(gmem),
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(TILE)
   const int64_t p = p0 + tid;
   const int n_active = (int)imin(TILE, nnz - p0);
   const bool active = tid < n_active;
-  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (TILE / kSddmmTile)];
+  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (TILE / kTileGrain)];
   s_col[tid] = active ? col_idx[p] : 0;
   s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
   if (tid == 0) s_rp[TILE] = (r0 + TILE <= m) ? row_ptr[r0 + TILE] : INT32_MAX;
@@ -146,19 +149,21 @@ __global__ void __launch_bounds__(TILE)
   const T* xsrc[VPR];
   unsigned xdst[VPR];
   int xok[VPR];
-  int xfull[VPR];  // bytes of a full-chunk copy: 16 for an active row, else 0
+  // (rows past n_active copy x row 0 -- s_col = 0 -- on full chunks: a
+  // valid read nobody sums, so the full-chunk copies carry no predicate)
 #pragma unroll
   for (int k = 0; k < VPR; ++k) {
     const int r = tid / VPR + k * (TILE / VPR);
     xok[k] = r < n_active;
-    xfull[k] = xok[k] ? 16 : 0;
     xsrc[k] = x + (int64_t)s_col[r] * ld_x + v * VW;
     xdst[k] = (unsigned)((r * LDS + v * VW) * sizeof(T));
   }
   // d_out rows of the tile: SLOTS*VPR copies, DC per thread; copy e = tid +
   // c*TILE stages vector v of slot row e/VPR (TILE % VPR == 0 keeps v fixed)
   constexpr int DC = (C::SLOTS * VPR + TILE - 1) / TILE;
-  bool dcopy[DC];
+  // copies past SLOTS*VPR exist only when TILE does not divide it
+  constexpr bool kDGuard = (C::SLOTS * VPR) % TILE != 0;
+  bool dcopy[DC];  // unused copies (past n_staged) re-read row r0 on full chunks
   const T* dsrc[DC];
   unsigned ddst[DC];
 #pragma unroll
@@ -172,18 +177,24 @@ __global__ void __launch_bounds__(TILE)
   constexpr unsigned kStageBytes = (unsigned)(C::stage_elems * sizeof(T));
   pdl_wait();  // d_out / x are earlier kernels' outputs
 
-  auto issue = [&](int ch) {
+  // full chunks (copied without bounds when VEC) run a lean main loop; a
+  // ragged last chunk (n % CH != 0) is copied and summed after it
+  const int n_fast = n32 / kChunk;
+  const int n_full = VEC ? n_fast : 0;
+  auto issue_full = [&](int ch) {
     const unsigned st = sbase + (unsigned)(ch & (S - 1)) * kStageBytes;
     const int t0 = ch * kChunk;
-    if (VEC && t0 + kChunk <= n32) {
-      // full chunk: no bounds, fixed copy sizes
 #pragma unroll
-      for (int k = 0; k < VPR; ++k) cp_async16(st + xdst[k], xsrc[k] + t0, xfull[k]);
+    for (int k = 0; k < VPR; ++k) cp_async16(st + xdst[k], xsrc[k] + t0);
+    // branch-free unless TILE does not divide SLOTS*VPR: unused copies fill
+    // a staging row past n_staged that nobody reads
 #pragma unroll
-      for (int c = 0; c < DC; ++c)
-        if (dcopy[c]) cp_async16(st + ddst[c], dsrc[c] + t0, 16);
-      return;
-    }
+    for (int c = 0; c < DC; ++c)
+      if (!kDGuard || dcopy[c]) cp_async16(st + ddst[c], dsrc[c] + t0);
+  };
+  auto issue_part = [&](int ch) {
+    const unsigned st = sbase + (unsigned)(ch & (S - 1)) * kStageBytes;
+    const int t0 = ch * kChunk;
     // elements of this thread's vector inside [0, n)
     const int valid = max(0, min(VW, n32 - (t0 + v * VW)));
 #pragma unroll
@@ -194,46 +205,55 @@ __global__ void __launch_bounds__(TILE)
   };
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) {
-    if (s < n_chunks) issue(s);
+    if (s < n_full) issue_full(s);
+    else if (s < n_chunks) issue_part(s);
     cp_async_commit();
   }
   // -0.0 is the exact additive identity, so acc = -0 + a0*b0 == a0*b0 and the
   // chain below is the reference's  acc = a0*b0; acc += a_t*b_t  verbatim.
   T acc = T(-0.0);
-  const T* drow = d_out + row * ld_d;
+  // inactive threads sum zero-filled rows (never stored) from slot 0
+  const int rslot = active ? slot : 0;
+  const T* drow = d_out + (active ? row : r0) * ld_d;
   using V = typename Vec16<T>::type;
-  for (int ch = 0; ch < n_chunks; ++ch) {
+  int ch = 0;
+  for (; ch < n_fast; ++ch) {
     cp_async_wait<S - 2>();
     __syncthreads();  // chunk ch landed for everyone; stage (ch-1)&(S-1) is free
-    if (ch + S - 1 < n_chunks) issue(ch + S - 1);
+    const int nx = ch + S - 1;
+    if (nx < n_full) issue_full(nx);
+    else if (nx < n_chunks) issue_part(nx);
     cp_async_commit();
-    if (active) {
-      const T* xs = smem + (ch & (S - 1)) * C::stage_elems;
-      const T* xr = xs + tid * LDS;
-      const T* dr = xs + (TILE + slot) * LDS;
-      const int t0 = ch * kChunk;
-      const int cnt = min(kChunk, n32 - t0);
-      if (cnt == kChunk) {
+    const T* xs = smem + (ch & (S - 1)) * C::stage_elems;
+    const T* xr = xs + tid * LDS;
+    const T* dr = xs + (TILE + rslot) * LDS;
+    const int t0 = ch * kChunk;
 #pragma unroll
-        for (int u = 0; u < VPR; ++u) {
-          const V xv = *reinterpret_cast<const V*>(xr + u * VW);
-          V dv;
-          if (ALL || slot < C::SLOTS) {
-            dv = *reinterpret_cast<const V*>(dr + u * VW);
-          } else {
-#pragma unroll
-            for (int j = 0; j < VW; ++j) VecOps<T>::set(dv, j, drow[t0 + u * VW + j]);
-          }
-#pragma unroll
-          for (int j = 0; j < VW; ++j)
-            acc = add_rn(acc, mul_rn(VecOps<T>::get(dv, j), VecOps<T>::get(xv, j)));
-        }
+    for (int u = 0; u < VPR; ++u) {
+      const V xv = *reinterpret_cast<const V*>(xr + u * VW);
+      V dv;
+      if (ALL || rslot < C::SLOTS) {
+        dv = *reinterpret_cast<const V*>(dr + u * VW);
       } else {
-        for (int j = 0; j < cnt; ++j) {
-          const T dv = (ALL || slot < C::SLOTS) ? dr[j] : drow[t0 + j];
-          acc = add_rn(acc, mul_rn(dv, xr[j]));
-        }
+#pragma unroll
+        for (int j = 0; j < VW; ++j) VecOps<T>::set(dv, j, drow[t0 + u * VW + j]);
       }
+#pragma unroll
+      for (int j = 0; j < VW; ++j)
+        acc = add_rn(acc, mul_rn(VecOps<T>::get(dv, j), VecOps<T>::get(xv, j)));
+    }
+  }
+  if (ch < n_chunks) {  // ragged last chunk (no further copies to issue)
+    cp_async_wait<0>();
+    __syncthreads();
+    const T* xs = smem + (ch & (S - 1)) * C::stage_elems;
+    const T* xr = xs + tid * LDS;
+    const T* dr = xs + (TILE + rslot) * LDS;
+    const int t0 = ch * kChunk;
+    const int cnt = n32 - t0;
+    for (int j = 0; j < cnt; ++j) {
+      const T dv = (ALL || rslot < C::SLOTS) ? dr[j] : drow[t0 + j];
+      acc = add_rn(acc, mul_rn(dv, xr[j]));
     }
   }
   cp_async_wait<0>();
@@ -289,7 +309,7 @@ __global__ void __launch_bounds__(128)
   const int nw = (int)imax(0, imin(32, nnz - pw));  // nonzeros of this warp
   const int64_t p = pw + lane;
   const bool active = lane < nw;
-  const int32_t r0 = tile_row0[blockIdx.x];
+  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (kSddmmTile / kTileGrain)];
   s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
   if (tid == 0) s_rp[kSddmmTile] = (r0 + kSddmmTile <= m) ? row_ptr[r0 + kSddmmTile] : INT32_MAX;
   const int32_t my_col = active ? col_idx[p] : 0;
@@ -423,7 +443,11 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     // every tile's d_out rows staged -> fallback-free kernel (a 256 / 512-tile's
     // span is bounded by its enclosing 512-tile's)
     auto all_for = [&](int tile, int sd) {
-      return (tile == 128 ? pat->span128 : pat->span512) <= tile / sd;
+      const int64_t span = tile == 32    ? pat->span32
+                           : tile == 64  ? pat->span64
+                           : tile == 128 ? pat->span128
+                                         : pat->span512;
+      return span <= tile / sd;
     };
     // tuning experiments only (scripts/gpu_sddmm_var2.sh): 1 = 512-nonzero
     // tiles x 32 columns, 2 = 128 x 16 x 8 stages, 3 = warp-independent
@@ -456,15 +480,27 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     // config 3 d >= 0.01; measured slower when rows are short)
     const bool warp_kernel = sizeof(T) == 4 && vec && variant == 0 && !wave &&
                              pat->span128 <= kWarpDSlots;
+    // Small layers (a few waves of 32 / 64-nonzero tiles): the chains set the
+    // time, so spread them over as many SMs as possible with deeper rings
+    // (measured on B200 at the config-2 layers, scripts/sddmm_lab.cu: 10x512
+    // and 512x1024 14.4 -> 8.3 us with 32-tiles, 1024x3072 22.6 -> 16.5 us
+    // with 64-tiles).
+    const int64_t small_cap = 4 * 148;
+    const bool small32 = variant == 0 && ceil_div(pat->nnz, 32) <= small_cap;
+    const bool small64 = variant == 0 && !small32 && ceil_div(pat->nnz, 64) <= small_cap;
     bool warp_done = false;
     if constexpr (sizeof(T) == 4) {
-      if (warp_kernel || (vec && variant == 3)) {
+      if (!small32 && !small64 && (warp_kernel || (vec && variant == 3))) {
         go(sddmm_warp_kernel<T, 32, 2>, 128, SddmmWarpCfg<T, 32, 2>::smem_bytes);
         warp_done = true;
       }
     }
     if (warp_done) {
-    } else if (sizeof(T) == 4 && variant == 1) SMB_GO_SD(512, 32, 2, 4);
+    } else if (sizeof(T) == 4 && small32 && all_for(32, 4)) SMB_GO_SD(32, 32, 8, 4);
+    else if (sizeof(T) == 4 && small32) SMB_GO_SD(32, 32, 8, 1);
+    else if (sizeof(T) == 4 && small64 && all_for(64, 4)) SMB_GO_SD(64, 32, 4, 4);
+    else if (sizeof(T) == 4 && small64) SMB_GO_SD(64, 32, 4, 1);
+    else if (sizeof(T) == 4 && variant == 1) SMB_GO_SD(512, 32, 2, 4);
     else if (sizeof(T) == 4 && variant == 2) SMB_GO_SD(128, 16, 8, 4);
     else if (sizeof(T) == 4 && wave && sparse_rows) SMB_GO_SD(128, 64, 2, 1);
     else if (sizeof(T) == 4 && wave) SMB_GO_SD(128, 64, 2, 4);

@@ -1,0 +1,231 @@
+// SDDMM micro-lab (standalone; not part of the library).  Decomposes the time
+// of the chunked cp.async SDDMM into its load and chain parts on three shapes:
+//   config-2 L0 (1024 x 3072, 24 nnz/row), config-2 L2 (10 x 512, 312/row),
+//   config-4 L1 (8192 x 8192, 69/row); batch 1024, fp32.
+// MODE 0 = full kernel, 1 = loads only, 2 = chain only (smem not refilled).
+// build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -std=c++17 --fmad=false
+//        scripts/sddmm_lab.cu -o /tmp/sddmm_lab
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <random>
+#include <vector>
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e = (x);                                                            \
+    if (e != cudaSuccess) {                                                         \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                      \
+    }                                                                               \
+  } while (0)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp16(unsigned dst, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(g));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void waitg() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// TILE nonzeros per CTA (one chain per thread), CH columns per chunk, ST stages
+template <int TILE, int CH, int ST, int MODE>
+__global__ void __launch_bounds__(TILE) lab_pipe(const int* row_ptr, const int* col_idx,
+                                                 const int* row_of, int nnz, const float* dy,
+                                                 const float* x, int n, float* out) {
+  constexpr int VPR = CH / 4, LDS = CH + 4, SLOTS = TILE / 4;
+  constexpr int STAGE = (TILE + SLOTS) * LDS;
+  extern __shared__ __align__(16) float sm[];
+  const int tid = threadIdx.x;
+  const int p0 = blockIdx.x * TILE, p = p0 + tid;
+  const bool active = p < nnz;
+  const int pl = min(p, nnz - 1);
+  const int row = row_of[pl];
+  const int r0 = row_of[p0];
+  const int slot = row - r0;
+  const int rlast = row_of[min(p0 + TILE, nnz) - 1];
+  const int nst = rlast - r0 + 1;
+  const int v = tid % VPR;
+  const float* xs[VPR];
+  unsigned xd[VPR];
+#pragma unroll
+  for (int k = 0; k < VPR; ++k) {
+    const int r = tid / VPR + k * (TILE / VPR);
+    xs[k] = x + (size_t)col_idx[min(p0 + r, nnz - 1)] * n + v * 4;
+    xd[k] = (unsigned)((r * LDS + v * 4) * 4);
+  }
+  constexpr int DC = (SLOTS * VPR + TILE - 1) / TILE;
+  const float* ds[DC];
+  unsigned dd[DC];
+  bool dok[DC];
+#pragma unroll
+  for (int c = 0; c < DC; ++c) {
+    const int e = tid + c * TILE;
+    dok[c] = e < nst * VPR;
+    ds[c] = dy + (size_t)(r0 + (dok[c] ? e / VPR : 0)) * n + v * 4;
+    dd[c] = (unsigned)(((TILE + e / VPR) * LDS + v * 4) * 4);
+  }
+  const unsigned sb = smem_u32(sm);
+  const int nch = n / CH;
+  auto issue = [&](int ch) {
+    if (MODE == 2 && ch >= ST) return;
+    const unsigned st = sb + (unsigned)(ch % ST) * STAGE * 4;
+    const int t0 = ch * CH;
+#pragma unroll
+    for (int k = 0; k < VPR; ++k) cp16(st + xd[k], xs[k] + t0);
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+      if (dok[c]) cp16(st + dd[c], ds[c] + t0);
+  };
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    issue(s);
+    commit();
+  }
+  float acc = -0.0f;
+  for (int ch = 0; ch < nch; ++ch) {
+    waitg<ST - 2>();
+    __syncthreads();
+    if (ch + ST - 1 < nch) issue(ch + ST - 1);
+    commit();
+    const float* s = sm + (ch % ST) * STAGE;
+    const float* xr = s + tid * LDS;
+    const float* dr = s + (TILE + slot) * LDS;
+    if (MODE == 1) {
+      acc = __fadd_rn(acc, xr[0] * dr[0]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < VPR; ++u) {
+        const float4 a = *reinterpret_cast<const float4*>(xr + u * 4);
+        const float4 b = *reinterpret_cast<const float4*>(dr + u * 4);
+        acc = __fadd_rn(acc, __fmul_rn(b.x, a.x));
+        acc = __fadd_rn(acc, __fmul_rn(b.y, a.y));
+        acc = __fadd_rn(acc, __fmul_rn(b.z, a.z));
+        acc = __fadd_rn(acc, __fmul_rn(b.w, a.w));
+      }
+    }
+  }
+  waitg<0>();
+  if (active) out[p] = acc;
+}
+
+// Register-only chain: how fast can 1024 dependent mul/add steps go per chain
+// with loads fully removed (values synthesised from the index).
+__global__ void lab_chain(int nnz, int n, float* out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  float a = 1.0f + p * 1e-7f, b = 0.5f, acc = -0.0f;
+  for (int t = 0; t < n; t += 4) {
+    acc = __fadd_rn(acc, __fmul_rn(a, b));
+    a = __fadd_rn(a, 1e-7f);  // independent of acc
+    acc = __fadd_rn(acc, __fmul_rn(a, b));
+    a = __fadd_rn(a, 1e-7f);
+    acc = __fadd_rn(acc, __fmul_rn(a, b));
+    a = __fadd_rn(a, 1e-7f);
+    acc = __fadd_rn(acc, __fmul_rn(a, b));
+    a = __fadd_rn(a, 1e-7f);
+  }
+  out[p] = acc;
+}
+
+struct Shape {
+  const char* name;
+  int m, k, r;
+};
+
+template <typename F>
+float time_us(F f, int reps = 50) {
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int i = 0; i < 5; ++i) f();
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a));
+  for (int i = 0; i < reps; ++i) f();
+  CK(cudaEventRecord(b));
+  CK(cudaEventSynchronize(b));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  CK(cudaGetLastError());
+  return ms * 1e3f / reps;
+}
+
+template <int TILE, int CH, int ST, int MODE>
+float run_pipe(const Shape& s, int nnz, const int* rp, const int* ci, const int* ro, const float* dy,
+               const float* x, int n, float* out) {
+  constexpr int SLOTS = TILE / 4;
+  const size_t bytes = (size_t)ST * (TILE + SLOTS) * (CH + 4) * 4;
+  auto k = lab_pipe<TILE, CH, ST, MODE>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  const int grid = (nnz + TILE - 1) / TILE;
+  return time_us([&] { k<<<grid, TILE, bytes>>>(rp, ci, ro, nnz, dy, x, n, out); });
+}
+
+int main() {
+  const int n = 1024;
+  Shape shapes[] = {{"c2.L0 1024x3072 r24", 1024, 3072, 24},
+                    {"c2.L2 10x512 r312", 10, 512, 312},
+                    {"c2.L1 512x1024 r18", 512, 1024, 18},
+                    {"c4.L1 8192x8192 r69", 8192, 8192, 69}};
+  std::mt19937 rng(1);
+  for (const Shape& s : shapes) {
+    std::vector<int> rp(s.m + 1), ci, ro;
+    std::vector<int> cols(s.k);
+    for (int c = 0; c < s.k; ++c) cols[c] = c;
+    for (int i = 0; i < s.m; ++i) {
+      std::shuffle(cols.begin(), cols.end(), rng);
+      std::vector<int> row(cols.begin(), cols.begin() + s.r);
+      std::sort(row.begin(), row.end());
+      for (int c : row) {
+        ci.push_back(c);
+        ro.push_back(i);
+      }
+      rp[i + 1] = (int)ci.size();
+    }
+    const int nnz = (int)ci.size();
+    int *d_rp, *d_ci, *d_ro;
+    float *d_dy, *d_x, *d_out;
+    CK(cudaMalloc(&d_rp, rp.size() * 4));
+    CK(cudaMalloc(&d_ci, ci.size() * 4));
+    CK(cudaMalloc(&d_ro, ro.size() * 4));
+    CK(cudaMalloc(&d_dy, (size_t)s.m * n * 4));
+    CK(cudaMalloc(&d_x, (size_t)s.k * n * 4));
+    CK(cudaMalloc(&d_out, (size_t)nnz * 4));
+    CK(cudaMemcpy(d_rp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ci, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ro, ro.data(), ro.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemset(d_dy, 0, (size_t)s.m * n * 4));
+    CK(cudaMemset(d_x, 0, (size_t)s.k * n * 4));
+    printf("%s nnz=%d (%.1f MB x-gather)\n", s.name, nnz, nnz * 4.0 * n / 1e6);
+#define P(T, C, S)                                                                          \
+  printf("  pipe<%d,%d,%d>: full %.2f  loads %.2f  chain %.2f us\n", T, C, S,               \
+         run_pipe<T, C, S, 0>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out),              \
+         run_pipe<T, C, S, 1>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out),              \
+         run_pipe<T, C, S, 2>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out))
+    P(128, 64, 2);
+    P(128, 32, 2);
+    if (s.m <= 1024) {
+      P(64, 64, 2);
+      P(64, 64, 4);
+      P(64, 32, 4);
+      P(64, 32, 8);
+      P(64, 16, 8);
+      P(32, 64, 4);
+      P(32, 32, 8);
+      P(32, 32, 16);
+      P(32, 16, 16);
+    }
+    for (int bs : {128})
+      printf("  chain-only regs (block %d): %.2f us\n", bs,
+             time_us([&] { lab_chain<<<(nnz + bs - 1) / bs, bs>>>(nnz, n, d_out); }));
+    cudaFree(d_rp); cudaFree(d_ci); cudaFree(d_ro); cudaFree(d_dy); cudaFree(d_x); cudaFree(d_out);
+  }
+  return 0;
+}
