@@ -108,6 +108,16 @@ def fp32_peak_tflops() -> float:
         return 74.4  # 148 SMs x 128 lanes x 2 flop x 1.965 GHz
 
 
+def l2_gather_gbs() -> float:
+    """L2 -> SM row-gather bandwidth measured on a B200 by scripts/l2_peak.cu
+    (profiles/l2_peak.json): the bound of the per-nonzero row gathers."""
+    p = REPO / "profiles" / "l2_peak.json"
+    try:
+        return float(json.loads(p.read_text())["l2_gather_rows128_gbs"])
+    except Exception:
+        return 10684.7
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -403,6 +413,14 @@ def run_ours(args):
                     "t_roof_us": round(1e6 * max(t_bytes, t_flops), 3),
                     "roof_frac": round(max(t_bytes, t_flops) / (us * 1e-6), 4),
                     "pairs_per_s": round(u.nvals * B / (us * 1e-6), 1)}
+        # the operand each nonzero gathers (a B-wide row of x or d_out) comes
+        # from L2: 4*nnz*B bytes at the measured row-gather rate
+        l2 = l2_gather_gbs()
+        g_bytes = 4 * u.nvals * B
+        roofline["l2_gather"] = {"bytes": g_bytes, "peak_gbs": l2,
+                                 "t_us": round(1e6 * g_bytes / (l2 * 1e9), 3),
+                                 "frac": round(g_bytes / (l2 * 1e9) / (us * 1e-6), 4),
+                                 "peak_source": "profiles/l2_peak.json (scripts/l2_peak.cu)"}
 
     # ---- end to end through the public API: pinned host batches ----
     R = 4

@@ -187,6 +187,28 @@ SMB_API int smb_sddmm_update_into(int dtype, const smb_pattern* pattern, const v
                                   void* grad_bias_out, int opt_kind, double mu, double eta,
                                   void* stream);
 
+/* The whole backward of a wide sparse layer in ONE launch, bit-identical to
+ *   smb_spmm_t(pattern, values, d_out, ..., mask = mask ? x : NULL, d_x)
+ *   + smb_sddmm_update_into(pattern, d_out, x, ..., values, values_out, ...)
+ * (nn.py:178-198 minus the bias side; _kernels.py:40-75; train.py:400-401:
+ * d_x uses the pre-update weights).  Both products are walked in CSC order
+ * so every d_out row a column gathers feeds the transposed product AND the
+ * SDDMM chains of that column (half the L2 traffic of the two kernels).
+ * x is the layer input (the post-ReLU activation of the layer below, so
+ * mask != 0 applies ReLU.backward as d_x *= (x > 0), nn.py:89-91).  The bias
+ * sides of this layer and of the layer below are NOT computed
+ * (smb_bias_grad_update).  Valid when smb_backward_fused_supported() (every
+ * column holds <= 256 nonzeros).  values_out may equal values; d_x must not
+ * overlap d_out or x.  Measured slower than the two separate kernels on B200
+ * (shared-memory bound, csrc/bwd_fused.cu), so the fused training step does
+ * not use it. */
+SMB_API int smb_backward_fused_supported(int dtype, const smb_pattern* pattern);
+SMB_API int smb_backward_fused(int dtype, const smb_pattern* pattern, const void* d_out,
+                               int64_t ld_dout, const void* x, int64_t ld_x, int64_t n, int mask,
+                               void* d_x, int64_t ld_dx, const void* values, void* values_out,
+                               void* velocity, void* grad_out, int opt_kind, double mu,
+                               double eta, void* stream);
+
 /* grad_bias = row_sums(d_out) (numpy pairwise order) and the bias optimizer
  * update; one warp per row (nn.py:184, 118-131).  Dense layers and any
  * layer whose output gradient was not produced by smb_spmm_t_bias. */

@@ -24,6 +24,7 @@
 // (A TMA variant -- one cp.async.bulk per 128-byte row, producer warp +
 // mbarrier ring -- measured 4x slower on B200: 128-byte bulk copies are
 // request-rate bound at ~1.1 TB/s.  See DESIGN.md.)
+#include "async_copy.cuh"
 #include "pattern.cuh"
 
 namespace smb {
@@ -50,27 +51,6 @@ struct SddmmCfg {
   static_assert(TILE % VPR == 0, "tile / vector split");
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void cp_async16(unsigned dst, const void* gmem, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gmem),
-               "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async16(unsigned dst, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem));
-}
-template <int BYTES>
-__device__ __forceinline__ void cp_async_small(unsigned dst, const void* gmem, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(dst), "l"(gmem),
-               "n"(BYTES), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 // Row of nonzero p inside a tile starting at row r0, through a shared window
 // s_rp[0..W] = row_ptr[r0 .. r0+W]; global binary search when the tile spans
 // more than W rows (long runs of empty rows).
@@ -91,21 +71,6 @@ __device__ __forceinline__ int64_t tile_row_of(int64_t p, int32_t r0, const int3
     if ((int64_t)row_ptr[mid] <= p) lo = mid; else hi = mid;
   }
   return lo;
-}
-
-// Copy `bytes` (<= 16) of a 16-byte vector; VEC: one cp.async with zero fill,
-// else element-wise (unaligned operands).
-template <typename T, bool VEC>
-__device__ __forceinline__ void copy_vec(unsigned dst, const T* src, int valid_elems) {
-  constexpr int VW = 16 / sizeof(T);
-  if constexpr (VEC) {
-    cp_async16(dst, src, valid_elems * (int)sizeof(T));
-  } else {
-#pragma unroll
-    for (int j = 0; j < VW; ++j)
-      cp_async_small<sizeof(T)>(dst + j * sizeof(T), j < valid_elems ? src + j : src,
-                                j < valid_elems ? (int)sizeof(T) : 0);
-  }
 }
 
 // ALL: every tile's d_out rows fit the SLOTS staging rows (checked on the

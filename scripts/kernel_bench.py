@@ -19,6 +19,7 @@ from paper_2407_17437_b200.tensor_core import ptr, stream_ptr
 
 HBM = 6446.6  # GB/s, MEASURED_PEAKS.json hbm_gbs
 FP32_TFLOPS = 70.83  # FFMA peak, profiles/fp32_peak.json (scripts/fp32_peak.cu)
+L2_GATHER = 10684.7  # GB/s, L2 -> SM row gathers, profiles/l2_peak.json (scripts/l2_peak.cu)
 
 
 def bytes_model(m, k, z, B):
@@ -52,11 +53,18 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
                 elif kind == "spmm_t":
                     _lib.call("smb_spmm_t", 0, pat.handle, ptr(vals), ptr(dY), B, B, None, 0,
                               ptr(out), B, st)
-                else:
+                elif kind == "sddmm_update":
                     _lib.call("smb_sddmm_update", 0, pat.handle, ptr(dY), B, ptr(X), B, B,
                               ptr(vals), ptr(vel), None, None, None, None, 3, 0.9, 1e-6, st)
+                else:  # spmm_t (masked by X) + SDDMM + update in one CSC-order launch
+                    _lib.call("smb_backward_fused", 0, pat.handle, ptr(dY), B, ptr(X), B, B, 1,
+                              ptr(out), B, ptr(vals), ptr(vals), ptr(vel), None, 3, 0.9, 1e-6, st)
 
-            for kind in ("spmm", "spmm_t", "sddmm_update"):
+            kinds = ["spmm", "spmm_t", "sddmm_update"]
+            fused_ok = _lib.load().smb_backward_fused_supported(0, pat.handle) == 1
+            if fused_ok:
+                kinds.append("bwd_fused")
+            for kind in kinds:
                 times = []
                 for it in range(iters + 2):
                     flush.fill_(it)
@@ -70,12 +78,22 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
                 res[kind] = float(np.median(times))
             bs = bytes_model(n, n, nnz, B)
             rec = {"density": d, "nnz": nnz, "B": B}
-            for (kind, us), b in zip(res.items(), bs):
+            if fused_ok:
+                # spmm_t + SDDMM/update of one layer, staged once in CSC order
+                sep = res["spmm_t"] + res["sddmm_update"]
+                rec["bwd_fused"] = {"us": round(res["bwd_fused"], 2),
+                                    "separate_us": round(sep, 2),
+                                    "speedup": round(sep / res["bwd_fused"], 3),
+                                    "l2_gather_frac": round(4 * nnz * B / (L2_GATHER * 1e9)
+                                                            / (res["bwd_fused"] * 1e-6), 3)}
+            for (kind, us), b in zip(list(res.items())[:3], bs):
                 # t_roof = max(bytes / HBM, 2 z B / FP32 peak)
                 t_roof = max(b / (HBM * 1e9), 2 * nnz * B / (FP32_TFLOPS * 1e12))
                 rec[kind] = {"us": round(us, 2), "GB/s": round(b / us / 1e3, 1),
                              "frac_hbm": round(b / us / 1e3 / HBM, 3),
                              "roof_frac": round(t_roof / (us * 1e-6), 3),
+                             # each nonzero gathers one B-wide row (4 z B bytes)
+                             "l2_gather_frac": round(4 * nnz * B / (L2_GATHER * 1e9) / (us * 1e-6), 3),
                              "Gpairs/s": round(nnz * B / us / 1e3, 1)}
             print(json.dumps(rec), flush=True)
 
