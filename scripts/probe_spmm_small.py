@@ -26,8 +26,8 @@ for li, layer in enumerate(model.layers):
     d = torch.randn(m, B, device="cuda"); dx = torch.empty(k, B, device="cuda")
     mask = torch.rand(k, B, device="cuda") - 0.3
     bias = torch.zeros(m, device="cuda")
-    f = lambda: _lib.call("smb_spmm", 0, ptr(W.row_ptr), ptr(W.col_idx), ptr(W.values), m, k,
-                          ptr(x), B, B, ptr(bias), 1, ptr(y), B, stream_ptr())
+    f = lambda: _lib.call("smb_spmm_p", 0, W.pattern.handle, ptr(W.values), ptr(x), B, B,
+                          ptr(bias), 1, ptr(y), B, stream_ptr())
     g = lambda: _lib.call("smb_spmm_t", 0, W.pattern.handle, ptr(W.values), ptr(d), B, B,
                           ptr(mask), B, ptr(dx), B, stream_ptr())
     out.append(f"L{li} {m}x{k} z={W.nnz}: fwd {timeit(f):.2f} us, T {timeit(g):.2f} us")

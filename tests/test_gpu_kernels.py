@@ -362,7 +362,8 @@ def test_spmv_single_column_strided_with_epilogue(oracle, relu):
 @pytest.mark.parametrize("shape,density", [((10, 512, 1024), 0.6), ((7, 300, 777), 0.9),
                                            ((20, 2000, 600), 0.3), ((3, 50, 515), 0.05),
                                            ((10, 512, 100), 0.6), ((5, 1000, 37), 0.4),
-                                           ((12, 64, 300), 0.9)])
+                                           ((12, 64, 300), 0.9), ((16, 700, 512), 0.5),
+                                           ((4, 300, 64), 0.9), ((6, 1200, 256), 0.5)])
 def test_few_long_rows_wide_batch_bit_exact(oracle, shape, density):
     """Few output rows (the output layer): the three-group register-pipelined
     kernel (batch >= 512) and the parallel-products kernel (narrower
