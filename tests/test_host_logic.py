@@ -31,6 +31,14 @@ def test_library_exports_every_declared_symbol():
     assert lib.smb_abi_version() == 1
 
 
+def test_integration_doc_covers_every_entry_point():
+    """INTEGRATION.md maps every C-ABI entry point to the reference interface
+    it replaces (or says what it is for)."""
+    doc = (REPO / "INTEGRATION.md").read_text()
+    missing = [s for s in header_symbols() if s not in doc]
+    assert not missing, missing
+
+
 def test_status_codes_map_to_reference_exceptions():
     lib = _lib.load()
     # argument checks run on the host before any device work
