@@ -10,7 +10,7 @@ of the reference's per-batch loop (train.py:389-402):
                 + row_sums(d_{l-1}), update b_{l-1}              + bias side of layer l-1)
                 grad_l = sddmm(d_l, a_{l-1}); update W_l        smb_sddmm_update (fused)
     next batch  gathered ahead into the other input slot, step  smb_gather_columns_ahead +
-                counter += 1 (own stream, beside the forward)   smb_step_counter_advance
+                counter += 1 (own stream, beside the last SDDMM) smb_step_counter_advance
 
 spmm_t of layer l runs before the update of layer l (pre-update weights,
 train.py:400-401).  The layer-1 input gradient is never computed: the
@@ -342,10 +342,19 @@ class FusedTrainStep:
         main = torch.cuda.current_stream()
         # gather steps: this batch is already in x_in / t_in (prefetched by
         # the previous step or by step()'s prologue); the next one is
-        # gathered into the other slot beside the (latency-bound) forward
-        if gather:
+        # gathered into the other slot on its own stream, beside the layer-0
+        # SDDMM at the end of
+        # the backward (measured 78.2 -> 76.5 us/step at config 2 against
+        # launching it at the step start, where it competed with the
+        # L2-bound first-layer SpMM); SMB_PREFETCH_AT=start restores that
+        prefetch_at = os.environ.get("SMB_PREFETCH_AT", "end")
+
+        def prefetch():
             with torch.cuda.stream(fork("prefetch")):
                 self._gather_into(1 - self._slot, stream_ptr(), ahead=True)
+
+        if gather and prefetch_at == "start":
+            prefetch()
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
         tail = self.fuse_tail
@@ -456,6 +465,8 @@ class FusedTrainStep:
                                B, b, vb, gb, kind, mu, float(eta), st)
             if not (overlap and u.sparse):
                 self._weight_side(u, dy, x_prev, eta, fuse_update, st)
+        if gather and prefetch_at != "start":
+            prefetch()
         for s_ in forked:
             main.wait_stream(s_)  # join: the step ends when every update has
 
