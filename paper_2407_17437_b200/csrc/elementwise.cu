@@ -229,8 +229,12 @@ __global__ void __launch_bounds__(ROWS ? 1024 : 128)
     local += static_cast<double>(sub_rn(log_full(s), zt));
   }
   pdl_trigger();
-  // fixed-order block reduction of the loss
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (!ROWS) {
+    // nothing after the columns: no loss wanted, no counter to advance
+    if (loss_out == nullptr && counter == nullptr) return;
+  }
+  // fixed-order block reduction of the loss
   for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
   if (lane == 0) s_warp[warp] = local;
   __syncthreads();

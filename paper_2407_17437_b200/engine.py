@@ -350,7 +350,9 @@ class FusedTrainStep:
         prefetch_at = os.environ.get("SMB_PREFETCH_AT", "end")
 
         def prefetch():
-            with torch.cuda.stream(fork("prefetch")):
+            # (serialised on the main stream when overlap is off: the
+            # per-kernel timing pass then sees each kernel alone)
+            with torch.cuda.stream(fork("prefetch")) if overlap else _nullctx():
                 self._gather_into(1 - self._slot, stream_ptr(), ahead=True)
 
         if gather and prefetch_at == "start":
