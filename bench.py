@@ -190,8 +190,20 @@ def dist_env():
     return ws, rank, local
 
 
+def workload_name(args) -> str:
+    """Which BASELINE.json config this run measures."""
+    chain = args.layers.replace(",", "-")
+    if chain == "3072-8192-8192-8192-10":
+        return "configs[3]"
+    if chain == "3072-65536-65536-10":
+        return "configs[4]"
+    if chain == "3072-1024-512-10":
+        return "configs[1] point" if args.batch == 1024 else "configs[0]/[1] point"
+    return "custom"
+
+
 def config_dict(args, ws):
-    return {"workload": f"configs[1] point: MLP {args.layers.replace(',', '-')} ER d={args.density} "
+    return {"workload": f"{workload_name(args)}: MLP {args.layers.replace(',', '-')} ER d={args.density} "
                         f"B={args.batch}/GPU fp32 Nesterov lr={args.lr}"
                         + ("" if args.backend == "sparse" else f" backend={args.backend}"),
             "layers": [int(x) for x in args.layers.split(",")], "density": args.density,
