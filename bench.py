@@ -115,7 +115,7 @@ def l2_gather_gbs() -> float:
     try:
         return float(json.loads(p.read_text())["l2_gather_rows128_gbs"])
     except Exception:
-        return 10684.7
+        return 12563.7
 
 
 class ClockSampler:

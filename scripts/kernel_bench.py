@@ -19,7 +19,7 @@ from paper_2407_17437_b200.tensor_core import ptr, stream_ptr
 
 HBM = 6446.6  # GB/s, MEASURED_PEAKS.json hbm_gbs
 FP32_TFLOPS = 70.83  # FFMA peak, profiles/fp32_peak.json (scripts/fp32_peak.cu)
-L2_GATHER = 10684.7  # GB/s, L2 -> SM row gathers, profiles/l2_peak.json (scripts/l2_peak.cu)
+L2_GATHER = 12563.7  # GB/s, L2 -> SM row gathers, profiles/l2_peak.json (scripts/l2_peak.cu)
 
 
 def bytes_model(m, k, z, B):

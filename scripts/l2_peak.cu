@@ -1,6 +1,7 @@
 // L2 -> SM bandwidth on this GPU (standalone; writes JSON to stdout).
 //   stream : coalesced 16-byte loads over a 64 MB buffer that stays in L2
 //   rows128: each warp reads whole 128-byte row segments of random rows of a
+//            (8 independent loads in flight per thread)
 //            32 MB [8192 x 1024] fp32 matrix (the SpMM / SDDMM gather shape)
 //   rows64 : the same with 64-byte segments
 // Every variant reads the buffer a few times per launch; the first launch
@@ -22,8 +23,10 @@ __global__ void stream_kernel(const float4* __restrict__ a, size_t n4, int reps,
   if (acc == 123.456f) out[0] = acc;
 }
 
-// SEG bytes per row segment; a warp reads 512 / SEG segments per instruction
-template <int SEG>
+// SEG bytes per row segment; a warp reads 512 / SEG segments per instruction.
+// UNR independent loads per thread are in flight per iteration (the
+// addresses never depend on loaded data), so the rate is not latency-bound.
+template <int SEG, int UNR>
 __global__ void rows_kernel(const float* __restrict__ x, int rows, int ld, int iters,
                             const int* __restrict__ perm, float* out) {
   constexpr int LPS = SEG / 16;  // lanes per segment
@@ -31,13 +34,19 @@ __global__ void rows_kernel(const float* __restrict__ x, int rows, int ld, int i
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   float acc = 0.f;
   unsigned r = (unsigned)perm[gw % rows];
-  for (int it = 0; it < iters; ++it) {
-    // 32 / LPS segments per warp-instruction, each from a pseudo-random row
-    const int seg = lane / LPS;
-    const int row = (int)((r + seg * 977u + it * 131u) % (unsigned)rows);
-    const int col = ((it * 7 + seg) % (ld * 4 / SEG)) * (SEG / 4) + (lane % LPS) * 4;
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(x + (size_t)row * ld + col));
-    acc += v.x + v.y + v.z + v.w;
+  const int seg = lane / LPS;
+  for (int it = 0; it < iters; it += UNR) {
+    float4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      // 32 / LPS segments per warp-instruction, each from a pseudo-random row
+      const unsigned ru = r * (2654435761u * (u + 1)) + 977u * seg;
+      const int row = (int)(ru % (unsigned)rows);
+      const int col = (((it + u) * 7 + seg) % (ld * 4 / SEG)) * (SEG / 4) + (lane % LPS) * 4;
+      v[u] = __ldcg(reinterpret_cast<const float4*>(x + (size_t)row * ld + col));
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
     r = r * 1103515245u + 12345u;
   }
   if (acc == 123.456f) out[0] = acc;
@@ -76,16 +85,16 @@ int main() {
   const int iters = 2048, blocks = 148 * 8, threads = 256;
   const double gather_bytes = 5.0 * (double)blocks * threads * iters * 16;
   double g128, g64;
-  rows_kernel<128><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
+  rows_kernel<128, 8><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
   cudaEventRecord(a);
-  for (int i = 0; i < 5; ++i) rows_kernel<128><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
+  for (int i = 0; i < 5; ++i) rows_kernel<128, 8><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   cudaEventElapsedTime(&ms, a, b);
   g128 = gather_bytes / (ms * 1e-3) / 1e9;
-  rows_kernel<64><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
+  rows_kernel<64, 8><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
   cudaEventRecord(a);
-  for (int i = 0; i < 5; ++i) rows_kernel<64><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
+  for (int i = 0; i < 5; ++i) rows_kernel<64, 8><<<blocks, threads>>>(x, rows, ld, iters, perm, out);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   cudaEventElapsedTime(&ms, a, b);
