@@ -307,6 +307,18 @@ SMB_API int smb_softmax_ce_step(int dtype, const void* y, int64_t ld_y, const vo
                                 double eta, int32_t* step_counter, int32_t modulo,
                                 void* workspace, void* stream);
 
+/* d_x = W^T d_out for a dense layer of m <= 32 output rows (the
+ * ER-saturated output layer; DenseLinearLayer.backward, nn.py:241-255),
+ * each element summed over ascending i with separately rounded multiply /
+ * add, then d_x *= (mask > 0) when mask != NULL (ReLU.backward of the layer
+ * below, nn.py:89-91).  W is [m, ld_w] row-major, d_out [m, ld_d], mask /
+ * d_x [k, ld].  One HBM pass over mask and d_x (the cuBLAS product plus a
+ * separate mask kernel make three). */
+SMB_API int smb_dense_backward_input(int dtype, const void* w, int64_t ld_w, int64_t m, int64_t k,
+                                     const void* d_out, int64_t ld_d, int64_t n,
+                                     const void* mask, int64_t ld_mask, void* d_x,
+                                     int64_t ld_dx, void* stream);
+
 /* y = max(x, 0) (nn.py:86-87) and out = d_out * (x_cached > 0) (nn.py:89-91). */
 SMB_API int smb_relu(int dtype, const void* x, int64_t ld_x, int64_t m, int64_t n, void* y, int64_t ld_y,
              void* stream);

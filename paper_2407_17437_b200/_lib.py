@@ -63,6 +63,8 @@ SIGNATURES = {
         [_i32, _p, _p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _i32, _f64, _f64, _p],
     ),
     "smb_optimizer_step": (_i32, [_i32, _p, _p, _p, _i64, _i32, _f64, _f64, _p]),
+    "smb_dense_backward_input": (
+        _i32, [_i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p]),
     "smb_backward_fused_supported": (_i32, [_i32, _p]),
     "smb_backward_fused": (
         _i32,

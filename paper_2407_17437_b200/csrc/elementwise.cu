@@ -630,6 +630,91 @@ extern "C" int smb_relu_backward(int dtype, const void* d_out, int64_t ld_d, con
   });
 }
 
+namespace smb {
+namespace {
+// d_x[j, t] = sum_{i < m, ascending} W[i, j] * d_out[i, t]  (* (mask[j, t] > 0))
+// for an output layer of m <= kDenseTMaxRows rows (DenseLinearLayer.backward,
+// nn.py:241-255, + ReLU.backward of the layer below, nn.py:89-91).  CTA =
+// 256 batch columns x kDenseTRows rows of d_x: every thread keeps its column
+// of d_out (m values) in registers, the CTA's W block sits in shared memory,
+// and each d_x / mask element is touched once, coalesced.
+constexpr int kDenseTMaxRows = 32;
+constexpr int kDenseTRows = 16;
+
+// M: the row count when known at compile time (10 = the classes of every
+// BASELINE config; no predicated-off work), 0 = any m <= kDenseTMaxRows
+template <typename T, bool MASK, int M>
+__global__ void __launch_bounds__(256)
+    dense_t_kernel(const T* __restrict__ w, int64_t ld_w, int m_rt, int64_t k,
+                   const T* __restrict__ d, int64_t ld_d, int64_t n, const T* __restrict__ mask,
+                   int64_t ld_mask, T* __restrict__ dx, int64_t ld_dx) {
+  constexpr int MR = M > 0 ? M : kDenseTMaxRows;  // unrolled row count
+  const int m = M > 0 ? M : m_rt;
+  __shared__ T s_w[MR][kDenseTRows];
+  const int64_t j0 = (int64_t)blockIdx.y * kDenseTRows;
+  const int64_t t = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  for (int e = threadIdx.x; e < m * kDenseTRows; e += 256) {
+    const int i = e / kDenseTRows, jj = e % kDenseTRows;
+    s_w[i][jj] = (j0 + jj < k) ? w[(int64_t)i * ld_w + j0 + jj] : T(0);
+  }
+  pdl_wait();  // d_out / mask are earlier kernels' outputs
+  T dv[MR];
+#pragma unroll
+  for (int i = 0; i < MR; ++i) dv[i] = (i < m && t < n) ? d[(int64_t)i * ld_d + t] : T(0);
+  __syncthreads();
+  if (t >= n) return;
+  const int rows = (int)imin(kDenseTRows, k - j0);
+  // the mask column block first: kDenseTRows independent loads in flight
+  T mk[kDenseTRows];
+#pragma unroll
+  for (int jj = 0; jj < kDenseTRows; ++jj)
+    mk[jj] = (MASK && jj < rows) ? mask[(j0 + jj) * ld_mask + t] : T(1);
+#pragma unroll
+  for (int jj = 0; jj < kDenseTRows; ++jj) {
+    if (jj >= rows) break;
+    T acc = T(0);
+#pragma unroll
+    for (int i = 0; i < MR; ++i)
+      if (M > 0 || i < m) acc = add_rn(acc, mul_rn(s_w[i][jj], dv[i]));
+    if (MASK) acc = mask_np(acc, mk[jj]);
+    dx[(j0 + jj) * ld_dx + t] = acc;
+  }
+}
+}  // namespace
+}  // namespace smb
+
+extern "C" int smb_dense_backward_input(int dtype, const void* w, int64_t ld_w, int64_t m,
+                                        int64_t k, const void* d_out, int64_t ld_d, int64_t n,
+                                        const void* mask, int64_t ld_mask, void* d_x,
+                                        int64_t ld_dx, void* stream) {
+  clear_error();
+  SMB_REQUIRE(m >= 1 && m <= kDenseTMaxRows, "smb_dense_backward_input: needs 1 <= m <= %d",
+              kDenseTMaxRows);
+  SMB_REQUIRE(k >= 0 && n >= 0 && ld_w >= k && ld_d >= n && ld_dx >= n &&
+                  (mask == nullptr || ld_mask >= n),
+              "smb_dense_backward_input: bad shape");
+  if (k == 0 || n == 0) return SMB_OK;
+  SMB_REQUIRE(w && d_out && d_x, "smb_dense_backward_input: null pointer");
+  return dispatch_dtype(dtype, "smb_dense_backward_input", [&](auto tag) {
+    using T = decltype(tag);
+    const dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(k, kDenseTRows));
+    auto go = [&](auto kernel) {
+      launch_k(kernel, grid, dim3(256), 0, as_stream(stream), static_cast<const T*>(w), ld_w,
+               (int)m, k, static_cast<const T*>(d_out), ld_d, n, static_cast<const T*>(mask),
+               ld_mask, static_cast<T*>(d_x), ld_dx);
+    };
+    if (mask && m == 10)
+      go(dense_t_kernel<T, true, 10>);
+    else if (m == 10)
+      go(dense_t_kernel<T, false, 10>);
+    else if (mask)
+      go(dense_t_kernel<T, true, 0>);
+    else
+      go(dense_t_kernel<T, false, 0>);
+    return check_launch("smb_dense_backward_input");
+  });
+}
+
 static int gather_launch(int dtype, const void* src, int64_t n_samples, int64_t features,
                          const int32_t* perm, const int32_t* step_counter, int64_t base,
                          int32_t step_offset, int32_t modulo, int64_t batch, void* dst,

@@ -232,6 +232,10 @@ class SparseLinearLayer:
         _step(self.bias, self.grad_bias, self.velocity_bias, self.optimizer, eta)
 
 
+# output layers up to this many rows take smb_dense_backward_input for W^T d
+DENSE_T_MAX_ROWS = 32
+
+
 class DenseLinearLayer:
     """Dense linear layer; with a mask it is the masked-sparse baseline
     (nn.py:201-264).  Weights are an [n_out, n_in] CUDA tensor."""
@@ -286,7 +290,16 @@ class DenseLinearLayer:
             self.grad = d @ x.T
             if self.mask is not None:
                 self.grad *= self.mask
-            dx = self.weights.T @ d
+            if self.n_out > DENSE_T_MAX_ROWS:
+                dx = self.weights.T @ d
+        if self.n_out <= DENSE_T_MAX_ROWS:
+            # small output layer: the same kernel as the fused step (ascending
+            # rows, separately rounded; numpy BLAS order is unspecified)
+            d = d.contiguous()
+            dx = torch.empty((self.n_in, d.shape[1]), dtype=d.dtype, device=d.device)
+            _lib.call("smb_dense_backward_input", dtype_code(d.dtype), ptr(self.weights),
+                      self.n_in, self.n_out, self.n_in, ptr(d), d.shape[1], d.shape[1], None, 0,
+                      ptr(dx), d.shape[1], stream_ptr())
         self.grad_bias = row_sums(d)
         return dx
 

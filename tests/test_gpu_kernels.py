@@ -438,3 +438,35 @@ def test_sddmm_many_waves_long_rows_bit_exact(oracle, n):
     b = rng.standard_normal((k, n)).astype(np.float32)
     got = host(smb.sddmm(smb.SparsityPattern(m, k, rp, ci), dev(a), dev(b)).values)
     assert bits_equal(got, oracle.sddmm(rp, ci, a, b))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("m,k,n", [(10, 512, 1024), (10, 8192, 100), (1, 7, 3), (32, 300, 257),
+                                   (17, 1000, 1)])
+@pytest.mark.parametrize("with_mask", [True, False])
+def test_dense_backward_input_sequential_sum(dtype, m, k, n, with_mask):
+    """smb_dense_backward_input: W^T d summed over ascending rows with
+    separate roundings (bit-exact against that sequence on the host), times
+    (mask > 0); within BLAS tolerance of numpy's W.T @ d (nn.py:241-255)."""
+    from paper_2407_17437_b200 import _lib
+
+    rng = np.random.default_rng(m * 1000 + n)
+    w = rng.standard_normal((m, k)).astype(dtype)
+    d = rng.standard_normal((m, n)).astype(dtype)
+    mk = rng.standard_normal((k, n)).astype(dtype)
+    want = np.zeros((k, n), dtype)
+    for i in range(m):  # acc = fl(acc + fl(w * d)), ascending i
+        want = (want + (w[i][:, None] * d[i][None, :]).astype(dtype)).astype(dtype)
+    if with_mask:
+        want = want * (mk > 0).astype(dtype)
+    tw, td, tm = dev(w), dev(d), dev(mk)
+    out = torch.full((k, n), float("nan"), dtype=td.dtype, device="cuda")
+    code = _lib.SMB_F32 if dtype == np.float32 else _lib.SMB_F64
+    _lib.call("smb_dense_backward_input", code, tc.ptr(tw), k, m, k, tc.ptr(td), n, n,
+              tc.ptr(tm) if with_mask else None, n if with_mask else 0, tc.ptr(out), n,
+              tc.stream_ptr())
+    torch.cuda.synchronize()
+    got = host(out)
+    assert bits_equal(got, want)
+    ref = (w.astype(np.float64).T @ d.astype(np.float64)) * ((mk > 0) if with_mask else 1)
+    assert rel_err(got, ref) < (1e-5 if dtype == np.float32 else 1e-12)
