@@ -6,7 +6,11 @@ import numpy as np, torch, paper_2407_17437_b200 as smb
 from paper_2407_17437_b200 import engine
 import os
 B = int(os.environ.get("ABL_B", "1024"))
-data = smb.synthetic_dataset(seed=0, n_samples=16384 if B >= 1024 else 4096, features=3072)
+LAYERS = [int(x) for x in os.environ.get("ABL_LAYERS", "3072,1024,512,10").split(",")]
+DENS = float(os.environ.get("ABL_D", "0.01"))
+STEPS = int(os.environ.get("ABL_STEPS", "400"))
+data = smb.synthetic_dataset(seed=0, n_samples=16384 if B >= 1024 else 4096, features=LAYERS[0],
+                             classes=LAYERS[-1])
 ddata = smb.DeviceDataset(data)
 orig = engine.FusedTrainStep._call
 
@@ -17,8 +21,10 @@ def time_with(skip):
         return orig(self, tag, name, *args)
     engine.FusedTrainStep._call = patched
     try:
-        model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=[3072, 1024, 512, 10],
-                                                        density=0.01, batch_size=B, lr=0.01))
+        large = any(a * b >= 2**31 for a, b in zip(LAYERS[:-1], LAYERS[1:]))
+        model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=LAYERS, density=DENS,
+                                                        batch_size=B, lr=0.01),
+                                   large_patterns=large)
         st = smb.FusedTrainStep(model, B, fuse_logits=os.environ.get("ABL_FUSE_LOGITS") == "1")
         st.attach_dataset(ddata)
         st.set_epoch(np.arange(data.Xtrain.shape[1]))
@@ -26,20 +32,22 @@ def time_with(skip):
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        for _ in range(400): st.step(0.01)
+        for _ in range(STEPS): st.step(0.01)
         e.record(); e.synchronize()
-        return s.elapsed_time(e) * 1e3 / 400
+        return s.elapsed_time(e) * 1e3 / STEPS
     finally:
         engine.FusedTrainStep._call = orig
 
 base = time_with(set())
 print(f"baseline {base:.2f} us/step")
-tags = ["gather", "gather_t", "spmm[0]", "spmm[1]", "spmm[2]", "softmax_ce", "spmm_t[2]",
-        "spmm_t[1]", "sddmm_update[0]", "sddmm_update[1]", "sddmm_update[2]"]
+nl = len(LAYERS) - 1
+tags = (["gather", "gather_t"] + [f"spmm[{i}]" for i in range(nl)] + ["softmax_ce"]
+        + [f"spmm_t[{i}]" for i in range(nl - 1, 0, -1)] + [f"dense_t[{nl - 1}]"]
+        + [f"sddmm_update[{i}]" for i in range(nl)] + [f"bias[{i}]" for i in range(nl)])
 for t in tags:
     v = time_with({t})
     print(f"skip {t:18s} {v:8.2f} us/step  (saves {base - v:6.2f})")
-v = time_with({"sddmm_update[0]", "sddmm_update[1]", "sddmm_update[2]"})
+v = time_with({t for t in tags if t.startswith("sddmm")})
 print(f"skip all sddmm       {v:8.2f} us/step  (saves {base - v:6.2f})")
 v = time_with(set(tags))
 print(f"skip everything      {v:8.2f} us/step")

@@ -116,6 +116,41 @@ __global__ void __launch_bounds__(TILE) lab_pipe(const int* row_ptr, const int* 
   if (active) out[p] = acc;
 }
 
+// Direct-load variant: no shared memory; each thread streams its own x row
+// and its d_out row through L1 with 16-byte __ldg, R loads ahead.
+template <int R>
+__global__ void __launch_bounds__(128) lab_ldg(const int* row_of, const int* col_idx, int nnz,
+                                               const float* __restrict__ dy,
+                                               const float* __restrict__ x, int n, float* out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)col_idx[p] * n);
+  const float4* dr = reinterpret_cast<const float4*>(dy + (size_t)row_of[p] * n);
+  const int nv = n / 4;
+  float4 xa[R], da[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    xa[r] = __ldg(xr + r);
+    da[r] = __ldg(dr + r);
+  }
+  float acc = -0.0f;
+  for (int v = 0; v < nv; v += R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float4 a = xa[r], b = da[r];
+      if (v + R + r < nv) {
+        xa[r] = __ldg(xr + v + R + r);
+        da[r] = __ldg(dr + v + R + r);
+      }
+      acc = __fadd_rn(acc, __fmul_rn(b.x, a.x));
+      acc = __fadd_rn(acc, __fmul_rn(b.y, a.y));
+      acc = __fadd_rn(acc, __fmul_rn(b.z, a.z));
+      acc = __fadd_rn(acc, __fmul_rn(b.w, a.w));
+    }
+  }
+  out[p] = acc;
+}
+
 // Register-only chain: how fast can 1024 dependent mul/add steps go per chain
 // with loads fully removed (values synthesised from the index).
 __global__ void lab_chain(int nnz, int n, float* out) {
@@ -222,6 +257,10 @@ int main() {
       P(32, 32, 16);
       P(32, 16, 16);
     }
+    for (int R : {4, 8})
+      printf("  ldg R=%d: %.2f us\n", R,
+             R == 4 ? time_us([&] { lab_ldg<4><<<(nnz + 127) / 128, 128>>>(d_ro, d_ci, nnz, d_dy, d_x, n, d_out); })
+                    : time_us([&] { lab_ldg<8><<<(nnz + 127) / 128, 128>>>(d_ro, d_ci, nnz, d_dy, d_x, n, d_out); }));
     for (int bs : {128})
       printf("  chain-only regs (block %d): %.2f us\n", bs,
              time_us([&] { lab_chain<<<(nnz + bs - 1) / bs, bs>>>(nnz, n, d_out); }));
