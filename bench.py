@@ -371,19 +371,10 @@ def run_ours(args):
     barrier()
     b2b_ms = max_over_ranks(s_ev.elapsed_time(e_ev))
 
-    # ---- per-kernel spans (eager, GPU held while the step is enqueued) ----
-    # kernels serialised (no side-stream overlap) so each span is that
-    # kernel's own duration
-    timer = KernelTimer()
-    step.timer, step.use_graph = timer, False
-    overlap_saved, step.overlap = step.overlap, False
-    nk = min(10, args.steps)
-    for i in range(nk):
-        flush.fill_(float(i))
-        KernelTimer.hold_gpu()
-        step.step(eta)
-    summ = timer.summary()
-    step.timer, step.use_graph, step.overlap = None, True, overlap_saved
+    # ---- per-kernel durations: each launch of one serialised step timed
+    # alone (20 back-to-back launches in a CUDA graph, operands L2-resident
+    # as they are inside the step; KernelTimer.kernel_durations)
+    summ = KernelTimer().kernel_durations(step, eta)
     units = step.units
     best = None
     kernels = {}

@@ -49,6 +49,7 @@ class KernelTimer:
 
     def __init__(self):
         self.records = []  # (tag, start_event, end_event)
+        self.calls = None  # (tag, name, args) while kernel_durations records
 
     @staticmethod
     def hold_gpu(cycles: int = 40_000_000) -> None:
@@ -70,6 +71,51 @@ class KernelTimer:
                 timer.records.append((tag, self.s, self.e))
 
         return _Span()
+
+    def kernel_durations(self, step, eta: float, reps: int = 20, replays: int = 5):
+        """{tag: (launches, total_ms)}: every C-ABI launch of one serialised
+        step (no side-stream overlap; the input slot already filled) is
+        recorded once, then timed alone as `reps` back-to-back launches
+        captured in a CUDA graph and replayed `replays` times between two
+        events, so the average is the kernel's own launch duration with its
+        operands resident in L2 as they are inside the step.  (Event pairs
+        around single launches would not do: stream launches and event nodes
+        round every kernel up to the ~2 us period of the stream's dependency
+        polling -- scripts/launch_gap_lab.cu -- which swamps the 5-25 us
+        kernels of the small configs.)  The stream is the last argument of
+        every recorded call; sddmm_update writes the other value buffer, so
+        repeats recompute the same update."""
+        cur = torch.cuda.current_stream()
+        saved = (step.timer, step.overlap, step.use_graph)
+        self.calls = []
+        step.timer, step.overlap, step.use_graph = self, False, False
+        try:
+            step._launch_forward_backward(eta, True, False)
+        finally:
+            step.timer, step.overlap, step.use_graph = saved
+            self.calls, calls = None, self.calls
+        torch.cuda.synchronize()
+        cs = torch.cuda.Stream(device=step.dev)
+        out = {}
+        for tag, name, args in calls:
+            g = torch.cuda.CUDAGraph()
+            cs.wait_stream(cur)
+            with torch.cuda.stream(cs):
+                _lib.call(name, *args[:-1], stream_ptr())
+            with torch.cuda.graph(g, stream=cs):
+                for _ in range(reps):
+                    _lib.call(name, *args[:-1], stream_ptr())
+            cur.wait_stream(cs)
+            g.replay()
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_.record()
+            for _ in range(replays):
+                g.replay()
+            e_.record()
+            e_.synchronize()
+            c, t = out.get(tag, (0, 0.0))
+            out[tag] = (c + reps * replays, t + s_.elapsed_time(e_))
+        return out
 
     def summary(self):
         """{tag: (count, total_ms)} after synchronising."""
@@ -239,6 +285,10 @@ class FusedTrainStep:
     def _call(self, tag: str, name: str, *args) -> None:
         t = self.timer
         if t is None:
+            _lib.call(name, *args)
+            return
+        if t.calls is not None:  # KernelTimer.kernel_durations records the launch
+            t.calls.append((tag, name, args))
             _lib.call(name, *args)
             return
         with t.span(tag):

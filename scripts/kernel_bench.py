@@ -2,8 +2,11 @@
 uniform pattern (sample_pattern from Rng(seed).stream("pattern")), values and
 X / dY ~ N(0,1) fp32, B in {128, 512, 2048}.  Times forward SpMM, transposed
 SpMM and SDDMM + Nesterov update separately with CUDA events on the
-launching stream, flushing L2 (a 512 MB write) before every timed launch.
-Prints one JSON object per (density, B) with achieved algorithmic GB/s
+launching stream with L2 flushed (a 512 MB write) before every launch: R
+(flush, launch) pairs are captured in one CUDA graph and the same graph of R
+flushes alone is subtracted, so the time is the kernel's own cold-L2 launch
+duration without the ~2 us rounding that single stream launches bracketed by
+events add (scripts/launch_gap_lab.cu).  Prints one JSON object per (density, B) with achieved algorithmic GB/s
 (SURVEY.md 8(d) byte model) and pair rates."""
 import json
 import sys
@@ -17,7 +20,15 @@ import paper_2407_17437_b200 as smb
 from paper_2407_17437_b200 import _lib
 from paper_2407_17437_b200.tensor_core import ptr, stream_ptr
 
-HBM = 6446.6  # GB/s, MEASURED_PEAKS.json hbm_gbs
+def _hbm_gbs():
+    p = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"])
+    except Exception:
+        return 6446.6  # the pool's earlier MEASURED_PEAKS.json value
+
+
+HBM = _hbm_gbs()  # GB/s, MEASURED_PEAKS.json hbm_gbs
 FP32_TFLOPS = 70.83  # FFMA peak, profiles/fp32_peak.json (scripts/fp32_peak.cu)
 L2_GATHER = 12563.7  # GB/s, L2 -> SM row gathers, profiles/l2_peak.json (scripts/l2_peak.cu)
 
@@ -64,18 +75,30 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
             fused_ok = _lib.load().smb_backward_fused_supported(0, pat.handle) == 1
             if fused_ok:
                 kinds.append("bwd_fused")
-            for kind in kinds:
+            for kind in ["flush"] + kinds:
+                launch(kind) if kind != "flush" else None  # kernel attributes outside capture
+                g = torch.cuda.CUDAGraph()
+                cs = torch.cuda.Stream()
+                cs.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.graph(g, stream=cs):
+                    for it in range(iters):
+                        flush.fill_(it)
+                        if kind != "flush":
+                            launch(kind)
+                torch.cuda.current_stream().wait_stream(cs)
+                g.replay()
                 times = []
-                for it in range(iters + 2):
-                    flush.fill_(it)
+                for _ in range(3):
                     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     s.record()
-                    launch(kind)
+                    g.replay()
                     e.record()
                     e.synchronize()
-                    if it >= 2:
-                        times.append(s.elapsed_time(e) * 1e3)
+                    times.append(s.elapsed_time(e) * 1e3 / iters)
                 res[kind] = float(np.median(times))
+            t_flush = res.pop("flush")
+            for kind in kinds:
+                res[kind] -= t_flush
             bs = bytes_model(n, n, nnz, B)
             rec = {"density": d, "nnz": nnz, "B": B}
             if fused_ok:

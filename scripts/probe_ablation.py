@@ -40,6 +40,8 @@ def time_with(skip):
 
 base = time_with(set())
 print(f"baseline {base:.2f} us/step")
+if os.environ.get("ABL_ONLY_BASE") == "1":
+    sys.exit(0)
 nl = len(LAYERS) - 1
 tags = (["gather", "gather_t"] + [f"spmm[{i}]" for i in range(nl)] + ["softmax_ce"]
         + [f"spmm_t[{i}]" for i in range(nl - 1, 0, -1)] + [f"dense_t[{nl - 1}]"]

@@ -36,11 +36,11 @@ __device__ __forceinline__ void waitg() {
 }
 
 // TILE nonzeros per CTA (one chain per thread), CH columns per chunk, ST stages
-template <int TILE, int CH, int ST, int MODE>
+template <int TILE, int CH, int ST, int MODE, int SD = 4>
 __global__ void __launch_bounds__(TILE) lab_pipe(const int* row_ptr, const int* col_idx,
                                                  const int* row_of, int nnz, const float* dy,
                                                  const float* x, int n, float* out) {
-  constexpr int VPR = CH / 4, LDS = CH + 4, SLOTS = TILE / 4;
+  constexpr int VPR = CH / 4, LDS = CH + 4, SLOTS = TILE / SD;
   constexpr int STAGE = (TILE + SLOTS) * LDS;
   extern __shared__ __align__(16) float sm[];
   const int tid = threadIdx.x;
@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(TILE) lab_pipe(const int* row_ptr, const int* 
     commit();
   }
   float acc = -0.0f;
+  float4 a4 = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int ch = 0; ch < nch; ++ch) {
     waitg<ST - 2>();
     __syncthreads();
@@ -100,6 +101,16 @@ __global__ void __launch_bounds__(TILE) lab_pipe(const int* row_ptr, const int* 
     const float* dr = s + (TILE + slot) * LDS;
     if (MODE == 1) {
       acc = __fadd_rn(acc, xr[0] * dr[0]);
+    } else if (MODE == 3) {  // tolerance experiment: 4 FFMA accumulators (t mod 4)
+#pragma unroll
+      for (int u = 0; u < VPR; ++u) {
+        const float4 a = *reinterpret_cast<const float4*>(xr + u * 4);
+        const float4 b = *reinterpret_cast<const float4*>(dr + u * 4);
+        a4.x = fmaf(b.x, a.x, a4.x);
+        a4.y = fmaf(b.y, a.y, a4.y);
+        a4.z = fmaf(b.z, a.z, a4.z);
+        a4.w = fmaf(b.w, a.w, a4.w);
+      }
     } else {
 #pragma unroll
       for (int u = 0; u < VPR; ++u) {
@@ -113,6 +124,97 @@ __global__ void __launch_bounds__(TILE) lab_pipe(const int* row_ptr, const int* 
     }
   }
   waitg<0>();
+  if (MODE == 3) acc = (a4.x + a4.y) + (a4.z + a4.w);
+  if (active) out[p] = acc;
+}
+
+// Register-staged variant: 16-byte LDG into registers NR chunks ahead, then
+// STS into a 2-stage smem ring (no LDGSTS).  MODE 0 full, 1 loads only.
+template <int TILE, int CH, int NR, int MODE, int SD>
+__global__ void __launch_bounds__(TILE) lab_reg(const int* row_of, const int* col_idx, int nnz,
+                                                const float* __restrict__ dy,
+                                                const float* __restrict__ x, int n, float* out) {
+  constexpr int VPR = CH / 4, LDS = CH + 4, SLOTS = TILE / SD;
+  constexpr int STAGE = (TILE + SLOTS) * LDS;
+  constexpr int DC = (SLOTS * VPR + TILE - 1) / TILE;
+  extern __shared__ __align__(16) float sm[];
+  const int tid = threadIdx.x;
+  const int p0 = blockIdx.x * TILE, p = p0 + tid;
+  const bool active = p < nnz;
+  const int pl = min(p, nnz - 1);
+  const int row = row_of[pl];
+  const int r0 = row_of[p0];
+  const int slot = row - r0;
+  const int rlast = row_of[min(p0 + TILE, nnz) - 1];
+  const int nst = rlast - r0 + 1;
+  const int v = tid % VPR;
+  const float4* xs[VPR];
+  int xd[VPR];
+#pragma unroll
+  for (int k = 0; k < VPR; ++k) {
+    const int r = tid / VPR + k * (TILE / VPR);
+    xs[k] = reinterpret_cast<const float4*>(x + (size_t)col_idx[min(p0 + r, nnz - 1)] * n + v * 4);
+    xd[k] = r * LDS + v * 4;
+  }
+  const float4* ds[DC];
+  int dd[DC];
+  bool dok[DC];
+#pragma unroll
+  for (int c = 0; c < DC; ++c) {
+    const int e = tid + c * TILE;
+    dok[c] = e < nst * VPR;
+    ds[c] = reinterpret_cast<const float4*>(dy + (size_t)(r0 + (dok[c] ? e / VPR : 0)) * n + v * 4);
+    dd[c] = (TILE + e / VPR) * LDS + v * 4;
+  }
+  const int nch = n / CH;
+  float4 rx[NR][VPR], rd[NR][DC];
+  auto load = [&](int ch, float4(&ax)[VPR], float4(&ad)[DC]) {
+    const int q = ch * (CH / 4);
+#pragma unroll
+    for (int k = 0; k < VPR; ++k) ax[k] = __ldcg(xs[k] + q);
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+      if (dok[c]) ad[c] = __ldcg(ds[c] + q);
+  };
+  auto store = [&](int stg, const float4(&ax)[VPR], const float4(&ad)[DC]) {
+    float* st = sm + stg * STAGE;
+#pragma unroll
+    for (int k = 0; k < VPR; ++k) *reinterpret_cast<float4*>(st + xd[k]) = ax[k];
+#pragma unroll
+    for (int c = 0; c < DC; ++c)
+      if (dok[c]) *reinterpret_cast<float4*>(st + dd[c]) = ad[c];
+  };
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    if (r < nch) load(r, rx[r], rd[r]);
+  float acc = -0.0f;
+  for (int base = 0; base < nch; base += NR) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int ch = base + r;
+      if (ch < nch) {
+        store(ch & 1, rx[r], rd[r]);
+        if (ch + NR < nch) load(ch + NR, rx[r], rd[r]);
+        __syncthreads();
+        const float* s = sm + (ch & 1) * STAGE;
+        const float* xr = s + tid * LDS;
+        const float* dr = s + (TILE + slot) * LDS;
+        if (MODE == 1) {
+          acc = __fadd_rn(acc, xr[0] * dr[0]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < VPR; ++u) {
+            const float4 a = *reinterpret_cast<const float4*>(xr + u * 4);
+            const float4 b = *reinterpret_cast<const float4*>(dr + u * 4);
+            acc = __fadd_rn(acc, __fmul_rn(b.x, a.x));
+            acc = __fadd_rn(acc, __fmul_rn(b.y, a.y));
+            acc = __fadd_rn(acc, __fmul_rn(b.z, a.z));
+            acc = __fadd_rn(acc, __fmul_rn(b.w, a.w));
+          }
+        }
+      }
+    }
+  }
   if (active) out[p] = acc;
 }
 
@@ -192,15 +294,25 @@ float time_us(F f, int reps = 50) {
   return ms * 1e3f / reps;
 }
 
-template <int TILE, int CH, int ST, int MODE>
+template <int TILE, int CH, int ST, int MODE, int SD = 4>
 float run_pipe(const Shape& s, int nnz, const int* rp, const int* ci, const int* ro, const float* dy,
                const float* x, int n, float* out) {
-  constexpr int SLOTS = TILE / 4;
+  constexpr int SLOTS = TILE / SD;
   const size_t bytes = (size_t)ST * (TILE + SLOTS) * (CH + 4) * 4;
-  auto k = lab_pipe<TILE, CH, ST, MODE>;
+  auto k = lab_pipe<TILE, CH, ST, MODE, SD>;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   const int grid = (nnz + TILE - 1) / TILE;
   return time_us([&] { k<<<grid, TILE, bytes>>>(rp, ci, ro, nnz, dy, x, n, out); });
+}
+
+template <int TILE, int CH, int NR, int MODE, int SD>
+float run_reg(int nnz, const int* ro, const int* ci, const float* dy, const float* x, int n, float* out) {
+  constexpr int SLOTS = TILE / SD;
+  const size_t bytes = (size_t)2 * (TILE + SLOTS) * (CH + 4) * 4;
+  auto k = lab_reg<TILE, CH, NR, MODE, SD>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  const int grid = (nnz + TILE - 1) / TILE;
+  return time_us([&] { k<<<grid, TILE, bytes>>>(ro, ci, nnz, dy, x, n, out); });
 }
 
 int main() {
@@ -244,6 +356,43 @@ int main() {
          run_pipe<T, C, S, 0>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out),              \
          run_pipe<T, C, S, 1>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out),              \
          run_pipe<T, C, S, 2>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out))
+#define Q(T, C, S, D)                                                                       \
+  printf("  pipe<%d,%d,%d> SD=%d: full %.2f  split4 %.2f loads %.2f  chain %.2f us\n", T, C, S, D, \
+         run_pipe<T, C, S, 0, D>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out),              \
+         run_pipe<T, C, S, 3, D>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out),              \
+         run_pipe<T, C, S, 1, D>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out),              \
+         run_pipe<T, C, S, 2, D>(s, nnz, d_rp, d_ci, d_ro, d_dy, d_x, n, d_out))
+#define R(T, C, N, D)                                                                  \
+  printf("  reg<%d,%d,NR=%d> SD=%d: full %.2f  loads %.2f us\n", T, C, N, D,                \
+         run_reg<T, C, N, 0, D>(nnz, d_ro, d_ci, d_dy, d_x, n, d_out),                      \
+         run_reg<T, C, N, 1, D>(nnz, d_ro, d_ci, d_dy, d_x, n, d_out))
+    if (s.m == 8192) R(64, 32, 3, 8);
+    if (s.m == 10 || s.m == 512) {
+      Q(32, 32, 8, 4);
+      Q(64, 32, 4, 4);
+      Q(64, 64, 4, 4);
+      continue;
+    }
+    if (s.m == 8192) {
+      Q(128, 32, 2, 4);
+      continue;
+    }
+    if (s.m == 1024) {
+      Q(64, 32, 4, 4);
+      Q(64, 32, 4, 8);
+      Q(64, 32, 5, 8);
+      Q(64, 32, 6, 8);
+      Q(64, 32, 7, 8);
+      Q(64, 32, 6, 4);
+      Q(64, 16, 12, 8);
+      Q(64, 16, 14, 8);
+      Q(32, 32, 6, 8);
+      Q(32, 32, 4, 8);
+      Q(96, 32, 4, 8);
+      Q(96, 32, 5, 8);
+      Q(128, 32, 3, 8);
+      continue;
+    }
     P(128, 64, 2);
     P(128, 32, 2);
     if (s.m <= 1024) {

@@ -37,6 +37,28 @@ def max_rel(model, ref):
     return max(rel_err(a, b) for (_, a), (_, b) in zip(params_host(model), oracle_params(ref)))
 
 
+def test_kernel_durations_time_every_sparse_launch():
+    """bench.py's per-kernel durations (KernelTimer.kernel_durations): one
+    entry per C-ABI launch of the serialised step, each a positive graph-timed
+    duration, and the values the repeats write stay those of one update."""
+    chain, B = [3072, 1024, 512, 10], 256
+    data = smb.synthetic_dataset(seed=2, n_samples=B * 4, features=chain[0])
+    model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=chain, density=0.01, seed=4,
+                                                    batch_size=B))
+    st = smb.FusedTrainStep(model, B)
+    st.attach_dataset(smb.DeviceDataset(data))
+    st.set_epoch(np.arange(B * 4))
+    for _ in range(2):
+        st.step(0.02)
+    from paper_2407_17437_b200.engine import KernelTimer
+    out = KernelTimer().kernel_durations(st, 0.02, reps=4, replays=2)
+    for tag in ("spmm[0]", "spmm[1]", "spmm[2]", "softmax_ce", "spmm_t[2]", "spmm_t[1]",
+                "sddmm_update[0]", "sddmm_update[1]", "sddmm_update[2]"):
+        cnt, ms = out[tag]
+        assert cnt == 8 and 0.0 < ms / cnt < 5.0, (tag, cnt, ms)
+    assert st.timer is None and st.use_graph and st.overlap  # restored
+
+
 @pytest.mark.parametrize("chain,density,seed", [
     ([3072, 1024, 512, 10], 0.01, 3),
     ([3072, 1024, 512, 10], 0.1, 1),      # last layer saturates -> Dense
