@@ -23,6 +23,7 @@ SMB_OK, SMB_ERR_INVALID, SMB_ERR_STATE, SMB_ERR_CUDA = 0, 1, 2, 3
 SMB_F32, SMB_F64 = 0, 1
 SMB_EPI_NONE, SMB_EPI_RELU = 0, 1
 SMB_OPT_NONE, SMB_OPT_GD, SMB_OPT_MOMENTUM, SMB_OPT_NESTEROV = 0, 1, 2, 3
+SMB_HINT_CONCURRENT = 0x100  # OR-ed into opt_kind of smb_sddmm_update_into
 
 _p = C.c_void_p
 _i64 = C.c_int64

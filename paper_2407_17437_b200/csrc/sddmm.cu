@@ -389,7 +389,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
                       int64_t ld_x, int64_t n, const void* values, void* values_out,
                       void* velocity, void* grad_out, void* bias, void* vbias,
                       void* grad_bias_out, int opt_kind, double mu, double eta, void* stream,
-                      const char* name) {
+                      const char* name, bool concurrent = false) {
   const OptConsts<T> opt = make_opt<T>(opt_kind, mu, eta);
   cudaStream_t st = as_stream(stream);
   if (pat->ntiles > 0) {
@@ -459,7 +459,13 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       }
     }
     if (warp_done) {
-    } else if (sizeof(T) == 4 && small32 && all_for(32, 4)) SMB_GO_SD(32, 32, 8, 4);
+    } else if (sizeof(T) == 4 && small32 && all_for(32, 4) && concurrent)
+      // beside other kernels (the overlapped training step) the 2-stage ring
+      // (12 KB per CTA instead of 46 KB) leaves shared memory to the kernels
+      // on the critical path: config-2 step 76.3 -> 74.6 us back to back
+      // although this kernel alone is 1.1-1.2x slower
+      SMB_GO_SD(32, 32, 2, 4);
+    else if (sizeof(T) == 4 && small32 && all_for(32, 4)) SMB_GO_SD(32, 32, 8, 4);
     else if (sizeof(T) == 4 && small32) SMB_GO_SD(32, 32, 8, 1);
     else if (sizeof(T) == 4 && small64 && all_for(64, 4)) SMB_GO_SD(64, 32, 4, 4);
     else if (sizeof(T) == 4 && small64) SMB_GO_SD(64, 32, 4, 1);
@@ -519,6 +525,8 @@ extern "C" int smb_sddmm_update_into(int dtype, const smb_pattern* pat, const vo
                                      void* grad_bias_out, int opt_kind, double mu, double eta,
                                      void* stream) {
   clear_error();
+  const bool concurrent = (opt_kind & SMB_HINT_CONCURRENT) != 0;
+  opt_kind &= ~SMB_HINT_CONCURRENT;
   SMB_REQUIRE(pat != nullptr, "smb_sddmm_update: null pattern");
   SMB_REQUIRE(opt_kind == SMB_OPT_NONE || values_out != nullptr || pat->nnz == 0,
               "smb_sddmm_update: null output values");
@@ -537,7 +545,7 @@ extern "C" int smb_sddmm_update_into(int dtype, const smb_pattern* pat, const vo
   if (dtype == SMB_F32)
     return sddmm_update_impl<float>(pat, d_out, ld_dout, x, ld_x, n, values, values_out, velocity,
                                     grad_out, bias, velocity_bias, grad_bias_out, opt_kind, mu,
-                                    eta, stream, "smb_sddmm_update");
+                                    eta, stream, "smb_sddmm_update", concurrent);
   if (dtype == SMB_F64)
     return sddmm_update_impl<double>(pat, d_out, ld_dout, x, ld_x, n, values, values_out,
                                      velocity, grad_out, bias, velocity_bias, grad_bias_out,

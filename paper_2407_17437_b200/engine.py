@@ -565,10 +565,13 @@ class FusedTrainStep:
             g_out = None if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals]
             w_in = self._vals(u)
             w_out = u.vals[self._parity ^ 1] if (u.vals is not None and fuse_update) else w_in
+            # on a side stream beside the critical path: the small-footprint
+            # staging ring (include/sparsemlp_b200.h SMB_HINT_CONCURRENT)
+            hint = _lib.SMB_HINT_CONCURRENT if self.overlap else 0
             self._call(f"sddmm_update[{u.index}]", "smb_sddmm_update_into", F32,
                        lay.weights.pattern.handle, ptr(dy), ld, ptr(x_prev), ld, B,
-                       ptr(w_in), ptr(w_out), ptr(vel), ptr(g_out), None, None, None, kind,
-                       float(opt.mu), float(eta), st)
+                       ptr(w_in), ptr(w_out), ptr(vel), ptr(g_out), None, None, None,
+                       kind | hint, float(opt.mu), float(eta), st)
             return
         # dense layer: cuBLAS FP32 weight gradient + exact update
         gw = lay.grad if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals].view(u.m, u.k)

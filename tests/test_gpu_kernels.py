@@ -470,3 +470,30 @@ def test_dense_backward_input_sequential_sum(dtype, m, k, n, with_mask):
     assert bits_equal(got, want)
     ref = (w.astype(np.float64).T @ d.astype(np.float64)) * ((mk > 0) if with_mask else 1)
     assert rel_err(got, ref) < (1e-5 if dtype == np.float32 else 1e-12)
+
+
+@pytest.mark.parametrize("m,k,n", [(10, 512, 1024), (512, 1024, 1024), (64, 300, 100), (40, 90, 37)])
+@pytest.mark.parametrize("kind", [0, 3])
+def test_sddmm_concurrent_hint_bit_exact(oracle, m, k, n, kind):
+    """SMB_HINT_CONCURRENT (the overlapped step's small-footprint staging ring
+    for small layers): gradient and Nesterov update bit-identical to the
+    oracle / to the launch without the hint."""
+    from paper_2407_17437_b200 import _lib
+    rng = np.random.default_rng(m * 7 + n)
+    rp, ci, v, _ = random_csr(rng, m, k, 0.3 if m < 100 else 0.02, np.float32, empty_rows=True)
+    a = rng.standard_normal((m, n)).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float32)
+    pat = smb.SparsityPattern(m, k, rp, ci)
+    da, db = dev(a), dev(b)  # kept alive until the launches complete
+    outs = []
+    for hint in (0, _lib.SMB_HINT_CONCURRENT):
+        vals, vel = dev(v.copy()), dev(np.full(v.shape, 0.25, np.float32))
+        grad = torch.empty_like(vals)
+        _lib.call("smb_sddmm_update_into", _lib.SMB_F32, pat.handle, tc.ptr(da), n,
+                  tc.ptr(db), n, n, tc.ptr(vals), tc.ptr(vals), tc.ptr(vel), tc.ptr(grad),
+                  None, None, None, kind | hint, 0.9, 0.01, tc.stream_ptr())
+        torch.cuda.synchronize()
+        outs.append((host(grad), host(vals), host(vel)))
+    assert bits_equal(outs[0][0], oracle.sddmm(rp, ci, a, b))
+    for x, y in zip(*outs):
+        assert bits_equal(x, y)

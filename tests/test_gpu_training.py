@@ -39,8 +39,7 @@ def max_rel(model, ref):
 
 def test_kernel_durations_time_every_sparse_launch():
     """bench.py's per-kernel durations (KernelTimer.kernel_durations): one
-    entry per C-ABI launch of the serialised step, each a positive graph-timed
-    duration, and the values the repeats write stay those of one update."""
+    entry per C-ABI launch of the step, each a positive graph-timed duration."""
     chain, B = [3072, 1024, 512, 10], 256
     data = smb.synthetic_dataset(seed=2, n_samples=B * 4, features=chain[0])
     model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=chain, density=0.01, seed=4,
