@@ -371,7 +371,7 @@ def run_ours(args):
     barrier()
     b2b_ms = max_over_ranks(s_ev.elapsed_time(e_ev))
 
-    # ---- per-kernel durations: each launch of one serialised step timed
+    # ---- per-kernel durations: each launch of the step timed
     # alone (20 back-to-back launches in a CUDA graph, operands L2-resident
     # as they are inside the step; KernelTimer.kernel_durations)
     summ = KernelTimer().kernel_durations(step, eta)

@@ -293,10 +293,60 @@ __device__ T pairwise_sum(const T* a, int64_t n) {
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int warp_pairwise_leaves(int n) { return n / 64 + 2; }
 
+// n = 128 * L, L a power of two >= 2: every leaf holds exactly 128 elements
+// and numpy's split (n2 = n / 2 rounded down to a multiple of 8) halves the
+// leaf range at every level, so the combine is a balanced tree over the L
+// leaves.  Four leaves per round (8 lanes per leaf, lane j = accumulator j),
+// the next round's 16 loads per lane issued before this round is summed;
+// the tree runs level by level in shared memory with all lanes.
+template <typename T>
+__device__ T warp_pairwise_sum_pow2(const T* a, int L, T* leaf_buf) {
+  const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
+  const int rounds = (L + 3) >> 2;
+  T v[16], w[16];
+  auto load = [&](T(&x)[16], int leaf) {
+    const T* p = a + leaf * 128 + j;
+    const bool ok = leaf < L;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = ok ? p[8 * k] : T(0);
+  };
+  load(v, grp);
+  for (int r = 0; r < rounds; ++r) {
+    if (r + 1 < rounds) load(w, 4 * (r + 1) + grp);
+    T acc = v[0];  // accumulator j of the leaf: a[j], += a[8k + j] in k order
+#pragma unroll
+    for (int k = 1; k < 16; ++k) acc = add_rn(acc, v[k]);
+    // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
+    T t = __shfl_down_sync(0xffffffffu, acc, 1);
+    if ((j & 1) == 0) acc = add_rn(acc, t);
+    t = __shfl_down_sync(0xffffffffu, acc, 2);
+    if ((j & 3) == 0) acc = add_rn(acc, t);
+    t = __shfl_down_sync(0xffffffffu, acc, 4);
+    if (j == 0 && 4 * r + grp < L) leaf_buf[4 * r + grp] = add_rn(acc, t);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = w[k];
+  }
+  __syncwarp();
+  for (int h = L >> 1; h >= 1; h >>= 1) {  // level: h sums of adjacent pairs
+    T x0 = T(0), x1 = T(0);
+    if (lane < h) x0 = add_rn(leaf_buf[2 * lane], leaf_buf[2 * lane + 1]);
+    if (lane + 32 < h) x1 = add_rn(leaf_buf[2 * lane + 64], leaf_buf[2 * lane + 65]);
+    __syncwarp();
+    if (lane < h) leaf_buf[lane] = x0;
+    if (lane + 32 < h) leaf_buf[lane + 32] = x1;
+    __syncwarp();
+  }
+  const T ret = leaf_buf[0];
+  __syncwarp();
+  return ret;
+}
+
 template <typename T>
 __device__ T warp_pairwise_sum(const T* a, int n, T* leaf_buf) {
   const int lane = threadIdx.x & 31, grp = lane >> 3, j = lane & 7;
   if (n <= 0) return T(0);
+  if (n >= 256 && n <= 16384 && (n & 127) == 0 && ((n >> 7) & ((n >> 7) - 1)) == 0)
+    return warp_pairwise_sum_pow2(a, n >> 7, leaf_buf);
   int st_off[32], st_len[32];
   int sp = 0, leaf = 0;
   int cur_off = 0, cur_len = n;

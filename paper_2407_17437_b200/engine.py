@@ -73,9 +73,9 @@ class KernelTimer:
         return _Span()
 
     def kernel_durations(self, step, eta: float, reps: int = 20, replays: int = 5):
-        """{tag: (launches, total_ms)}: every C-ABI launch of one serialised
-        step (no side-stream overlap; the input slot already filled) is
-        recorded once, then timed alone as `reps` back-to-back launches
+        """{tag: (launches, total_ms)}: every C-ABI launch of one step (the
+        kernels of the overlapped step itself; the input slot already filled)
+        is recorded once from an eager run, then timed alone as `reps` back-to-back launches
         captured in a CUDA graph and replayed `replays` times between two
         events, so the average is the kernel's own launch duration with its
         operands resident in L2 as they are inside the step.  (Event pairs
@@ -86,13 +86,13 @@ class KernelTimer:
         every recorded call; sddmm_update writes the other value buffer, so
         repeats recompute the same update."""
         cur = torch.cuda.current_stream()
-        saved = (step.timer, step.overlap, step.use_graph)
+        saved = (step.timer, step.use_graph)
         self.calls = []
-        step.timer, step.overlap, step.use_graph = self, False, False
+        step.timer, step.use_graph = self, False
         try:
             step._launch_forward_backward(eta, True, False)
         finally:
-            step.timer, step.overlap, step.use_graph = saved
+            step.timer, step.use_graph = saved
             self.calls, calls = None, self.calls
         torch.cuda.synchronize()
         cs = torch.cuda.Stream(device=step.dev)

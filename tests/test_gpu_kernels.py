@@ -177,7 +177,9 @@ def test_csc_index_is_row_sorted(oracle):
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_row_sums_numpy_pairwise_order(dtype):
     rng = np.random.default_rng(12)
-    for n in [1, 7, 8, 9, 100, 128, 129, 257, 1000, 1024, 4096]:
+    # (256 ... 16384 = 128 * 2^p: the balanced-tree fast path)
+    for n in [1, 7, 8, 9, 100, 128, 129, 256, 257, 384, 512, 1000, 1024, 2048, 4096, 8192, 16384,
+              16512]:
         a = (rng.standard_normal((33, n)) * np.exp(3 * rng.standard_normal((33, n)))).astype(dtype)
         assert bits_equal(smb.row_sums(a), a.sum(axis=1))
 
