@@ -141,6 +141,11 @@ __global__ void __launch_bounds__(TILE)
   const unsigned sbase = smem_u32(smem);
   constexpr unsigned kStageBytes = (unsigned)(C::stage_elems * sizeof(T));
   pdl_wait();  // d_out / x are earlier kernels' outputs
+  // the update's operands, loaded now so they arrive during the chain instead
+  // of costing one more memory round trip after it
+  const bool upd = active && opt.kind != SMB_OPT_NONE;
+  T w_pre = upd ? values[p] : T(0);
+  T v_pre = (upd && velocity) ? velocity[p] : T(0);
 
   // full chunks (copied without bounds when VEC) run a lean main loop; a
   // ragged last chunk (n % CH != 0) is copied and summed after it
@@ -224,14 +229,12 @@ __global__ void __launch_bounds__(TILE)
   if (!active) return;
   const T g = (n == 0) ? T(0) : acc;  // tensor_core.py:283-284: zero batch -> zeros
   if (grad_out) grad_out[p] = g;
-  if (opt.kind != SMB_OPT_NONE) {
-    // read the pre-update value from `values`, write the result to
+  if (upd) {
+    // pre-update value read from `values` (above), the result written to
     // `values_out` (== values for the in-place update)
-    T w = values[p];
-    T v = velocity ? velocity[p] : T(0);
-    apply_update(opt, g, &w, &v);
-    values_out[p] = w;
-    if (velocity) velocity[p] = v;
+    apply_update(opt, g, &w_pre, &v_pre);
+    values_out[p] = w_pre;
+    if (velocity) velocity[p] = v_pre;
   }
 }
 
@@ -304,6 +307,9 @@ __global__ void __launch_bounds__(128)
   const unsigned ddst = (unsigned)(((32 + lane / VPR) * LDS + (lane % VPR) * VW) * sizeof(T));
   const unsigned sbase = smem_u32(wsm);
   pdl_wait();  // d_out / x are earlier kernels' outputs
+  const bool upd = active && opt.kind != SMB_OPT_NONE;  // update operands loaded early
+  T w_pre = upd ? values[p] : T(0);
+  T v_pre = (upd && velocity) ? velocity[p] : T(0);
   auto issue = [&](int ch) {
     const unsigned st = sbase + (unsigned)(ch % S) * kStageBytes;
     const int t0 = ch * CH;
@@ -369,12 +375,10 @@ __global__ void __launch_bounds__(128)
   if (!active) return;
   const T g = (n == 0) ? T(0) : acc;  // tensor_core.py:283-284: zero batch -> zeros
   if (grad_out) grad_out[p] = g;
-  if (opt.kind != SMB_OPT_NONE) {
-    T w = values[p];
-    T v = velocity ? velocity[p] : T(0);
-    apply_update(opt, g, &w, &v);
-    values_out[p] = w;
-    if (velocity) velocity[p] = v;
+  if (upd) {
+    apply_update(opt, g, &w_pre, &v_pre);
+    values_out[p] = w_pre;
+    if (velocity) velocity[p] = v_pre;
   }
 }
 
@@ -449,17 +453,25 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     // and 512x1024 14.4 -> 8.3 us with 32-tiles, 1024x3072 22.6 -> 16.5 us
     // with 64-tiles).
     const int64_t small_cap = 4 * 148;
-    const bool small32 = variant == 0 && ceil_div(pat->nnz, 32) <= small_cap;
-    const bool small64 = variant == 0 && !small32 && ceil_div(pat->nnz, 64) <= small_cap;
+    const bool small32 = (variant == 0 || variant == 4) && ceil_div(pat->nnz, 32) <= small_cap;
+    const bool small64 = (variant == 0 || variant == 4) && !small32 &&
+                         ceil_div(pat->nnz, 64) <= small_cap;
+    // One wave of 32-nonzero tiles with 4-stage rings (23 KB, up to 9 CTAs
+    // per SM) beyond that: config-2 layer 0 (1024 x 3072) 16.3 -> 15.0 us
+    // against 64-nonzero tiles (graph-timed, scripts/sddmm_lab.cu)
+    // (SMB_SDDMM_VARIANT=4: the 64-nonzero tiles instead, for comparison)
+    const bool mid32 = variant == 0 && ceil_div(pat->nnz, 32) > small_cap &&
+                       ceil_div(pat->nnz, 32) <= 9 * 148 && all_for(32, 4);
     bool warp_done = false;
     if constexpr (sizeof(T) == 4) {
-      if (!small32 && !small64 && (warp_kernel || (vec && variant == 3))) {
+      if (!small32 && !small64 && !mid32 && (warp_kernel || (vec && variant == 3))) {
         go(sddmm_warp_kernel<T, 32, 2>, 128, SddmmWarpCfg<T, 32, 2>::smem_bytes);
         warp_done = true;
       }
     }
     if (warp_done) {
-    } else if (sizeof(T) == 4 && small32 && all_for(32, 4) && concurrent)
+    } else if (sizeof(T) == 4 && mid32) SMB_GO_SD(32, 32, 4, 4);
+    else if (sizeof(T) == 4 && small32 && all_for(32, 4) && concurrent)
       // beside other kernels (the overlapped training step) the 2-stage ring
       // (12 KB per CTA instead of 46 KB) leaves shared memory to the kernels
       // on the critical path: config-2 step 76.3 -> 74.6 us back to back
@@ -467,7 +479,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       SMB_GO_SD(32, 32, 2, 4);
     else if (sizeof(T) == 4 && small32 && all_for(32, 4)) SMB_GO_SD(32, 32, 8, 4);
     else if (sizeof(T) == 4 && small32) SMB_GO_SD(32, 32, 8, 1);
-    else if (sizeof(T) == 4 && small64 && all_for(64, 4)) SMB_GO_SD(64, 32, 4, 4);
+    else if (sizeof(T) == 4 && small64 && !mid32 && all_for(64, 4)) SMB_GO_SD(64, 32, 4, 4);
     else if (sizeof(T) == 4 && small64) SMB_GO_SD(64, 32, 4, 1);
     else if (sizeof(T) == 4 && variant == 1) SMB_GO_SD(512, 32, 2, 4);
     else if (sizeof(T) == 4 && variant == 2) SMB_GO_SD(128, 16, 8, 4);
