@@ -90,7 +90,7 @@ class KernelTimer:
         self.calls = []
         step.timer, step.use_graph = self, False
         try:
-            step._launch_forward_backward(eta, True, False)
+            step._launch_forward_backward(eta, not step.dp, False)
         finally:
             step.timer, step.use_graph = saved
             self.calls, calls = None, self.calls
