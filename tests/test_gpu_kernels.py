@@ -499,3 +499,25 @@ def test_sddmm_concurrent_hint_bit_exact(oracle, m, k, n, kind):
     assert bits_equal(outs[0][0], oracle.sddmm(rp, ci, a, b))
     for x, y in zip(*outs):
         assert bits_equal(x, y)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("features,batch", [(3072, 1024), (130, 37), (100, 64), (7, 5), (256, 1)])
+def test_gather_columns_equals_host_gather(dtype, features, batch):
+    """smb_gather_columns: dst[f, j] = src[perm[base + j], f] (the host gather
+    Xtrain[:, batch] of train.py:390-396), ragged feature / batch tails."""
+    from paper_2407_17437_b200 import _lib
+    rng = np.random.default_rng(features + batch)
+    n = 3 * batch + 5
+    src = rng.standard_normal((n, features)).astype(dtype)
+    perm = rng.permutation(n).astype(np.int32)
+    base = batch + 2
+    d_src, d_perm = dev(src), dev(perm)
+    ld = batch + 3
+    out = torch.full((features, ld), -7.0, dtype=d_src.dtype, device="cuda")
+    code = _lib.SMB_F32 if dtype == np.float32 else _lib.SMB_F64
+    _lib.call("smb_gather_columns", code, tc.ptr(d_src), n, features, tc.ptr(d_perm), None, base,
+              batch, tc.ptr(out), ld, tc.stream_ptr())
+    got = host(out)
+    assert bits_equal(got[:, :batch], src[perm[base:base + batch]].T)
+    assert np.all(got[:, batch:] == -7.0)
