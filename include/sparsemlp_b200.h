@@ -131,6 +131,22 @@ SMB_API int smb_spmm_t(int dtype, const smb_pattern* pattern, const void* values
                int64_t ld_dense, int64_t n, const void* mask, int64_t ld_mask, void* out,
                int64_t ld_out, void* stream);
 
+/* smb_spmm_t with the values already in CSC slot order (values_csc[q] =
+ * values[perm[q]], see smb_values_to_csc): the same sums bit for bit without
+ * the per-nonzero indirection through perm.  The training step keeps such a
+ * copy next to each layer's value buffer (refreshed after every update on
+ * the update's own stream): config-4 hidden layer 149 -> 132 us, config-5
+ * 608 -> 503 us (scripts/probe_spmm_t_cost.py). */
+SMB_API int smb_spmm_t_csc(int dtype, const smb_pattern* pattern, const void* values_csc,
+                           const void* dense, int64_t ld_dense, int64_t n, const void* mask,
+                           int64_t ld_mask, void* out, int64_t ld_out, void* stream);
+
+/* values_csc[q] = values[perm[q]] for the nnz CSC slots q of the pattern
+ * (the CSR -> CSC permutation of a value array; no reference counterpart:
+ * the reference's spmm_t_kernel indexes values in CSR order). */
+SMB_API int smb_values_to_csc(int dtype, const smb_pattern* pattern, const void* values,
+                              void* values_csc, void* stream);
+
 /* smb_spmm_t plus the bias side of the layer BELOW, fused into the epilogue:
  * grad_bias[c] = row_sums(out[c, :]) in numpy's pairwise order (nn.py:184,
  * tensor_core.py:353-356) and the optimizer update of bias / velocity_bias

@@ -41,6 +41,8 @@ SIGNATURES = {
     "smb_pattern_destroy": (_i32, [_p]),
     "smb_pattern_csc": (_i32, [_p, _p, _p, _p, _p]),
     "smb_spmm_t": (_i32, [_i32, _p, _p, _p, _i64, _i64, _p, _i64, _p, _i64, _p]),
+    "smb_spmm_t_csc": (_i32, [_i32, _p, _p, _p, _i64, _i64, _p, _i64, _p, _i64, _p]),
+    "smb_values_to_csc": (_i32, [_i32, _p, _p, _p, _p]),
     "smb_spmm_p": (_i32, [_i32, _p, _p, _p, _i64, _i64, _p, _i32, _p, _i64, _p]),
     "smb_sddmm": (_i32, [_i32, _p, _p, _i64, _p, _i64, _i64, _p, _p]),
     "smb_axpby": (_i32, [_i32, _f64, _p, _f64, _p, _i64, _p]),

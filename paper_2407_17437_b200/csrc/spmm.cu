@@ -698,7 +698,7 @@ template <typename T>
 int spmm_t_fused_impl(const smb_pattern* pat, const void* values, const void* dense,
                       int64_t ld_dense, int64_t n, const void* mask, int64_t ld_mask, void* out,
                       int64_t ld_out, void* bias, void* vbias, void* grad_bias_out, int opt_kind,
-                      double mu, double eta, void* stream) {
+                      double mu, double eta, void* stream, bool csc_values = false) {
   const bool want_rows =
       grad_bias_out != nullptr || (opt_kind != SMB_OPT_NONE && bias != nullptr);
   EpiArgs<T> epi{};
@@ -711,10 +711,16 @@ int spmm_t_fused_impl(const smb_pattern* pat, const void* values, const void* de
   epi.opt = make_opt<T>(opt_kind, mu, eta);
   bool done = false;
   cudaStream_t st = as_stream(stream);
-  int rc = launch_segment_spmm<T, kEpiMask, true>(
-      pat->col_ptr, pat->row_idx, pat->perm, static_cast<const T*>(values), pat->k,
-      static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi, st,
-      "smb_spmm_t", &done, pat->k > 0 ? (double)pat->nnz / (double)pat->k : -1.0);
+  const double avg = pat->k > 0 ? (double)pat->nnz / (double)pat->k : -1.0;
+  int rc = csc_values
+               ? launch_segment_spmm<T, kEpiMask, false>(
+                     pat->col_ptr, pat->row_idx, nullptr, static_cast<const T*>(values), pat->k,
+                     static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi,
+                     st, "smb_spmm_t_csc", &done, avg)
+               : launch_segment_spmm<T, kEpiMask, true>(
+                     pat->col_ptr, pat->row_idx, pat->perm, static_cast<const T*>(values), pat->k,
+                     static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi,
+                     st, "smb_spmm_t", &done, avg);
   if (rc != SMB_OK || !want_rows || done) return rc;
   return launch_bias_rows<T>(static_cast<const T*>(out), ld_out, pat->k, n, epi.rb_bias,
                              epi.rb_vbias, epi.rb_grad, epi.opt, st);
@@ -807,6 +813,59 @@ extern "C" int smb_spmm_t(int dtype, const smb_pattern* pat, const void* values,
                                      nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0, stream);
   set_error("smb_spmm_t: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
+}
+
+extern "C" int smb_spmm_t_csc(int dtype, const smb_pattern* pat, const void* values_csc,
+                              const void* dense, int64_t ld_dense, int64_t n, const void* mask,
+                              int64_t ld_mask, void* out, int64_t ld_out, void* stream) {
+  clear_error();
+  const int rc = spmm_t_checks(pat, ld_dense, n, mask, ld_mask, out, ld_out);
+  if (rc != SMB_OK) return rc;
+  if (dtype == SMB_F32)
+    return spmm_t_fused_impl<float>(pat, values_csc, dense, ld_dense, n, mask, ld_mask, out,
+                                    ld_out, nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0,
+                                    stream, true);
+  if (dtype == SMB_F64)
+    return spmm_t_fused_impl<double>(pat, values_csc, dense, ld_dense, n, mask, ld_mask, out,
+                                     ld_out, nullptr, nullptr, nullptr, SMB_OPT_NONE, 0.0, 0.0,
+                                     stream, true);
+  set_error("smb_spmm_t_csc: unsupported dtype %d", dtype);
+  return SMB_ERR_INVALID;
+}
+
+namespace smb {
+namespace {
+template <typename T>
+__global__ void values_to_csc_kernel(const int32_t* __restrict__ perm, const T* __restrict__ src,
+                                     T* __restrict__ dst, int64_t nnz) {
+  pdl_wait();  // src is the update kernel's output
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nnz; q += stride)
+    dst[q] = src[perm[q]];
+  pdl_trigger();
+}
+}  // namespace
+}  // namespace smb
+
+extern "C" int smb_values_to_csc(int dtype, const smb_pattern* pat, const void* values,
+                                 void* values_csc, void* stream) {
+  clear_error();
+  SMB_REQUIRE(pat != nullptr, "smb_values_to_csc: null pattern");
+  if (pat->nnz == 0) return SMB_OK;
+  SMB_REQUIRE(values != nullptr && values_csc != nullptr, "smb_values_to_csc: null values");
+  SMB_REQUIRE(values != values_csc, "smb_values_to_csc: in-place permutation");
+  const unsigned grid = (unsigned)imin(ceil_div(pat->nnz, 256), 148 * 8);
+  if (dtype == SMB_F32)
+    launch_k(values_to_csc_kernel<float>, dim3(grid), dim3(256), 0, as_stream(stream), pat->perm,
+             static_cast<const float*>(values), static_cast<float*>(values_csc), pat->nnz);
+  else if (dtype == SMB_F64)
+    launch_k(values_to_csc_kernel<double>, dim3(grid), dim3(256), 0, as_stream(stream), pat->perm,
+             static_cast<const double*>(values), static_cast<double*>(values_csc), pat->nnz);
+  else {
+    set_error("smb_values_to_csc: unsupported dtype %d", dtype);
+    return SMB_ERR_INVALID;
+  }
+  return check_launch("smb_values_to_csc");
 }
 
 extern "C" int smb_spmm_t_bias(int dtype, const smb_pattern* pat, const void* values,

@@ -164,7 +164,7 @@ def flat_layout(units):
 
 class _Unit:
     __slots__ = ("layer", "relu", "sparse", "m", "k", "grad_off", "bias_off", "nvals", "index",
-                 "vals")
+                 "vals", "vals_csc")
 
     def __init__(self, layer, relu, index=0):
         self.index = index
@@ -278,9 +278,26 @@ class FusedTrainStep:
         self._sides = {}
         for u in self.units:
             u.vals = None
+            u.vals_csc = None
             if u.sparse and self.overlap and not self.dp:
                 cur = u.layer.weights.values
                 u.vals = [cur, cur.clone()]
+                if u.index > 0:
+                    # the transposed SpMM reads a CSC-ordered copy of the
+                    # values (no per-nonzero perm indirection), refreshed
+                    # after every update on the update's stream
+                    u.vals_csc = [torch.empty_like(cur), torch.empty_like(cur)]
+        self.sync_weights()
+
+    def sync_weights(self) -> None:
+        """Re-derive the CSC-ordered value copies from the layers' current
+        values.  The step keeps them up to date itself; call this after
+        changing a layer's weights in place between steps (attach_dataset and
+        set_epoch also do)."""
+        for u in self.units:
+            if u.vals_csc is not None:
+                _lib.call("smb_values_to_csc", _lib.SMB_F32, u.layer.weights.pattern.handle,
+                          ptr(self._vals(u)), ptr(u.vals_csc[self._parity]), stream_ptr())
 
     def _call(self, tag: str, name: str, *args) -> None:
         t = self.timer
@@ -327,6 +344,7 @@ class FusedTrainStep:
         self.data = ddata
         self._graphs.clear()
         self._prefetched = False
+        self.sync_weights()
 
     def set_epoch(self, perm: np.ndarray, rank_offset: int = 0) -> None:
         """Upload the epoch's sample order; this rank's batch k is
@@ -338,6 +356,7 @@ class FusedTrainStep:
             self._graphs.clear()
         self.perm.copy_(flat)
         self.counter.zero_()
+        self.sync_weights()
         self.steps_per_epoch = kb
         self._prefetched = False  # the next step gathers batch 0 of this order first
 
@@ -496,9 +515,15 @@ class FusedTrainStep:
                 if u.sparse and overlap and self.split_bias:
                     # d_{l-1} alone on the critical path; the bias side of
                     # layer l-1 (row sums cross the batch) beside it
-                    self._call(f"spmm_t[{li}]", "smb_spmm_t", F32, lay.weights.pattern.handle,
-                               ptr(self._vals(u)), ptr(dy), ld, B, ptr(mask),
-                               ld if mask is not None else 0, ptr(dst), ld, st)
+                    if u.vals_csc is not None:
+                        self._call(f"spmm_t[{li}]", "smb_spmm_t_csc", F32,
+                                   lay.weights.pattern.handle, ptr(u.vals_csc[self._parity]),
+                                   ptr(dy), ld, B, ptr(mask), ld if mask is not None else 0,
+                                   ptr(dst), ld, st)
+                    else:
+                        self._call(f"spmm_t[{li}]", "smb_spmm_t", F32, lay.weights.pattern.handle,
+                                   ptr(self._vals(u)), ptr(dy), ld, B, ptr(mask),
+                                   ld if mask is not None else 0, ptr(dst), ld, st)
                     with torch.cuda.stream(fork(("weights", li - 1))):
                         self._call(f"bias[{li - 1}]", "smb_bias_grad_update", F32, ptr(dst), ld,
                                    u.k, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
@@ -572,6 +597,10 @@ class FusedTrainStep:
                        lay.weights.pattern.handle, ptr(dy), ld, ptr(x_prev), ld, B,
                        ptr(w_in), ptr(w_out), ptr(vel), ptr(g_out), None, None, None,
                        kind | hint, float(opt.mu), float(eta), st)
+            if u.vals_csc is not None and fuse_update:
+                self._call(f"to_csc[{u.index}]", "smb_values_to_csc", F32,
+                           lay.weights.pattern.handle, ptr(w_out),
+                           ptr(u.vals_csc[self._parity ^ 1]), st)
             return
         # dense layer: cuBLAS FP32 weight gradient + exact update
         gw = lay.grad if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals].view(u.m, u.k)

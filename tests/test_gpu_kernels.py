@@ -521,3 +521,32 @@ def test_gather_columns_equals_host_gather(dtype, features, batch):
     got = host(out)
     assert bits_equal(got[:, :batch], src[perm[base:base + batch]].T)
     assert np.all(got[:, batch:] == -7.0)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (17, 13, 5), (512, 1024, 130), (300, 200, 1),
+                                   (1000, 700, 257)])
+@pytest.mark.parametrize("density", [0.0, 0.05, 1.0])
+@pytest.mark.parametrize("with_mask", [False, True])
+def test_spmm_t_csc_values_equal_perm_path(dtype, shape, density, with_mask):
+    """smb_values_to_csc + smb_spmm_t_csc (the training step's transposed
+    SpMM) == smb_spmm_t through perm, bit for bit."""
+    from paper_2407_17437_b200 import _lib
+    m, k, n = shape
+    rng = np.random.default_rng(m + 3 * k + n)
+    rp, ci, v, _ = random_csr(rng, m, k, density, dtype, empty_rows=True)
+    pat = smb.SparsityPattern(m, k, rp, ci)
+    code = _lib.SMB_F32 if dtype == np.float32 else _lib.SMB_F64
+    d_v = dev(v) if v.size else torch.zeros(1, dtype=torch.float64 if dtype == np.float64 else torch.float32, device="cuda")
+    d = dev(rng.standard_normal((m, n)).astype(dtype))
+    mask = dev(rng.standard_normal((k, n)).astype(dtype)) if with_mask else None
+    csc = torch.empty_like(d_v)
+    _lib.call("smb_values_to_csc", code, pat.handle, tc.ptr(d_v), tc.ptr(csc), tc.stream_ptr())
+    outs = []
+    for name, vals in (("smb_spmm_t", d_v), ("smb_spmm_t_csc", csc)):
+        out = torch.full((k, n), 5.0, dtype=d.dtype, device="cuda")
+        _lib.call(name, code, pat.handle, tc.ptr(vals), tc.ptr(d), n, n,
+                  tc.ptr(mask) if mask is not None else None, n if mask is not None else 0,
+                  tc.ptr(out), n, tc.stream_ptr())
+        outs.append(host(out))
+    assert bits_equal(outs[0], outs[1])
