@@ -550,7 +550,13 @@ class FusedTrainStep:
                                    ptr(mask), ld, u.k, B, ptr(dst), ld, st)
                     self._call(f"bias[{li - 1}]", "smb_bias_grad_update", F32, ptr(dst), ld, u.k,
                                B, b, vb, gb, kind, mu, float(eta), st)
-            if not (overlap and u.sparse):
+            if overlap and not u.sparse:
+                # dense layer: its weight gradient GEMM + update beside the
+                # chain, forked after the kernel that reads the pre-update
+                # weights (dense_t / the W^T d GEMM above) was enqueued
+                with torch.cuda.stream(fork(("weights", li))):
+                    self._weight_side(u, dy, x_prev, eta, fuse_update, stream_ptr())
+            elif not (overlap and u.sparse):
                 self._weight_side(u, dy, x_prev, eta, fuse_update, st)
         if gather and prefetch_at != "start":
             prefetch()
