@@ -339,6 +339,17 @@ SMB_API int smb_dense_backward_input(int dtype, const void* w, int64_t ld_w, int
                                      const void* mask, int64_t ld_mask, void* d_x,
                                      int64_t ld_dx, void* stream);
 
+/* y = W x + bias for a dense layer of m <= 32 output rows (the ER-saturated
+ * output layer; DenseLinearLayer.forward, nn.py:241-255 -- numpy BLAS there,
+ * so tolerance parity): a deterministic split-K pass (each K slice summed in
+ * ascending order with fused multiply-add, the slices then summed in
+ * ascending order, then bias).  W [m, ld_w], x [k, ld_x], y [m, ld_y];
+ * `workspace` holds smb_dense_forward_workspace_bytes(m, k, n) bytes. */
+SMB_API size_t smb_dense_forward_workspace_bytes(int64_t m, int64_t k, int64_t n);
+SMB_API int smb_dense_forward_small(int dtype, const void* w, int64_t ld_w, int64_t m, int64_t k,
+                                    const void* x, int64_t ld_x, int64_t n, const void* bias,
+                                    void* y, int64_t ld_y, void* workspace, void* stream);
+
 /* y = max(x, 0) (nn.py:86-87) and out = d_out * (x_cached > 0) (nn.py:89-91). */
 SMB_API int smb_relu(int dtype, const void* x, int64_t ld_x, int64_t m, int64_t n, void* y, int64_t ld_y,
              void* stream);

@@ -683,6 +683,195 @@ __global__ void __launch_bounds__(256)
 }  // namespace
 }  // namespace smb
 
+namespace smb {
+namespace {
+// y[i, t] = bias[i] + sum_s part[s][i][t], part[s][i][t] = sum_{j in slice s,
+// ascending} W[i, j] * x[j, t] (fused multiply-add): the forward of a small
+// dense output layer (m <= kDenseTMaxRows; DenseLinearLayer.forward,
+// nn.py:241-255, numpy BLAS -- tolerance parity) as a deterministic split-K
+// pass.  CTA = 128 batch columns x one K slice (thread per column, the W
+// slice in shared memory), 8 x loads in flight per thread; a second launch
+// sums the slices in ascending order.  Replaces a cuBLAS SIMT GEMM that ran
+// 30-35 us on the 10 x 8192 x 1024 config-4 shape.
+constexpr int kDfCols = 128;
+
+struct DenseFwdPlan {
+  int64_t slices, ks, col_blocks;
+};
+inline DenseFwdPlan dense_fwd_plan(int64_t k, int64_t n, int cw = 4) {
+  DenseFwdPlan p;
+  p.col_blocks = ceil_div(n > 0 ? n : 1, kDfCols * cw);
+  // ~256 CTAs (16 x loads of 16 bytes in flight per thread keep HBM busy),
+  // slices of >= 64 rows so the partial sums stay small next to x
+  int64_t s = ceil_div(256, p.col_blocks);
+  s = imax(1, imin(s, ceil_div(k > 0 ? k : 1, cw > 1 ? 64 : 32)));
+  p.ks = ceil_div(ceil_div(k > 0 ? k : 1, s), 32) * 32;
+  p.slices = ceil_div(k > 0 ? k : 1, p.ks);
+  return p;
+}
+
+// CW columns per thread: 16 / sizeof(T) with 16-byte x loads (aligned x),
+// else 1
+template <typename T, int M, int CW>
+__global__ void __launch_bounds__(kDfCols)
+    dense_fwd_part_kernel(const T* __restrict__ w, int64_t ld_w, int m_rt, int64_t k, int64_t ks,
+                          const T* __restrict__ x, int64_t ld_x, int64_t n, T* __restrict__ part) {
+  constexpr int MR = M > 0 ? M : kDenseTMaxRows;
+  constexpr int VW = 16 / sizeof(T);
+  constexpr int MP = (MR + VW - 1) / VW * VW;  // smem row padded to 16-byte vectors
+  using V = typename Vec16<T>::type;
+  const int m = M > 0 ? M : m_rt;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s_w = reinterpret_cast<T*>(smem_raw);  // [ks][MP]: W^T of the slice
+  const int64_t j0 = (int64_t)blockIdx.y * ks;
+  const int len = (int)imin(ks, k - j0);
+  for (int e = threadIdx.x; e < MP * len; e += kDfCols) {
+    const int i = e / len, jj = e % len;
+    s_w[jj * MP + i] = i < m ? w[(int64_t)i * ld_w + j0 + jj] : T(0);
+  }
+  pdl_wait();  // x is the previous kernel's output
+  __syncthreads();
+  const int64_t t = ((int64_t)blockIdx.x * kDfCols + threadIdx.x) * CW;
+  if (t >= n) return;
+  const bool full = t + CW <= n;  // (CW > 1: n % CW == 0 is required by the host)
+  T acc[MR][CW];
+#pragma unroll
+  for (int i = 0; i < MR; ++i)
+#pragma unroll
+    for (int c = 0; c < CW; ++c) acc[i][c] = T(0);
+  const T* xp = x + j0 * ld_x + t;
+  constexpr int U = CW > 1 ? 16 : 8;  // x loads in flight per thread
+  auto fma_row = [&](int jj, const T(&xv)[CW]) {
+    const V* wr = reinterpret_cast<const V*>(s_w + jj * MP);  // broadcast 16-byte reads
+#pragma unroll
+    for (int q = 0; q < MP / VW; ++q) {
+      const V wv = wr[q];
+#pragma unroll
+      for (int r = 0; r < VW; ++r) {
+        const int i = q * VW + r;
+        if (i < MR && (M > 0 || i < m)) {
+          const T wi = VecOps<T>::get(wv, r);
+#pragma unroll
+          for (int c = 0; c < CW; ++c) acc[i][c] = fma(wi, xv[c], acc[i][c]);
+        }
+      }
+    }
+  };
+  auto load = [&](int jj, T(&xv)[CW]) {
+    if constexpr (CW > 1) {
+      const V v = *reinterpret_cast<const V*>(xp + (int64_t)jj * ld_x);
+#pragma unroll
+      for (int c = 0; c < CW; ++c) xv[c] = VecOps<T>::get(v, c);
+    } else {
+      xv[0] = xp[(int64_t)jj * ld_x];
+    }
+  };
+  (void)full;
+  int jj = 0;
+  for (; jj + U <= len; jj += U) {
+    T xv[U][CW];
+#pragma unroll
+    for (int u = 0; u < U; ++u) load(jj + u, xv[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) fma_row(jj + u, xv[u]);
+  }
+  for (; jj < len; ++jj) {
+    T xv[CW];
+    load(jj, xv);
+    fma_row(jj, xv);
+  }
+  pdl_trigger();
+  T* pp = part + (int64_t)blockIdx.y * m * n + t;
+#pragma unroll
+  for (int i = 0; i < MR; ++i)
+    if (M > 0 || i < m) {
+#pragma unroll
+      for (int c = 0; c < CW; ++c) pp[(int64_t)i * n + c] = acc[i][c];
+    }
+}
+
+template <typename T>
+__global__ void dense_fwd_sum_kernel(const T* __restrict__ part, int64_t slices, int64_t m,
+                                     int64_t n, const T* __restrict__ bias, T* __restrict__ y,
+                                     int64_t ld_y) {
+  pdl_wait();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * n) return;
+  const int64_t i = e / n, t = e - i * n;
+  const int64_t mn = m * n;
+  T acc = part[e];
+  int64_t s = 1;
+  for (; s + 16 <= slices; s += 16) {  // 16 loads in flight, summed in slice order
+    T v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = part[(s + u) * mn + e];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc += v[u];
+  }
+  for (; s < slices; ++s) acc += part[s * mn + e];
+  y[i * ld_y + t] = (bias ? bias[i] : T(0)) + acc;
+}
+}  // namespace
+}  // namespace smb
+
+extern "C" size_t smb_dense_forward_workspace_bytes(int64_t m, int64_t k, int64_t n) {
+  int64_t slices = 0;
+  for (int cw : {1, 2, 4}) slices = imax(slices, dense_fwd_plan(k, n, cw).slices);
+  return (size_t)(slices * (m > 0 ? m : 1) * (n > 0 ? n : 1)) * sizeof(double);
+}
+
+extern "C" int smb_dense_forward_small(int dtype, const void* w, int64_t ld_w, int64_t m,
+                                       int64_t k, const void* x, int64_t ld_x, int64_t n,
+                                       const void* bias, void* y, int64_t ld_y, void* workspace,
+                                       void* stream) {
+  clear_error();
+  SMB_REQUIRE(m >= 1 && m <= kDenseTMaxRows, "smb_dense_forward_small: needs 1 <= m <= %d",
+              kDenseTMaxRows);
+  SMB_REQUIRE(k >= 0 && n >= 0 && ld_y >= n && (k == 0 || (ld_w >= k && ld_x >= n)),
+              "smb_dense_forward_small: bad shape");
+  if (n == 0) return SMB_OK;
+  SMB_REQUIRE(y && workspace && (k == 0 || (w && x)), "smb_dense_forward_small: null pointer");
+  return dispatch_dtype(dtype, "smb_dense_forward_small", [&](auto tag) {
+    using T = decltype(tag);
+    T* part = static_cast<T*>(workspace);
+    constexpr int VW = 16 / (int)sizeof(T);
+    // 16-byte x loads (VW columns per thread) unless that leaves too few CTAs
+    // (small k): then one column per thread
+    bool vec = aligned16(x) && ld_x % VW == 0 && n % VW == 0;
+    if (vec) {
+      const DenseFwdPlan pv = dense_fwd_plan(k, n, VW);
+      vec = pv.col_blocks * pv.slices >= 148;
+    }
+    const DenseFwdPlan p = dense_fwd_plan(k, n, vec ? VW : 1);
+    if (k == 0) {  // y = bias
+      cudaMemsetAsync(part, 0, sizeof(T) * m * n, as_stream(stream));
+    } else {
+      const dim3 grid((unsigned)p.col_blocks, (unsigned)p.slices);
+      const int vw = 16 / (int)sizeof(T);
+      const int mr = ((m == 10 ? 10 : kDenseTMaxRows) + vw - 1) / vw * vw;  // padded row
+      const size_t smem = sizeof(T) * (size_t)p.ks * mr;
+      auto go = [&](auto kernel) {
+        ensure_smem(kernel, smem);
+        launch_k(kernel, grid, dim3(kDfCols), smem, as_stream(stream),
+                 static_cast<const T*>(w), ld_w, (int)m, k, p.ks, static_cast<const T*>(x),
+                 ld_x, n, part);
+      };
+      if (m == 10 && vec)
+        go(dense_fwd_part_kernel<T, 10, VW>);
+      else if (m == 10)
+        go(dense_fwd_part_kernel<T, 10, 1>);
+      else if (vec)
+        go(dense_fwd_part_kernel<T, 0, VW>);
+      else
+        go(dense_fwd_part_kernel<T, 0, 1>);
+    }
+    launch_k(dense_fwd_sum_kernel<T>, dim3((unsigned)ceil_div(m * n, 256)), dim3(256), 0,
+             as_stream(stream), static_cast<const T*>(part), k == 0 ? int64_t(1) : p.slices,
+             m, n, static_cast<const T*>(bias), static_cast<T*>(y), ld_y);
+    return check_launch("smb_dense_forward_small");
+  });
+}
+
 extern "C" int smb_dense_backward_input(int dtype, const void* w, int64_t ld_w, int64_t m,
                                         int64_t k, const void* d_out, int64_t ld_d, int64_t n,
                                         const void* mask, int64_t ld_mask, void* d_x,

@@ -273,6 +273,9 @@ class FusedTrainStep:
         # writes the second of two value buffers (ping-pong), so the
         # transposed SpMM of the same layer keeps reading the pre-update
         # weights (train.py:400-401); `parity` selects the current buffer.
+        nb = max([int(_lib.load().smb_dense_forward_workspace_bytes(u.m, u.k, self.B))
+                  for u in self.units if not u.sparse and u.m <= DENSE_T_MAX_ROWS] or [0])
+        self._dense_ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev) if nb else None
         self.overlap = True
         self._parity = 0
         self._sides = {}
@@ -439,6 +442,12 @@ class FusedTrainStep:
                 self._call(f"spmm[{li}]", "smb_spmm_p", F32, lay.weights.pattern.handle,
                            ptr(lay.weights.values), ptr(x), ld, B, ptr(lay.bias),
                            _lib.SMB_EPI_RELU if u.relu else _lib.SMB_EPI_NONE, ptr(a), ld, st)
+            elif u.m <= DENSE_T_MAX_ROWS and lay.mask is None:
+                # small (ER-saturated output) layer: split-K kernel, not a
+                # cuBLAS SIMT GEMM (config 4: ~7 vs ~36 us)
+                self._call(f"dense_fwd[{li}]", "smb_dense_forward_small", F32, ptr(lay.weights),
+                           u.k, u.m, u.k, ptr(x), ld, B, ptr(lay.bias), ptr(a), ld,
+                           ptr(self._dense_ws), st)
             else:
                 with _no_tf32():
                     torch.addmm(lay.bias[:, None], lay.weights, x[:, :B], out=a[:, :B])

@@ -4,7 +4,8 @@ Replaces the reference's single-example latency path (bench.py:366-399:
 ``model.feedforward(x)`` on a [features, 1] column in eval mode).
 ``InferenceSession`` keeps every buffer resident and captures ONE CUDA graph
 per session: the pinned-host -> HBM copy of the input, the forward chain
-(smb_spmm with bias + ReLU fused per sparse layer; cuBLAS FP32 for dense /
+(smb_spmm with bias + ReLU fused per sparse layer; smb_dense_forward_small for
+small dense output layers, cuBLAS FP32 for other dense /
 masked-dense layers) and the HBM -> pinned-host copy of the logits.  A call
 is one graph replay plus one stream synchronisation.  Results are bit-identical
 to ``Sequential.feedforward`` (same kernels, same rounding order).
@@ -19,7 +20,8 @@ import torch
 
 from . import _lib
 from .errors import InvalidArgumentError
-from .nn import ActivationLayer, DenseLinearLayer, ReLU, SparseLinearLayer
+from .nn import (DENSE_T_MAX_ROWS, ActivationLayer, DenseLinearLayer, ReLU,
+                 SparseLinearLayer, dense_forward_small)
 from .sparsity import Rng
 from .tensor_core import _no_tf32, ptr, stream_ptr
 
@@ -59,6 +61,11 @@ class InferenceSession:
         self.x_host = torch.zeros((n_in, self.B), dtype=dt).pin_memory()
         self.y_host = torch.zeros((self.units[-1][0].n_out, self.B), dtype=dt).pin_memory()
         self._xh, self._yh = self.x_host.numpy(), self.y_host.numpy()
+        # split-K workspace of the small (ER-saturated output) dense layers
+        nb = max([int(_lib.load().smb_dense_forward_workspace_bytes(l.n_out, l.n_in, self.B))
+                  for l, _ in self.units if isinstance(l, DenseLinearLayer)
+                  and l.n_out <= DENSE_T_MAX_ROWS and l.mask is None] or [0])
+        self._dws = torch.empty(nb, dtype=torch.uint8, device=dev) if nb else None
         self.use_graph = use_graph
         self._graph = None
         self._stream = torch.cuda.Stream(device=dev)
@@ -76,8 +83,13 @@ class InferenceSession:
                           lay.n_out, lay.n_in, ptr(x), B, B, ptr(lay.bias),
                           _lib.SMB_EPI_RELU if relu else _lib.SMB_EPI_NONE, ptr(a), B, st)
             else:
-                with _no_tf32():
-                    torch.addmm(lay.bias[:, None], lay.weights, x, out=a)
+                if lay.n_out <= DENSE_T_MAX_ROWS and lay.mask is None:
+                    # the same kernel as DenseLinearLayer.forward / the step
+                    dense_forward_small(lay.weights, x, lay.bias, out=a, workspace=self._dws,
+                                        stream=st)
+                else:
+                    with _no_tf32():
+                        torch.addmm(lay.bias[:, None], lay.weights, x, out=a)
                 if relu:
                     _lib.call("smb_relu", code, ptr(a), B, lay.n_out, B, ptr(a), B, st)
             x = a

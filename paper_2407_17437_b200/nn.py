@@ -233,7 +233,25 @@ class SparseLinearLayer:
 
 
 # output layers up to this many rows take smb_dense_backward_input for W^T d
+# and (unmasked) smb_dense_forward_small for W x + b
 DENSE_T_MAX_ROWS = 32
+
+
+def dense_forward_small(w, x, bias, out=None, workspace=None, stream=None):
+    """y = w @ x + bias for m <= DENSE_T_MAX_ROWS rows (smb_dense_forward_small:
+    deterministic split-K; the reference's numpy BLAS order is unspecified,
+    nn.py:241-255).  x is [k, n] with a unit column stride."""
+    m, k = w.shape
+    n = x.shape[1]
+    if out is None:
+        out = torch.empty((m, n), dtype=w.dtype, device=w.device)
+    if workspace is None:
+        nb = int(_lib.load().smb_dense_forward_workspace_bytes(m, k, n))
+        workspace = torch.empty(nb, dtype=torch.uint8, device=w.device)
+    _lib.call("smb_dense_forward_small", dtype_code(w.dtype), ptr(w), w.stride(0), m, k, ptr(x),
+              x.stride(0), n, ptr(bias), ptr(out), out.stride(0), ptr(workspace),
+              stream if stream is not None else stream_ptr())
+    return out
 
 
 class DenseLinearLayer:
@@ -275,8 +293,12 @@ class DenseLinearLayer:
 
     def forward(self, x, training=True):
         x = _act(x, self.n_in, self.weights.dtype)
-        with _no_tf32():
-            y = torch.addmm(self.bias[:, None], self.weights, x)
+        if self.n_out <= DENSE_T_MAX_ROWS and self.mask is None:
+            # small (ER-saturated output) layer: the fused step's split-K kernel
+            y = dense_forward_small(self.weights, x, self.bias)
+        else:
+            with _no_tf32():
+                y = torch.addmm(self.bias[:, None], self.weights, x)
         if training:
             self._cached_input = x
         return y

@@ -550,3 +550,23 @@ def test_spmm_t_csc_values_equal_perm_path(dtype, shape, density, with_mask):
                   tc.ptr(out), n, tc.stream_ptr())
         outs.append(host(out))
     assert bits_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("m,k,n", [(10, 8192, 1024), (10, 512, 100), (10, 65536, 64), (3, 7, 5),
+                                   (32, 300, 257), (17, 1000, 1), (10, 0, 4), (10, 3000, 6)])
+def test_dense_forward_small_matches_blas(dtype, m, k, n):
+    """smb_dense_forward_small (split-K, fixed order): deterministic and within
+    BLAS tolerance of W @ x + b (DenseLinearLayer.forward, nn.py:241-255)."""
+    from paper_2407_17437_b200.nn import dense_forward_small
+    rng = np.random.default_rng(m * k + n)
+    w = rng.standard_normal((m, k)).astype(dtype)
+    x = rng.standard_normal((k, n)).astype(dtype)
+    b = rng.standard_normal(m).astype(dtype)
+    y1 = host(dense_forward_small(dev(w), dev(x), dev(b)))
+    y2 = host(dense_forward_small(dev(w), dev(x), dev(b)))
+    assert bits_equal(y1, y2)
+    want = w.astype(np.float64) @ x.astype(np.float64) + b[:, None]
+    # rounding of a k-term fp32 sum grows ~sqrt(k) (cuBLAS / numpy BLAS alike)
+    tol = (1e-5 if dtype == np.float32 else 1e-12) * max(1.0, np.sqrt(k) / 16)
+    assert rel_err(y1, want) <= tol
