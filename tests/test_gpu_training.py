@@ -273,3 +273,39 @@ def test_data_parallel_structure_on_one_gpu_equals_fused(density, B):
     for (n1, a), (n2, b) in zip(params_host(models[0]), params_host(models[1])):
         assert n1 == n2
         assert bits_equal(a, b), n1
+
+
+def test_sync_weights_after_in_place_change():
+    """The step's CSC-ordered value copies (smb_spmm_t_csc) follow an in-place
+    change of the layer values once sync_weights() is called: the next steps
+    equal those of a fresh step object built on the changed model."""
+    chain, B = [3072, 1024, 512, 10], 128
+    data = smb.synthetic_dataset(seed=5, n_samples=B * 8, features=chain[0])
+    models, steps = [], []
+    for _ in range(2):
+        model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=chain, density=0.01, seed=6,
+                                                        batch_size=B))
+        st = smb.FusedTrainStep(model, B)
+        st.attach_dataset(smb.DeviceDataset(data))
+        st.set_epoch(np.arange(B * 8))
+        models.append(model)
+        steps.append(st)
+    for _ in range(2):
+        steps[0].step(0.02)
+        steps[1].step(0.02)
+    for m_ in models:  # same in-place change on both replicas
+        for lay in m_.layers:
+            if isinstance(lay, smb.SparseLinearLayer):
+                lay.weights.values.mul_(0.5)
+    steps[0].sync_weights()
+    # replica 1: a fresh step object on the changed model, same batch order
+    fresh = smb.FusedTrainStep(models[1], B)
+    fresh.attach_dataset(smb.DeviceDataset(data))
+    fresh.set_epoch(np.arange(B * 8))
+    fresh.counter.copy_(steps[1].counter)
+    for _ in range(2):
+        steps[0].step(0.02)
+        fresh.step(0.02)
+    torch.cuda.synchronize()
+    for (_, a), (_, b) in zip(params_host(models[0]), params_host(models[1])):
+        assert bits_equal(a, b)
