@@ -15,8 +15,10 @@ Our arm prints one JSON line with: value (device-resident throughput, per-step
 CUDA events on the launching stream, L2 flushed before every timed step, max
 over ranks), e2e (the public FusedTrainStep.train_batch API fed from pinned
 host buffers, H2D + step + D2H of the loss inside the timed region), roofline
-(dominant kernel, algorithmic bytes / CUDA-event duration vs the measured HBM
-peak), cpu_baseline (the oracle port timed on this host's cores), clocks and
+(dominant kernel, algorithmic bytes / its launch duration vs the measured HBM
+peak; durations from 20 back-to-back launches of each of the step's kernels
+captured in a CUDA graph between two CUDA events on the launching stream,
+KernelTimer.kernel_durations), cpu_baseline (the oracle port timed on this host's cores), clocks and
 gpu_launches.  `--impl reference` times the reference algorithm's CPU
 implementation (the C/numpy oracle port, all host threads) on the same config.
 """
