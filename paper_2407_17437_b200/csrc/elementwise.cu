@@ -695,6 +695,8 @@ namespace {
 // 30-35 us on the 10 x 8192 x 1024 config-4 shape.
 constexpr int kDfCols = 128;
 
+constexpr int64_t kDfMaxSlice = 768;  // 768 x 32 x 8 B = 192 KB of shared memory
+
 struct DenseFwdPlan {
   int64_t slices, ks, col_blocks;
 };
@@ -706,6 +708,10 @@ inline DenseFwdPlan dense_fwd_plan(int64_t k, int64_t n, int cw = 4) {
   int64_t s = ceil_div(256, p.col_blocks);
   s = imax(1, imin(s, ceil_div(k > 0 ? k : 1, cw > 1 ? 64 : 32)));
   p.ks = ceil_div(ceil_div(k > 0 ? k : 1, s), 32) * 32;
+  // the W^T slice lives in shared memory (ks x 32 padded rows x 8 bytes at
+  // most): cap the slice so it fits the 227 KB opt-in limit for every m,
+  // dtype and width (the workspace size uses the same plan)
+  p.ks = imin(p.ks, kDfMaxSlice);
   p.slices = ceil_div(k > 0 ? k : 1, p.ks);
   return p;
 }

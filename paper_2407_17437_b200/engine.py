@@ -86,6 +86,10 @@ class KernelTimer:
         every recorded call; sddmm_update writes the other value buffer, so
         repeats recompute the same update."""
         cur = torch.cuda.current_stream()
+        # every replayed launch writes its outputs again (velocity, bias,
+        # dense weights are updated in place): snapshot the step's whole
+        # mutable state and restore it afterwards
+        snapshot = [(t, t.clone()) for t in step.state_tensors()]
         saved = (step.timer, step.use_graph)
         self.calls = []
         step.timer, step.use_graph = self, False
@@ -115,6 +119,10 @@ class KernelTimer:
             e_.synchronize()
             c, t = out.get(tag, (0, 0.0))
             out[tag] = (c + reps * replays, t + s_.elapsed_time(e_))
+        torch.cuda.synchronize()
+        for t, saved_t in snapshot:
+            t.copy_(saved_t)
+        torch.cuda.synchronize()
         return out
 
     def summary(self):
@@ -164,7 +172,7 @@ def flat_layout(units):
 
 class _Unit:
     __slots__ = ("layer", "relu", "sparse", "m", "k", "grad_off", "bias_off", "nvals", "index",
-                 "vals", "vals_csc")
+                 "vals", "vals_csc", "seen")
 
     def __init__(self, layer, relu, index=0):
         self.index = index
@@ -179,7 +187,8 @@ class _Unit:
 class FusedTrainStep:
     def __init__(self, model, batch_size: int, global_batch: int | None = None,
                  process_group=None, use_graph: bool = True, fuse_tail: bool | None = None,
-                 force_dp: bool = False, fuse_logits: bool = False):
+                 force_dp: bool = False, fuse_logits: bool = False,
+                 bucketed: bool | None = None):
         self.units = self._parse(model)
         self.model = model
         self.B = int(batch_size)
@@ -188,10 +197,22 @@ class FusedTrainStep:
             raise InvalidArgumentError("batch_size must be positive")
         self.pg = process_group
         self.world = 1
+        backend = None
         if process_group is not None:
             import torch.distributed as dist
 
             self.world = dist.get_world_size(process_group)
+            backend = str(dist.get_backend(process_group)).lower()
+        # data parallel: one all-reduce per layer bucket, issued as soon as the
+        # layer's gradients exist and followed by that layer's update, so the
+        # collectives overlap the backward of the layers below (bucketed);
+        # with NCCL the collectives are captured into the step's CUDA graph
+        # (graph_comm), other backends (gloo) run the same sequence eagerly.
+        # bucketed=False: one all-reduce of the whole flat buffer after the
+        # backward, then one update launch (the round-1 structure).
+        self.bucketed = (os.environ.get("SMB_DP_BUCKETED", "1") != "0"
+                         if bucketed is None else bool(bucketed))
+        self.graph_comm = process_group is None or backend == "nccl"
         # data-parallel structure: a forward/backward pass that only produces
         # gradients (flat buffer), the all-reduce, then the update pass.
         # force_dp runs that structure on one process (testing; the
@@ -282,25 +303,82 @@ class FusedTrainStep:
         for u in self.units:
             u.vals = None
             u.vals_csc = None
+            u.seen = None
             if u.sparse and self.overlap and not self.dp:
+                # two value buffers; the layer's own `weights.values` tensor
+                # object stays the same and is re-pointed (set_) at the current
+                # buffer after every step, so a caller holding it always reads
+                # the updated weights, like the reference's in-place update
+                # (nn.py:187-198)
                 cur = u.layer.weights.values
-                u.vals = [cur, cur.clone()]
+                u.vals = [cur.view_as(cur), cur.clone()]
                 if u.index > 0:
                     # the transposed SpMM reads a CSC-ordered copy of the
                     # values (no per-nonzero perm indirection), refreshed
                     # after every update on the update's stream
                     u.vals_csc = [torch.empty_like(cur), torch.empty_like(cur)]
+            elif u.sparse and self.overlap and self.dp and u.index > 0:
+                # data parallel: no ping-pong (the update waits for the
+                # layer's transposed SpMM), one CSC copy refreshed after the
+                # update on the same stream
+                c = torch.empty_like(u.layer.weights.values)
+                u.vals_csc = [c, c]
         self.sync_weights()
 
     def sync_weights(self) -> None:
         """Re-derive the CSC-ordered value copies from the layers' current
-        values.  The step keeps them up to date itself; call this after
-        changing a layer's weights in place between steps (attach_dataset and
-        set_epoch also do)."""
+        values.  Not needed by callers: every step first checks each layer's
+        `weights.values` (a replaced tensor or a bumped version counter, i.e. an
+        in-place torch op or a layer-API optimize()) and re-syncs itself."""
         for u in self.units:
-            if u.vals_csc is not None:
-                _lib.call("smb_values_to_csc", _lib.SMB_F32, u.layer.weights.pattern.handle,
-                          ptr(self._vals(u)), ptr(u.vals_csc[self._parity]), stream_ptr())
+            self._sync_unit(u)
+
+    def _sync_unit(self, u) -> None:
+        if u.vals is not None:
+            v = u.layer.weights.values
+            cur = u.vals[self._parity]
+            if v.data_ptr() != cur.data_ptr():
+                # the caller assigned a new value tensor: adopt its contents
+                # into the current buffer and point the tensor at that buffer
+                if v.shape != cur.shape or v.dtype != cur.dtype:
+                    raise InvalidArgumentError("weights.values changed shape or dtype")
+                cur.copy_(v)
+                v.set_(cur)
+        if u.sparse:
+            u.seen = u.layer.weights.values._version
+        if u.vals_csc is not None:
+            _lib.call("smb_values_to_csc", _lib.SMB_F32, u.layer.weights.pattern.handle,
+                      ptr(self._vals(u)), ptr(u.vals_csc[self._parity]), stream_ptr())
+
+    def _adopt_external_changes(self) -> None:
+        """Re-sync any layer whose values changed outside the step."""
+        for u in self.units:
+            if u.vals is None and u.vals_csc is None:
+                continue
+            v = u.layer.weights.values
+            if v._version != u.seen or (
+                    u.vals is not None and v.data_ptr() != u.vals[self._parity].data_ptr()):
+                self._sync_unit(u)
+
+    def state_tensors(self):
+        """Every tensor a step mutates (parameters, optimizer state, both value
+        buffers and the CSC copies): KernelTimer snapshots and restores them."""
+        out = []
+        for u in self.units:
+            lay = u.layer
+            if u.sparse:
+                out += list(u.vals) if u.vals is not None else [lay.weights.values]
+                out += list(u.vals_csc) if u.vals_csc is not None else []
+                out += [lay.velocity.values] if lay.velocity is not None else []
+                out += [lay.grad.values]
+            else:
+                out += [lay.weights, lay.grad]
+                out += [lay.velocity] if lay.velocity is not None else []
+            out += [lay.bias] + ([lay.velocity_bias] if lay.velocity_bias is not None else [])
+        out += [self.loss, self.counter] + self.acts + self.dys
+        if self.flat is not None:
+            out.append(self.flat)
+        return out
 
     def _call(self, tag: str, name: str, *args) -> None:
         t = self.timer
@@ -394,7 +472,51 @@ class FusedTrainStep:
         return (None, None, ptr(self.flat[u.bias_off:u.bias_off + u.m]), _lib.SMB_OPT_NONE,
                 float(opt.mu))
 
-    def _launch_forward_backward(self, eta: float, fuse_update: bool, gather: bool) -> None:
+    def _allreduce_bucket(self, u) -> None:
+        """SUM-all-reduce of unit u's flat-buffer bucket [values | bias].
+        Buckets are issued in the same order (last layer first) on every rank,
+        so the communicator sees one consistent sequence of collectives."""
+        if self.pg is None:  # force_dp on one process: the identity
+            return
+        import torch.distributed as dist
+
+        work = dist.all_reduce(self.flat[u.grad_off:u.bias_off + u.m], group=self.pg,
+                               async_op=True)
+        work.wait()  # the current (weights) stream waits for the collective
+
+    def _update_unit_from_flat(self, u, eta: float, st) -> None:
+        """The exact optimizer update of unit u from its summed bucket."""
+        lay = u.layer
+        opt = lay.optimizer
+        kind = optimizer_kind(opt)
+        g = self.flat[u.grad_off:u.grad_off + u.nvals]
+        gb = self.flat[u.bias_off:u.bias_off + u.m]
+        if u.sparse:
+            vals = lay.weights.values
+            vel = lay.velocity.values if lay.velocity is not None else None
+        else:
+            vals = lay.weights
+            vel = lay.velocity.view(-1) if lay.velocity is not None else None
+        if not u.sparse and lay.mask is not None:
+            self._call(f"update[{u.index}]", "smb_masked_optimizer_step", _lib.SMB_F32,
+                       ptr(vals), ptr(vel), ptr(g), ptr(lay.mask), u.nvals, kind,
+                       float(opt.mu), float(eta), st)
+        else:
+            self._call(f"update[{u.index}]", "smb_optimizer_step", _lib.SMB_F32, ptr(vals),
+                       ptr(vel), ptr(g), u.nvals, kind, float(opt.mu), float(eta), st)
+        self._call(f"update_bias[{u.index}]", "smb_optimizer_step", _lib.SMB_F32,
+                   ptr(lay.bias), ptr(lay.velocity_bias), ptr(gb), u.m, kind, float(opt.mu),
+                   float(eta), st)
+        self._refresh_csc(u, st)
+
+    def _refresh_csc(self, u, st) -> None:
+        if u.vals_csc is not None and u.vals is None:  # data parallel: one CSC copy
+            self._call(f"to_csc[{u.index}]", "smb_values_to_csc", _lib.SMB_F32,
+                       u.layer.weights.pattern.handle, ptr(u.layer.weights.values),
+                       ptr(u.vals_csc[0]), st)
+
+    def _launch_forward_backward(self, eta: float, fuse_update: bool, gather: bool,
+                                 comm: bool = False) -> None:
         st = stream_ptr()
         B, ld = self.B, self.ld
         F32 = _lib.SMB_F32
@@ -440,7 +562,7 @@ class FusedTrainStep:
                 break
             if u.sparse:
                 self._call(f"spmm[{li}]", "smb_spmm_p", F32, lay.weights.pattern.handle,
-                           ptr(lay.weights.values), ptr(x), ld, B, ptr(lay.bias),
+                           ptr(self._vals(u)), ptr(x), ld, B, ptr(lay.bias),
                            _lib.SMB_EPI_RELU if u.relu else _lib.SMB_EPI_NONE, ptr(a), ld, st)
             elif u.m <= DENSE_T_MAX_ROWS and lay.mask is None:
                 # small (ER-saturated output) layer: split-K kernel, not a
@@ -451,8 +573,8 @@ class FusedTrainStep:
             else:
                 with _no_tf32():
                     torch.addmm(lay.bias[:, None], lay.weights, x[:, :B], out=a[:, :B])
-                if u.relu:
-                    self._call(f"relu[{li}]", "smb_relu", F32, ptr(a), ld, u.m, B, ptr(a), ld, st)
+            if not u.sparse and u.relu:
+                self._call(f"relu[{li}]", "smb_relu", F32, ptr(a), ld, u.m, B, ptr(a), ld, st)
             x = a
         # loss gradient (softmax CE) scaled by 1/B_global; the same launch
         # applies the last layer's bias side and advances the step counter
@@ -567,6 +689,17 @@ class FusedTrainStep:
                     self._weight_side(u, dy, x_prev, eta, fuse_update, stream_ptr())
             elif not (overlap and u.sparse):
                 self._weight_side(u, dy, x_prev, eta, fuse_update, st)
+            if comm:
+                # data parallel, per-layer bucket: layer li's [values | bias]
+                # gradients are complete on its weights stream (bias side
+                # forked at layer li+1, SDDMM / dense GEMM above); the
+                # stream also waits for main, which now holds the last reader
+                # of the pre-update W_li (its transposed product).  Sum the
+                # bucket over the ranks, then update layer li there, while
+                # the backward of the layers below continues on main.
+                with torch.cuda.stream(fork(("weights", li)) if overlap else main):
+                    self._allreduce_bucket(u)
+                    self._update_unit_from_flat(u, eta, stream_ptr())
         if gather and prefetch_at != "start":
             prefetch()
         for s_ in forked:
@@ -592,7 +725,9 @@ class FusedTrainStep:
         self._parity ^= 1
         for u in self.units:
             if u.vals is not None:
-                u.layer.weights.values = u.vals[self._parity]
+                v = u.layer.weights.values
+                v.set_(u.vals[self._parity])
+                u.seen = v._version
 
     def _weight_side(self, u, dy, x_prev, eta, fuse_update, st):
         lay = u.layer
@@ -670,6 +805,8 @@ class FusedTrainStep:
             kind, mu = self._seg_kind
             self._call("update", "smb_optimizer_step_multi", _lib.SMB_F32, ptr(segs),
                        2 * len(self.units), self.flat.numel(), kind, mu, float(eta), st)
+            for u in self.units:
+                self._refresh_csc(u, st)
             return
         for u in self.units:
             lay = u.layer
@@ -693,11 +830,14 @@ class FusedTrainStep:
             self._call(f"update_bias[{u.index}]", "smb_optimizer_step", _lib.SMB_F32,
                        ptr(lay.bias), ptr(lay.velocity_bias), ptr(gb), u.m, kind, float(opt.mu),
                        float(eta), st)
+            self._refresh_csc(u, st)
 
     # ------------------------------------------------------------------
     def _run_eager(self, eta: float, gather: bool, part: str) -> None:
         if not self.dp:
             self._launch_forward_backward(eta, True, gather)
+        elif part == "dp":  # gradients, per-layer all-reduce buckets and updates
+            self._launch_forward_backward(eta, False, gather, comm=True)
         elif part == "fb":
             self._launch_forward_backward(eta, False, gather)
         else:
@@ -710,6 +850,7 @@ class FusedTrainStep:
         (``x_slots[slot]`` / ``t_slots[slot]``; slot 0 is ``x_in`` / ``t_in``)."""
         if gather is None:
             gather = self.data is not None
+        self._adopt_external_changes()
         if gather and (self.data is None or self.perm is None):
             raise InvalidArgumentError("attach_dataset() and set_epoch() before gathering steps")
         if gather:
@@ -722,6 +863,8 @@ class FusedTrainStep:
         if not self.dp:
             self._replay_or_run(eta, gather, "all")
             self._flip_parity()
+        elif self.bucketed:
+            self._replay_or_run(eta, gather, "dp")
         else:
             self._replay_or_run(eta, gather, "fb")
             if self.pg is not None:  # (a world of 1 is the identity)
@@ -733,7 +876,7 @@ class FusedTrainStep:
             self._gslot ^= 1  # the next batch was prefetched into the other slot
 
     def _replay_or_run(self, eta, gather, part):
-        if not self.use_graph:
+        if not self.use_graph or (part == "dp" and not self.graph_comm):
             self._run_eager(eta, gather, part)
             return
         key = (float(eta), gather, part, self._slot, self._parity)

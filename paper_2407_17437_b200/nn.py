@@ -112,6 +112,9 @@ def _step(param: torch.Tensor, grad: torch.Tensor, velocity, opt, eta: float) ->
         "smb_optimizer_step", dtype_code(param.dtype), ptr(param), ptr(velocity), ptr(grad), n,
         optimizer_kind(opt), float(opt.mu), float(eta), stream_ptr(),
     )
+    # the kernel wrote through a raw pointer: bump the tensor's version like
+    # an in-place torch op would, so FusedTrainStep sees the changed weights
+    torch.autograd.graph.increment_version(param)
 
 
 def _act(x, rows: int, dtype: torch.dtype) -> torch.Tensor:
@@ -243,6 +246,8 @@ def dense_forward_small(w, x, bias, out=None, workspace=None, stream=None):
     nn.py:241-255).  x is [k, n] with a unit column stride."""
     m, k = w.shape
     n = x.shape[1]
+    if n > 1 and (x.stride(1) != 1 or (k > 1 and x.stride(0) < n)):
+        x = x.contiguous()  # the kernel reads rows of unit column stride
     if out is None:
         out = torch.empty((m, n), dtype=w.dtype, device=w.device)
     if workspace is None:

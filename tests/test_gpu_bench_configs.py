@@ -1,0 +1,172 @@
+"""Oracle parity at every configuration bench.py and scripts/kernel_bench.py time.
+
+The kernels pick their variant (lane width, ring depth, tile size, blocked or
+row-split form) from the batch width, the row/column lengths and the wave
+count, so parity proven on small shapes does not cover the variants that run
+at the benchmarked shapes.  These tests step the fused path (or launch the
+single kernels) at exactly those shapes beside the CPU oracle:
+
+* BASELINE config 2 point (3072-1024-512-10, d=0.01, B=1024): 20 fused steps,
+  per-step loss and weights within 1e-4 (north_star tolerance);
+* config 2 at d=0.05 / 0.5 (dense output layer) with B=100 and 1024;
+* config 4 (3072-8192x3-10, d=0.01, B=1024): 3 steps;
+* config 5 (3072-65536-65536-10, d=0.001, injected pattern) at B=512: 2 steps;
+* config 3 (8192x8192 CSR, d in {0.001, 0.01, 0.1}, B in {128, 512, 2048}):
+  forward SpMM, transposed SpMM (CSR-value and CSC-value forms) and
+  SDDMM + Nesterov update, each BIT-EXACT against the oracle's restatement of
+  _kernels.py:25-83 and nn.py:189-193.
+
+Reference: train.py:398-401 (the step), _kernels.py:25-83 (the kernels).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bits_equal, rel_err
+
+pytestmark = pytest.mark.gpu
+
+import paper_2407_17437_b200 as smb  # noqa: E402
+from paper_2407_17437_b200 import _lib  # noqa: E402
+from paper_2407_17437_b200.tensor_core import ptr, stream_ptr  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def orc():
+    from oracle import oracle as O
+
+    O.build()
+    O.set_threads(os.cpu_count() or 1)
+    return O
+
+
+def _params(model):
+    return [(n, t.detach().cpu().numpy().reshape(-1)) for n, t in model.parameters()]
+
+
+def _max_rel(model, ref):
+    return max(rel_err(a, b.reshape(-1))
+               for (_, a), (_, b) in zip(_params(model), ref.parameters()))
+
+
+def _track(orc, chain, density, B, steps, eta=0.01, seed=0, large=False, n_samples=None,
+           check_every=1):
+    """Fused steps beside the oracle on the same batches; asserts the north_star
+    per-step tolerance and returns the worst parameter rel_err."""
+    n_samples = n_samples or B * steps
+    data = smb.synthetic_dataset(seed=seed + 7, n_samples=n_samples, features=chain[0],
+                                 classes=chain[-1])
+    cfg = smb.ExperimentConfig(layer_dims=chain, density=density, seed=seed, batch_size=B, lr=eta)
+    model, _ = smb.build_model(cfg, large_patterns=large)
+    ref = orc.OracleMLP.build(chain, density, seed=seed, large_patterns=large)
+    for (n1, a), (n2, b) in zip(_params(model), ref.parameters()):
+        assert n1 == n2 and bits_equal(a, b.reshape(-1)), n1  # same initial model
+    step = smb.FusedTrainStep(model, B)
+    step.attach_dataset(smb.DeviceDataset(data))
+    perm = np.random.default_rng(seed).permutation(n_samples)
+    step.set_epoch(perm)
+    worst = 0.0
+    for k in range(steps):
+        step.step(eta)
+        cols = perm[k * B:(k + 1) * B]
+        ref_loss = ref.step(np.ascontiguousarray(data.Xtrain[:, cols]),
+                            np.ascontiguousarray(data.Ttrain[:, cols]), eta)
+        gpu_loss = step.loss_value()
+        assert abs(gpu_loss - ref_loss) <= 1e-4 * abs(ref_loss), (k, gpu_loss, ref_loss)
+        if k % check_every == check_every - 1 or k == steps - 1:
+            worst = max(worst, _max_rel(model, ref))
+            assert worst <= 1e-4, (k, worst)
+    return worst
+
+
+def test_config2_point_b1024_twenty_steps(orc):
+    """The BENCH line's workload: 3072-1024-512-10, d=0.01, B=1024, 20 steps."""
+    _track(orc, [3072, 1024, 512, 10], 0.01, 1024, 20, check_every=5)
+
+
+@pytest.mark.parametrize("density", [0.05, 0.5])
+@pytest.mark.parametrize("B", [100, 1024])
+def test_config2_sweep_points(orc, density, B):
+    """Sweep points with an ER-saturated (dense) output layer."""
+    _track(orc, [3072, 1024, 512, 10], density, B, 4)
+
+
+def test_config4_b1024_three_steps(orc):
+    """BASELINE config 4: 3072-8192-8192-8192-10, d=0.01, B=1024."""
+    _track(orc, [3072, 8192, 8192, 8192, 10], 0.01, 1024, 3)
+
+
+def test_config5_b512_two_steps(orc):
+    """BASELINE config 5 at the bench batch (B=512 per GPU), injected pattern."""
+    _track(orc, [3072, 65536, 65536, 10], 0.001, 512, 2, large=True)
+
+
+# ---------------------------------------------------------------------------
+# config 3: the single-layer kernels at the kernel_bench.py shapes, bit-exact
+# ---------------------------------------------------------------------------
+_PATTERNS = {}
+
+
+def _pattern(d):
+    if d not in _PATTERNS:
+        n = 8192
+        nnz = int(round(d * n * n))
+        _PATTERNS[d] = smb.sample_pattern(n, n, nnz, smb.Rng(0).stream("pattern"))
+    return _PATTERNS[d]
+
+
+@pytest.mark.parametrize("density", [0.001, 0.01, 0.1])
+@pytest.mark.parametrize("B", [128, 512, 2048])
+def test_config3_kernels_bit_exact(orc, density, B):
+    n = 8192
+    pat = _pattern(density)
+    rp, ci = pat.host_arrays()
+    nnz = ci.shape[0]
+    rng = np.random.default_rng(int(density * 1e4) + B)
+    vals_h = rng.standard_normal(nnz).astype(np.float32)
+    x_h = rng.standard_normal((n, B)).astype(np.float32)
+    dy_h = rng.standard_normal((n, B)).astype(np.float32)
+    vel_h = (0.1 * rng.standard_normal(nnz)).astype(np.float32)
+    dev = torch.device("cuda")
+    vals = torch.from_numpy(vals_h).to(dev)
+    X = torch.from_numpy(x_h).to(dev)
+    dY = torch.from_numpy(dy_h).to(dev)
+    out = torch.empty(n, B, device=dev)
+    st = stream_ptr()
+
+    # forward SpMM (_kernels.py:25-37)
+    _lib.call("smb_spmm_p", 0, pat.handle, ptr(vals), ptr(X), B, B, None, 0, ptr(out), B, st)
+    assert bits_equal(out.cpu().numpy(), orc.spmm(rp, ci, vals_h, x_h)), "spmm"
+
+    # transposed SpMM (_kernels.py:40-59), CSR values and CSC-ordered values
+    ref_t = orc.spmm_t(rp, ci, vals_h, n, dy_h)
+    _lib.call("smb_spmm_t", 0, pat.handle, ptr(vals), ptr(dY), B, B, None, 0, ptr(out), B, st)
+    assert bits_equal(out.cpu().numpy(), ref_t), "spmm_t"
+    vcsc = torch.empty_like(vals)
+    _lib.call("smb_values_to_csc", 0, pat.handle, ptr(vals), ptr(vcsc), st)
+    out.zero_()
+    _lib.call("smb_spmm_t_csc", 0, pat.handle, ptr(vcsc), ptr(dY), B, B, None, 0, ptr(out), B,
+              st)
+    assert bits_equal(out.cpu().numpy(), ref_t), "spmm_t_csc"
+
+    # SDDMM + Nesterov update of values / velocity (_kernels.py:62-83, nn.py:189-193)
+    mu, eta = 0.9, 1e-3
+    vel = torch.from_numpy(vel_h).to(dev)
+    vout = torch.empty_like(vals)
+    _lib.call("smb_sddmm_update_into", 0, pat.handle, ptr(dY), B, ptr(X), B, B, ptr(vals),
+              ptr(vout), ptr(vel), None, None, None, None, _lib.SMB_OPT_NESTEROV, mu, eta, st)
+    g = orc.sddmm(rp, ci, dy_h, x_h)
+    v_ref, w_ref = vel_h.copy(), vals_h.copy()
+    orc.axpby(mu, v_ref, 1.0, g)
+    orc.axpby(1.0, w_ref, -eta * mu, v_ref)
+    orc.axpby(1.0, w_ref, -eta, g)
+    assert bits_equal(vel.cpu().numpy(), v_ref), "sddmm velocity"
+    assert bits_equal(vout.cpu().numpy(), w_ref), "sddmm values"
+    # the gradient itself (SMB_OPT_NONE writes grad_out)
+    gout = torch.empty_like(vals)
+    _lib.call("smb_sddmm_update", 0, pat.handle, ptr(dY), B, ptr(X), B, B, ptr(vals), None,
+              ptr(gout), None, None, None, _lib.SMB_OPT_NONE, 0.0, 0.0, st)
+    assert bits_equal(gout.cpu().numpy(), g), "sddmm grad"

@@ -49,8 +49,13 @@ def test_kernel_durations_time_every_sparse_launch():
     st.set_epoch(np.arange(B * 4))
     for _ in range(2):
         st.step(0.02)
+    torch.cuda.synchronize()
+    before = params_host(model)
     from paper_2407_17437_b200.engine import KernelTimer
     out = KernelTimer().kernel_durations(st, 0.02, reps=4, replays=2)
+    # the timing pass replays in-place updates; it must leave the model as it was
+    for (n1, a), (n2, b) in zip(before, params_host(model)):
+        assert n1 == n2 and bits_equal(a, b), n1
     for tag in ("spmm[0]", "spmm[1]", "spmm[2]", "softmax_ce", "spmm_t[2]", "spmm_t[1]",
                 "sddmm_update[0]", "sddmm_update[1]", "sddmm_update[2]"):
         cnt, ms = out[tag]
@@ -106,6 +111,7 @@ def _fused_and_layerwise(chain, density, seed, B, steps, eta=0.05, fuse_tail=Fal
     ([3072, 1024, 512, 10], 0.01, 100),
     ([3072, 1024, 512, 10], 0.01, 1024),
     ([3072, 1024, 512, 10], 0.1, 256),    # dense last layer (cuBLAS on both paths)
+    ([3072, 1024, 32, 10], 0.1, 128),     # small dense HIDDEN layer + ReLU (split-K forward)
     ([200, 300, 10], 0.2, 37),            # odd batch, padded leading dimension
 ])
 def test_fused_step_equals_layer_api_bitwise(chain, density, B):
@@ -275,10 +281,13 @@ def test_data_parallel_structure_on_one_gpu_equals_fused(density, B):
         assert bits_equal(a, b), n1
 
 
-def test_sync_weights_after_in_place_change():
-    """The step's CSC-ordered value copies (smb_spmm_t_csc) follow an in-place
-    change of the layer values once sync_weights() is called: the next steps
-    equal those of a fresh step object built on the changed model."""
+@pytest.mark.parametrize("how", ["in_place", "assign", "layer_optimize"])
+def test_step_follows_external_weight_change(how):
+    """The step's value buffers and CSC-ordered copies (smb_spmm_t_csc) follow
+    a change of the layer values made between steps -- an in-place torch op,
+    a newly assigned tensor, or the layer API's optimize() -- without any
+    explicit sync call: the next steps equal those of a fresh step object
+    built on the changed model."""
     chain, B = [3072, 1024, 512, 10], 128
     data = smb.synthetic_dataset(seed=5, n_samples=B * 8, features=chain[0])
     models, steps = [], []
@@ -293,11 +302,17 @@ def test_sync_weights_after_in_place_change():
     for _ in range(2):
         steps[0].step(0.02)
         steps[1].step(0.02)
-    for m_ in models:  # same in-place change on both replicas
+    for m_ in models:  # same change on both replicas
         for lay in m_.layers:
             if isinstance(lay, smb.SparseLinearLayer):
-                lay.weights.values.mul_(0.5)
-    steps[0].sync_weights()
+                if how == "in_place":
+                    lay.weights.values.mul_(0.5)
+                elif how == "assign":
+                    lay.weights.values = lay.weights.values * 0.5
+                else:
+                    lay.grad.values.fill_(0.25)
+                    lay.grad_bias = torch.full_like(lay.bias, 0.5)
+                    lay.optimize(0.1)
     # replica 1: a fresh step object on the changed model, same batch order
     fresh = smb.FusedTrainStep(models[1], B)
     fresh.attach_dataset(smb.DeviceDataset(data))
@@ -309,3 +324,29 @@ def test_sync_weights_after_in_place_change():
     torch.cuda.synchronize()
     for (_, a), (_, b) in zip(params_host(models[0]), params_host(models[1])):
         assert bits_equal(a, b)
+
+
+def test_values_identity_stable_across_steps():
+    """A caller holding `layer.weights.values` sees every update in place, as
+    with the reference's in-place sparse_combine (nn.py:187-198): the
+    overlapped step ping-pongs two buffers underneath, but the layer's tensor
+    object is re-pointed at the current one."""
+    chain, B = [3072, 1024, 512, 10], 128
+    data = smb.synthetic_dataset(seed=5, n_samples=B * 8, features=chain[0])
+    model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=chain, density=0.01, seed=6,
+                                                    batch_size=B))
+    held = [lay.weights.values for lay in model.layers if isinstance(lay, smb.SparseLinearLayer)]
+    before = [h.cpu().clone() for h in held]
+    st = smb.FusedTrainStep(model, B)
+    st.attach_dataset(smb.DeviceDataset(data))
+    st.set_epoch(np.arange(B * 8))
+    for n_steps in (1, 2, 3):
+        st.step(0.02)
+        torch.cuda.synchronize()
+        now = [lay.weights.values for lay in model.layers
+               if isinstance(lay, smb.SparseLinearLayer)]
+        for h, cur in zip(held, now):
+            assert h is cur
+            assert h.data_ptr() == cur.data_ptr()
+    for h, b in zip(held, before):
+        assert not torch.equal(h.cpu(), b)  # the held tensors moved with training
