@@ -207,28 +207,6 @@ SMB_API int smb_sddmm_update_into(int dtype, const smb_pattern* pattern, const v
                                   void* grad_bias_out, int opt_kind, double mu, double eta,
                                   void* stream);
 
-/* The whole backward of a wide sparse layer in ONE launch, bit-identical to
- *   smb_spmm_t(pattern, values, d_out, ..., mask = mask ? x : NULL, d_x)
- *   + smb_sddmm_update_into(pattern, d_out, x, ..., values, values_out, ...)
- * (nn.py:178-198 minus the bias side; _kernels.py:40-75; train.py:400-401:
- * d_x uses the pre-update weights).  Both products are walked in CSC order
- * so every d_out row a column gathers feeds the transposed product AND the
- * SDDMM chains of that column (half the L2 traffic of the two kernels).
- * x is the layer input (the post-ReLU activation of the layer below, so
- * mask != 0 applies ReLU.backward as d_x *= (x > 0), nn.py:89-91).  The bias
- * sides of this layer and of the layer below are NOT computed
- * (smb_bias_grad_update).  Valid when smb_backward_fused_supported() (every
- * column holds <= 256 nonzeros).  values_out may equal values; d_x must not
- * overlap d_out or x.  Measured slower than the two separate kernels on B200
- * (shared-memory bound, csrc/bwd_fused.cu), so the fused training step does
- * not use it. */
-SMB_API int smb_backward_fused_supported(int dtype, const smb_pattern* pattern);
-SMB_API int smb_backward_fused(int dtype, const smb_pattern* pattern, const void* d_out,
-                               int64_t ld_dout, const void* x, int64_t ld_x, int64_t n, int mask,
-                               void* d_x, int64_t ld_dx, const void* values, void* values_out,
-                               void* velocity, void* grad_out, int opt_kind, double mu,
-                               double eta, void* stream);
-
 /* grad_bias = row_sums(d_out) (numpy pairwise order) and the bias optimizer
  * update; one warp per row (nn.py:184, 118-131).  Dense layers and any
  * layer whose output gradient was not produced by smb_spmm_t_bias. */
@@ -240,43 +218,6 @@ SMB_API int smb_bias_grad_update(int dtype, const void* d_out, int64_t ld, int64
  * sparse_combine / _step_vector rounding (nn.py:118-131, 187-198). */
 SMB_API int smb_optimizer_step(int dtype, void* param, void* velocity, const void* grad, int64_t count,
                        int opt_kind, double mu, double eta, void* stream);
-
-/* Fused output-layer tail for one batch (nn.py:169-176 forward of the last
- * sparse layer, nn.py:411-417 + train.py:399 softmax-CE gradient / divisor,
- * nn.py:397-408 loss, nn.py:185 spmm_transposed, nn.py:89-91 ReLU.backward
- * of the layer below):
- *   y = W h + bias;  d_y = (softmax(y) - t) / divisor;  loss = summed CE;
- *   d_h = (W^T d_y) * (h > 0)   (mask != 0; h is the post-ReLU input)
- * with every accumulation in the reference's order (bit-identical to
- * smb_spmm + smb_softmax_ce_grad + smb_spmm_t).  Activations are [rows, ld]
- * row-major.  y may be NULL.  step_counter (may be NULL) is advanced modulo
- * `modulo` like smb_softmax_ce_step.  The bias row sums of d_y / d_h are NOT
- * computed (smb_bias_grad_update).  Valid when smb_tail_step_supported()
- * (<= 32 output rows, layer small enough for one CTA's shared memory);
- * workspace: smb_tail_step_workspace_bytes(n) zero-initialised bytes. */
-SMB_API int smb_tail_step_supported(int dtype, const smb_pattern* pattern);
-SMB_API size_t smb_tail_step_workspace_bytes(int64_t n);
-SMB_API int smb_tail_step(int dtype, const smb_pattern* pattern, const void* values,
-                          const void* h, int64_t ld_h, int mask, const void* bias, const void* t,
-                          int64_t ld_t, int64_t n, double divisor, void* y, int64_t ld_y,
-                          void* d_y, int64_t ld_dy, void* d_h, int64_t ld_dh, double* loss_out,
-                          int32_t* step_counter, int32_t modulo, void* workspace, void* stream);
-
-/* Output layer fused with the softmax-CE step, for m <= 12 output rows:
- * y = W h + bias (SparseLinearLayer.forward, nn.py:169-176; row order and
- * rounding of smb_spmm), d_y = (softmax(y) - t) / divisor and the summed loss
- * (nn.py:397-417, train.py:399; arithmetic of smb_softmax_ce_grad).  W in CSR
- * (row_ptr, col_idx, values), m x k.  y may be NULL.  The bias row sums of
- * d_y are not computed (smb_bias_grad_update).  workspace:
- * smb_logits_softmax_workspace_bytes(n) zero-initialised bytes (ticket +
- * per-CTA loss partials). */
-SMB_API size_t smb_logits_softmax_workspace_bytes(int64_t n);
-SMB_API int smb_logits_softmax_step(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
-                                    const void* values, int64_t m, int64_t k, const void* h,
-                                    int64_t ld_h, const void* bias, const void* t, int64_t ld_t,
-                                    int64_t n, double divisor, void* y, int64_t ld_y, void* d_y,
-                                    int64_t ld_dy, double* loss_out, void* workspace,
-                                    void* stream);
 
 /* The data-parallel update pass in one launch: `segments` is a DEVICE array of
  * n_segments (<= 32) records {void* param; void* velocity; const void* grad;
@@ -338,6 +279,22 @@ SMB_API int smb_dense_backward_input(int dtype, const void* w, int64_t ld_w, int
                                      const void* d_out, int64_t ld_d, int64_t n,
                                      const void* mask, int64_t ld_mask, void* d_x,
                                      int64_t ld_dx, void* stream);
+
+/* Weight side of a dense layer of m <= 32 output rows (the ER-saturated
+ * output layer; DenseLinearLayer.backward + optimize, nn.py:241-264):
+ *   grad[i, c] = sum_t d_out[i, t] * x[c, t]   (one sequential chain per
+ *   element over ascending t, multiply and add rounded separately -- the
+ *   SDDMM chain of _kernels.py:62-75 over a full pattern; the reference's
+ *   d @ x.T is numpy BLAS, so parity is tolerance-exact)
+ * then the optimizer update of w[i, c] / velocity[i, c] (_step_vector,
+ * nn.py:118-131) in the same launch.  opt_kind == SMB_OPT_NONE writes the
+ * gradient to grad_out ([m, k] contiguous; data-parallel path) and updates
+ * nothing; grad_out may be NULL otherwise.  d_out [m, ld_d], x [k, ld_x],
+ * w / velocity [m, ld_w]. */
+SMB_API int smb_dense_grad_update(int dtype, const void* d_out, int64_t ld_d, int64_t m,
+                                  const void* x, int64_t ld_x, int64_t k, int64_t n, void* w,
+                                  int64_t ld_w, void* velocity, void* grad_out, int opt_kind,
+                                  double mu, double eta, void* stream);
 
 /* y = W x + bias for a dense layer of m <= 32 output rows (the ER-saturated
  * output layer; DenseLinearLayer.forward, nn.py:241-255 -- numpy BLAS there,

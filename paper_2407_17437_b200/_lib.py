@@ -68,28 +68,12 @@ SIGNATURES = {
     "smb_optimizer_step": (_i32, [_i32, _p, _p, _p, _i64, _i32, _f64, _f64, _p]),
     "smb_dense_backward_input": (
         _i32, [_i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _i64, _p, _i64, _p]),
+    "smb_dense_grad_update": (
+        _i32, [_i32, _p, _i64, _i64, _p, _i64, _i64, _i64, _p, _i64, _p, _p, _i32, _f64, _f64,
+               _p]),
     "smb_dense_forward_workspace_bytes": (C.c_size_t, [_i64, _i64, _i64]),
     "smb_dense_forward_small": (
         _i32, [_i32, _p, _i64, _i64, _i64, _p, _i64, _i64, _p, _p, _i64, _p, _p]),
-    "smb_backward_fused_supported": (_i32, [_i32, _p]),
-    "smb_backward_fused": (
-        _i32,
-        [_i32, _p, _p, _i64, _p, _i64, _i64, _i32, _p, _i64, _p, _p, _p, _p, _i32, _f64, _f64,
-         _p],
-    ),
-    "smb_tail_step_supported": (_i32, [_i32, _p]),
-    "smb_tail_step_workspace_bytes": (C.c_size_t, [_i64]),
-    "smb_tail_step": (
-        _i32,
-        [_i32, _p, _p, _p, _i64, _i32, _p, _p, _i64, _i64, _f64, _p, _i64, _p, _i64, _p, _i64,
-         _p, _p, _i32, _p, _p],
-    ),
-    "smb_logits_softmax_workspace_bytes": (C.c_size_t, [_i64]),
-    "smb_logits_softmax_step": (
-        _i32,
-        [_i32, _p, _p, _p, _i64, _i64, _p, _i64, _p, _p, _i64, _i64, _f64, _p, _i64, _p, _i64,
-         _p, _p, _p],
-    ),
     "smb_optimizer_step_multi": (_i32, [_i32, _p, _i32, _i64, _i32, _f64, _f64, _p]),
     "smb_masked_optimizer_step": (_i32, [_i32, _p, _p, _p, _p, _i64, _i32, _f64, _f64, _p]),
     "smb_row_sums": (_i32, [_i32, _p, _i64, _i64, _i64, _p, _p]),

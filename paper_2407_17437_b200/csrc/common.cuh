@@ -33,6 +33,15 @@ int check_launch(const char* what, uint64_t launches = 1);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// fn(T{}) for the value dtype code (SMB_F32 / SMB_F64)
+template <typename F>
+inline int dispatch_dtype(int dtype, const char* name, F&& fn) {
+  if (dtype == SMB_F32) return fn(float{});
+  if (dtype == SMB_F64) return fn(double{});
+  set_error("%s: unsupported dtype %d", name, dtype);
+  return SMB_ERR_INVALID;
+}
+
 // Opt a kernel into `bytes` of dynamic shared memory, once per kernel per
 // process (device-wide attribute; cheap registry keyed by the entry point).
 void ensure_dynamic_smem(const void* kernel, size_t bytes);

@@ -387,14 +387,6 @@ __global__ void __launch_bounds__(256)
     dst[(f0 + c) * ld_dst + j0 + tx] = tile[tx][c];
 }
 
-template <typename F>
-int dispatch_dtype(int dtype, const char* name, F&& fn) {
-  if (dtype == SMB_F32) return fn(float{});
-  if (dtype == SMB_F64) return fn(double{});
-  set_error("%s: unsupported dtype %d", name, dtype);
-  return SMB_ERR_INVALID;
-}
-
 }  // namespace
 
 template <typename T>

@@ -135,7 +135,6 @@ void free_pattern(smb_pattern* p) {
   cudaFree(p->row_idx);
   cudaFree(p->perm);
   cudaFree(p->tile_row0);
-  cudaFree(p->ctile);
   delete p;
 }
 
@@ -251,34 +250,6 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
     p->span64 = span(64 / kTileGrain);
     p->span128 = span(128 / kTileGrain);
     p->span512 = span(512 / kTileGrain);
-  }
-  {
-    // column tiles of the fused backward: greedy over consecutive columns
-    std::vector<int32_t> cp(k + 1);
-    if (cudaMemcpy(cp.data(), p->col_ptr, sizeof(int32_t) * (k + 1), cudaMemcpyDeviceToHost) !=
-        cudaSuccess)
-      return fail_cuda("column index readback");
-    std::vector<int32_t> tiles;
-    for (int64_t j = 0; j < k; ++j) p->max_col = imax(p->max_col, cp[j + 1] - cp[j]);
-    if (p->max_col <= kBwdTile && k > 0) {
-      // long columns fill a tile with a few of them: reserve staging rows for
-      // kBwdColsLong x rows only (smaller stages, more CTAs per SM)
-      p->bwd_cols = (nnz >= 32 * k) ? kBwdColsLong : kBwdCols;
-      int64_t j = 0;
-      while (j < k) {
-        tiles.push_back((int32_t)j);
-        const int32_t q0 = cp[j];
-        int64_t e = j + 1;
-        while (e < k && e - j < p->bwd_cols && cp[e + 1] - q0 <= kBwdTile) ++e;
-        j = e;
-      }
-      tiles.push_back((int32_t)k);
-      p->n_ctiles = (int64_t)tiles.size() - 1;
-      if (cudaMalloc(&p->ctile, sizeof(int32_t) * tiles.size()) != cudaSuccess ||
-          cudaMemcpy(p->ctile, tiles.data(), sizeof(int32_t) * tiles.size(),
-                     cudaMemcpyHostToDevice) != cudaSuccess)
-        return fail_cuda("column tile index");
-    }
   }
   *out = p;
   return SMB_OK;

@@ -17,20 +17,9 @@ struct smb_pattern {
   // most rows spanned by any tile of 32 / 64 / 128 / 512 consecutive nonzeros
   // (aligned; first row .. row of the last nonzero)
   int64_t span32 = 0, span64 = 0, span128 = 0, span512 = 0;
-  // column tiles of the fused backward (bwd_fused.cu): whole consecutive
-  // columns, <= kBwdTile nonzeros and <= kBwdCols columns each; ctile[t] is
-  // the first column of tile t, ctile[n_ctiles] = k.  n_ctiles = 0 when some
-  // column holds more than kBwdTile nonzeros (fused backward unsupported).
-  int32_t* ctile = nullptr;  // owned, [n_ctiles + 1]
-  int64_t n_ctiles = 0;
-  int64_t max_col = 0;  // longest column (nonzeros)
-  int bwd_cols = 0;     // column cap of the tiles: kBwdColsLong or kBwdCols
 };
 
 namespace smb {
 constexpr int kSddmmTile = 128;  // nonzeros per SDDMM CTA (one per thread)
 constexpr int kTileGrain = 32;   // granularity of the tile -> first-row table
-constexpr int kBwdTile = 256;    // nonzeros per fused-backward CTA (one per thread)
-constexpr int kBwdCols = 32;     // columns per fused-backward CTA (short columns)
-constexpr int kBwdColsLong = 8;  // ... when columns average >= 32 nonzeros
 }

@@ -416,12 +416,6 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
                                          : pat->span512;
       return span <= tile / sd;
     };
-    // tuning experiments only (scripts/gpu_sddmm_var2.sh): 1 = 512-nonzero
-    // tiles x 32 columns, 2 = 128 x 16 x 8 stages, 3 = warp-independent
-    static const int variant = [] {
-      const char* e = getenv("SMB_SDDMM_VARIANT");
-      return e ? atoi(e) : 0;
-    }();
 #define SMB_GO_SD(TL, CHK, STG, SDV)                                                      \
   do {                                                                                     \
     using C = SddmmCfg<T, TL, CHK, STG, SDV>;                                              \
@@ -445,7 +439,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     // many waves and every 128-tile within kWarpDSlots rows (>= ~10 nonzeros
     // per row): warp-independent staging, no CTA barrier (1.1-1.2x at
     // config 3 d >= 0.01; measured slower when rows are short)
-    const bool warp_kernel = sizeof(T) == 4 && vec && variant == 0 && !wave &&
+    const bool warp_kernel = sizeof(T) == 4 && vec && !wave &&
                              pat->span128 <= kWarpDSlots;
     // Small layers (a few waves of 32 / 64-nonzero tiles): the chains set the
     // time, so spread them over as many SMs as possible with deeper rings
@@ -453,18 +447,17 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     // and 512x1024 14.4 -> 8.3 us with 32-tiles, 1024x3072 22.6 -> 16.5 us
     // with 64-tiles).
     const int64_t small_cap = 4 * 148;
-    const bool small32 = (variant == 0 || variant == 4) && ceil_div(pat->nnz, 32) <= small_cap;
-    const bool small64 = (variant == 0 || variant == 4) && !small32 &&
+    const bool small32 = ceil_div(pat->nnz, 32) <= small_cap;
+    const bool small64 = !small32 &&
                          ceil_div(pat->nnz, 64) <= small_cap;
     // One wave of 32-nonzero tiles with 4-stage rings (23 KB, up to 9 CTAs
     // per SM) beyond that: config-2 layer 0 (1024 x 3072) 16.3 -> 15.0 us
     // against 64-nonzero tiles (graph-timed, scripts/sddmm_lab.cu)
-    // (SMB_SDDMM_VARIANT=4: the 64-nonzero tiles instead, for comparison)
-    const bool mid32 = variant == 0 && ceil_div(pat->nnz, 32) > small_cap &&
+    const bool mid32 = ceil_div(pat->nnz, 32) > small_cap &&
                        ceil_div(pat->nnz, 32) <= 9 * 148 && all_for(32, 4);
     bool warp_done = false;
     if constexpr (sizeof(T) == 4) {
-      if (!small32 && !small64 && !mid32 && (warp_kernel || (vec && variant == 3))) {
+      if (!small32 && !small64 && !mid32 && warp_kernel) {
         go(sddmm_warp_kernel<T, 32, 2>, 128, SddmmWarpCfg<T, 32, 2>::smem_bytes);
         warp_done = true;
       }
@@ -481,8 +474,6 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     else if (sizeof(T) == 4 && small32) SMB_GO_SD(32, 32, 8, 1);
     else if (sizeof(T) == 4 && small64 && !mid32 && all_for(64, 4)) SMB_GO_SD(64, 32, 4, 4);
     else if (sizeof(T) == 4 && small64) SMB_GO_SD(64, 32, 4, 1);
-    else if (sizeof(T) == 4 && variant == 1) SMB_GO_SD(512, 32, 2, 4);
-    else if (sizeof(T) == 4 && variant == 2) SMB_GO_SD(128, 16, 8, 4);
     else if (sizeof(T) == 4 && wave && sparse_rows) SMB_GO_SD(128, 64, 2, 1);
     else if (sizeof(T) == 4 && wave) SMB_GO_SD(128, 64, 2, 4);
     else if (sizeof(T) == 4 && sparse_rows) SMB_GO_SD(128, 32, 2, 1);

@@ -506,74 +506,6 @@ __global__ void __launch_bounds__(32)
   out[row * ld_out + col] = acc;
 }
 
-// Output layer fused with the softmax-CE step (nn.py:169-176, 397-417,
-// train.py:399): CTA = 32 batch columns, warp r = output row r (m <= 12).
-// Each warp runs deep_row_chain for its row (+ bias), the logits meet in
-// shared memory, and warp 0 computes every column's softmax-CE gradient /
-// divisor and loss with softmax_step_kernel's arithmetic.  Per-CTA loss
-// partials are summed in CTA order by the last CTA (ticket).  The bias row
-// sums of d_y are left to smb_bias_grad_update (they cross columns).
-constexpr int kLogitsMaxRows = 12;  // 384 threads: ~170 registers per thread for the chain
-
-template <typename T>
-__global__ void __launch_bounds__(32 * kLogitsMaxRows)
-    logits_softmax_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                          const T* __restrict__ vals, int m, const T* __restrict__ h,
-                          int64_t ld_h, int64_t n, const T* __restrict__ bias,
-                          const T* __restrict__ t, int64_t ld_t, T divisor, T* __restrict__ y,
-                          int64_t ld_y, T* __restrict__ dy, int64_t ld_dy, double* loss_out,
-                          double* loss_parts, unsigned* ticket) {
-  __shared__ T s_y[kLogitsMaxRows][33];
-  __shared__ bool s_last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t col = (int64_t)blockIdx.x * 32 + lane;
-  const bool valid = col < n;
-  const T b = (bias != nullptr) ? bias[warp] : T(0);
-  T acc = deep_row_chain<T, false>(row_ptr, col_idx, nullptr, vals, h + (valid ? col : 0),
-                                   (uint32_t)ld_h, warp, lane);
-  if (bias != nullptr) acc = add_rn(acc, b);
-  s_y[warp][lane] = acc;
-  if (y != nullptr && valid) y[warp * ld_y + col] = acc;
-  pdl_trigger();
-  __syncthreads();
-  if (warp != 0) return;
-  double local = 0.0;
-  if (valid) {
-    T mx = s_y[0][lane];
-    for (int c = 1; c < m; ++c) {
-      const T v = s_y[c][lane];
-      mx = (v > mx || v != v) ? v : mx;
-    }
-    T ssum = T(0), zt = T(0);
-    for (int c = 0; c < m; ++c) {
-      const T z = sub_rn(s_y[c][lane], mx);
-      const T e = exp_full(z);
-      s_y[c][lane] = e;
-      ssum = add_rn(ssum, e);
-      zt = add_rn(zt, mul_rn(z, t[c * ld_t + col]));
-    }
-    for (int c = 0; c < m; ++c)
-      dy[c * ld_dy + col] = div_rn(sub_rn(div_rn(s_y[c][lane], ssum), t[c * ld_t + col]), divisor);
-    local = static_cast<double>(sub_rn(log_full(ssum), zt));
-  }
-  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
-  if (lane == 0) {
-    if (gridDim.x == 1) {
-      if (loss_out) *loss_out = local;
-      return;
-    }
-    loss_parts[blockIdx.x] = local;
-    __threadfence();
-    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-    if (s_last) {
-      __threadfence();
-      double tot = 0.0;
-      for (unsigned c = 0; c < gridDim.x; ++c) tot += loss_parts[c];
-      if (loss_out) *loss_out = tot;
-      *ticket = 0u;  // ready for the next launch / graph replay
-    }
-  }
-}
 
 template <typename T, int W, int U, int EPI, bool PERM>
 bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm, const T* vals,
@@ -890,42 +822,5 @@ extern "C" int smb_spmm_t_bias(int dtype, const smb_pattern* pat, const void* va
                                      bias, velocity_bias, grad_bias_out, opt_kind, mu, eta,
                                      stream);
   set_error("smb_spmm_t_bias: unsupported dtype %d", dtype);
-  return SMB_ERR_INVALID;
-}
-
-extern "C" size_t smb_logits_softmax_workspace_bytes(int64_t n) {
-  return 256 + sizeof(double) * (size_t)ceil_div(n > 0 ? n : 1, 32);
-}
-
-extern "C" int smb_logits_softmax_step(int dtype, const int32_t* row_ptr, const int32_t* col_idx,
-                                       const void* values, int64_t m, int64_t k, const void* h,
-                                       int64_t ld_h, const void* bias, const void* t,
-                                       int64_t ld_t, int64_t n, double divisor, void* y,
-                                       int64_t ld_y, void* d_y, int64_t ld_dy, double* loss_out,
-                                       void* workspace, void* stream) {
-  clear_error();
-  SMB_REQUIRE(m >= 1 && m <= kLogitsMaxRows && k >= 1,
-              "smb_logits_softmax_step: needs 1 <= m <= %d output rows", kLogitsMaxRows);
-  SMB_REQUIRE(n >= 1 && n <= (int64_t(1) << 30), "smb_logits_softmax_step: bad batch width");
-  SMB_REQUIRE(ld_h >= n && ld_t >= n && ld_dy >= n && (y == nullptr || ld_y >= n),
-              "smb_logits_softmax_step: leading dimension");
-  SMB_REQUIRE(divisor != 0.0, "smb_logits_softmax_step: zero divisor");
-  SMB_REQUIRE(row_ptr && col_idx && values && h && t && d_y, "smb_logits_softmax_step: null pointer");
-  const unsigned grid = (unsigned)ceil_div(n, 32);
-  SMB_REQUIRE(grid == 1 || workspace != nullptr, "smb_logits_softmax_step: workspace required");
-  unsigned* ticket = static_cast<unsigned*>(workspace);
-  double* parts =
-      workspace ? reinterpret_cast<double*>(static_cast<char*>(workspace) + 256) : nullptr;
-  auto go = [&](auto tag) {
-    using T = decltype(tag);
-    launch_k(logits_softmax_kernel<T>, dim3(grid), dim3((unsigned)(32 * m)), 0, as_stream(stream),
-             row_ptr, col_idx, static_cast<const T*>(values), (int)m, static_cast<const T*>(h),
-             ld_h, n, static_cast<const T*>(bias), static_cast<const T*>(t), ld_t, T(divisor),
-             static_cast<T*>(y), ld_y, static_cast<T*>(d_y), ld_dy, loss_out, parts, ticket);
-    return check_launch("smb_logits_softmax_step");
-  };
-  if (dtype == SMB_F32) return go(float{});
-  if (dtype == SMB_F64) return go(double{});
-  set_error("smb_logits_softmax_step: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
 }

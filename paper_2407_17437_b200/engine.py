@@ -186,8 +186,7 @@ class _Unit:
 
 class FusedTrainStep:
     def __init__(self, model, batch_size: int, global_batch: int | None = None,
-                 process_group=None, use_graph: bool = True, fuse_tail: bool | None = None,
-                 force_dp: bool = False, fuse_logits: bool = False,
+                 process_group=None, use_graph: bool = True, force_dp: bool = False,
                  bucketed: bool | None = None):
         self.units = self._parse(model)
         self.model = model
@@ -257,30 +256,6 @@ class FusedTrainStep:
             for u, (g_off, b_off) in zip(self.units, layout):
                 u.grad_off, u.bias_off = g_off, b_off
             self.flat = torch.zeros(total, dtype=f32, device=dev)
-        # fused output-layer tail (smb_tail_step: last layer sparse, no
-        # activation, <= 32 outputs, small enough for one CTA's smem).  Off by
-        # default: on B200 at the config-2 point it measured ~10 us slower
-        # than spmm + softmax step + spmm_t; SMB_FUSE_TAIL=1 or
-        # fuse_tail=True selects it.
-        top = self.units[-1]
-        self.tail_ok = bool(
-            len(self.units) >= 2 and top.sparse and not top.relu
-            and _lib.load().smb_tail_step_supported(_lib.SMB_F32,
-                                                    top.layer.weights.pattern.handle))
-        want = fuse_tail if fuse_tail is not None else os.environ.get("SMB_FUSE_TAIL") == "1"
-        self.fuse_tail = bool(want and self.tail_ok)
-        self._tail_ws = torch.zeros(int(_lib.load().smb_tail_step_workspace_bytes(self.B)),
-                                    dtype=torch.uint8, device=dev) if self.tail_ok else None
-        # output layer fused with the softmax step (smb_logits_softmax_step:
-        # last layer sparse, no activation, <= 12 outputs, after >= 1 layer).
-        # Off by default: at config 2 it measured ~1 us/step slower than the
-        # separate deep kernel (320 one-warp CTAs) + softmax step -- the fused
-        # CTAs put all ten row chains of 32 columns on one SM.
-        self.logits_ok = bool(len(self.units) >= 2 and top.sparse and not top.relu
-                              and top.m <= 12)
-        self.fuse_logits = bool(fuse_logits and self.logits_ok)
-        self._ls_ws = torch.zeros(int(_lib.load().smb_logits_softmax_workspace_bytes(self.B)),
-                                  dtype=torch.uint8, device=dev) if self.logits_ok else None
         # single GPU: bias row sums of transposed-SpMM outputs on a side stream
         # instead of fused into the critical-path kernel's epilogue
         self.split_bias = True
@@ -537,11 +512,9 @@ class FusedTrainStep:
         # gather steps: this batch is already in x_in / t_in (prefetched by
         # the previous step or by step()'s prologue); the next one is
         # gathered into the other slot on its own stream, beside the layer-0
-        # SDDMM at the end of
-        # the backward (measured 78.2 -> 76.5 us/step at config 2 against
-        # launching it at the step start, where it competed with the
-        # L2-bound first-layer SpMM); SMB_PREFETCH_AT=start restores that
-        prefetch_at = os.environ.get("SMB_PREFETCH_AT", "end")
+        # SDDMM at the end of the backward (measured 78.2 -> 76.5 us/step at
+        # config 2 against launching it at the step start, where it competed
+        # with the L2-bound first-layer SpMM)
 
         def prefetch():
             # (serialised on the main stream when overlap is off: the
@@ -549,17 +522,10 @@ class FusedTrainStep:
             with torch.cuda.stream(fork("prefetch")) if overlap else _nullctx():
                 self._gather_into(1 - self._slot, stream_ptr(), ahead=True)
 
-        if gather and prefetch_at == "start":
-            prefetch()
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
-        tail = self.fuse_tail
-        logits = self.fuse_logits and not tail
-        L = len(self.units)
         for li, (u, a) in enumerate(zip(self.units, self.acts)):
             lay = u.layer
-            if (tail or logits) and li == L - 1:
-                break
             if u.sparse:
                 self._call(f"spmm[{li}]", "smb_spmm_p", F32, lay.weights.pattern.handle,
                            ptr(self._vals(u)), ptr(x), ld, B, ptr(lay.bias),
@@ -580,37 +546,7 @@ class FusedTrainStep:
         # applies the last layer's bias side and advances the step counter
         top = self.units[-1]
         b, vb, gb, kind, mu = self._bias_target(top, fuse_update)
-        if tail:
-            # one launch: logits -> softmax-CE gradient / B_global (+ loss,
-            # step counter) -> d_{L-2} = (W_top^T d_top) * mask
-            below = self.units[-2]
-            self._call("tail", "smb_tail_step", F32, top.layer.weights.pattern.handle,
-                       ptr(self._vals(top)), ptr(self.acts[-2]), ld, 1 if below.relu else 0,
-                       ptr(top.layer.bias), ptr(t_in), ld, B, float(self.B_global),
-                       ptr(self.acts[-1]), ld, ptr(self.dys[-1]), ld, ptr(self.dys[-2]), ld,
-                       ptr(self.loss), None, 0, ptr(self._tail_ws), st)
-            # the bias sides of the top two layers cross columns: beside the
-            # critical path when overlapping
-            sides = ((top, self.dys[-1]), (below, self.dys[-2]))
-            with torch.cuda.stream(fork("bias")) if overlap else _nullctx():
-                sst = stream_ptr()
-                for u, d_u in sides:
-                    bb, bv, bg, bk, bmu = self._bias_target(u, fuse_update)
-                    self._call(f"bias[{u.index}]", "smb_bias_grad_update", F32, ptr(d_u), ld, u.m,
-                               B, bb, bv, bg, bk, bmu, float(eta), sst)
-        elif logits:
-            # output layer + softmax-CE step in one launch; the bias row sums
-            # of d_y (they cross columns) beside the critical path
-            lw = top.layer.weights
-            self._call("logits_softmax", "smb_logits_softmax_step", F32, ptr(lw.row_ptr),
-                       ptr(lw.col_idx), ptr(lw.values), top.m, top.k, ptr(self.acts[-2]), ld,
-                       ptr(top.layer.bias), ptr(t_in), ld, B, float(self.B_global),
-                       ptr(self.acts[-1]), ld, ptr(self.dys[-1]), ld, ptr(self.loss),
-                       ptr(self._ls_ws), st)
-            with torch.cuda.stream(fork(("weights", L - 1))) if overlap else _nullctx():
-                self._call(f"bias[{top.index}]", "smb_bias_grad_update", F32, ptr(self.dys[-1]),
-                           ld, top.m, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
-        elif overlap:
+        if overlap:
             # the column-parallel softmax step on the critical path; the last
             # layer's bias row sums + update (they cross columns) beside it
             self._call("softmax_ce", "smb_softmax_ce_step", F32, ptr(self.acts[-1]), ld,
@@ -638,7 +574,7 @@ class FusedTrainStep:
             if overlap and u.sparse:
                 with torch.cuda.stream(fork(("weights", li))):  # d_l is ready
                     self._weight_side(u, dy, x_prev, eta, fuse_update, stream_ptr())
-            if li > 0 and not (tail and li == L - 1):  # the tail produced d_{L-2}
+            if li > 0:
                 below = self.units[li - 1]
                 mask = self.acts[li - 1] if below.relu else None
                 dst = self.dys[li - 1]
@@ -700,7 +636,7 @@ class FusedTrainStep:
                 with torch.cuda.stream(fork(("weights", li)) if overlap else main):
                     self._allreduce_bucket(u)
                     self._update_unit_from_flat(u, eta, stream_ptr())
-        if gather and prefetch_at != "start":
+        if gather:
             prefetch()
         for s_ in forked:
             main.wait_stream(s_)  # join: the step ends when every update has
@@ -752,7 +688,17 @@ class FusedTrainStep:
                            lay.weights.pattern.handle, ptr(w_out),
                            ptr(u.vals_csc[self._parity ^ 1]), st)
             return
-        # dense layer: cuBLAS FP32 weight gradient + exact update
+        if u.m <= DENSE_T_MAX_ROWS and lay.mask is None:
+            # ER-saturated output layer: gradient chains + update in one
+            # launch (smb_dense_grad_update), no dense gradient round trip
+            vel = lay.velocity.view(-1) if lay.velocity is not None else None
+            g_out = None if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals]
+            self._call(f"dense_grad[{u.index}]", "smb_dense_grad_update", F32, ptr(dy), ld, u.m,
+                       ptr(x_prev), ld, u.k, B, ptr(lay.weights), u.k, ptr(vel), ptr(g_out),
+                       kind, float(opt.mu), float(eta), st)
+            return
+        # wider dense / masked-dense baseline layer: cuBLAS FP32 weight
+        # gradient + exact (masked) update
         gw = lay.grad if fuse_update else self.flat[u.grad_off:u.grad_off + u.nvals].view(u.m, u.k)
         with _no_tf32():
             torch.mm(dy[:, :B], x_prev[:, :B].T, out=gw)

@@ -313,8 +313,21 @@ class DenseLinearLayer:
         if x is None:
             raise StateError("backward called before forward")
         d = _act(d_out, self.n_out, self.weights.dtype)
+        small = self.n_out <= DENSE_T_MAX_ROWS and self.mask is None
+        if small:
+            # ER-saturated output layer: one sequential chain per gradient
+            # element (smb_dense_grad_update, the fused step's kernel; numpy
+            # BLAS order is unspecified, nn.py:241-255)
+            d = d.contiguous()
+            if x.shape[1] > 1 and (x.stride(1) != 1 or x.stride(0) < x.shape[1]):
+                x = x.contiguous()
+            self.grad = torch.empty_like(self.weights)
+            _lib.call("smb_dense_grad_update", dtype_code(d.dtype), ptr(d), _ld(d), self.n_out,
+                      ptr(x), _ld(x), self.n_in, d.shape[1], None, self.n_in, None,
+                      ptr(self.grad), _lib.SMB_OPT_NONE, 0.0, 0.0, stream_ptr())
         with _no_tf32():
-            self.grad = d @ x.T
+            if not small:
+                self.grad = d @ x.T
             if self.mask is not None:
                 self.grad *= self.mask
             if self.n_out > DENSE_T_MAX_ROWS:

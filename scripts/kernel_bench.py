@@ -67,14 +67,8 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
                 elif kind == "sddmm_update":
                     _lib.call("smb_sddmm_update", 0, pat.handle, ptr(dY), B, ptr(X), B, B,
                               ptr(vals), ptr(vel), None, None, None, None, 3, 0.9, 1e-6, st)
-                else:  # spmm_t (masked by X) + SDDMM + update in one CSC-order launch
-                    _lib.call("smb_backward_fused", 0, pat.handle, ptr(dY), B, ptr(X), B, B, 1,
-                              ptr(out), B, ptr(vals), ptr(vals), ptr(vel), None, 3, 0.9, 1e-6, st)
 
             kinds = ["spmm", "spmm_t", "sddmm_update"]
-            fused_ok = _lib.load().smb_backward_fused_supported(0, pat.handle) == 1
-            if fused_ok:
-                kinds.append("bwd_fused")
             for kind in ["flush"] + kinds:
                 launch(kind) if kind != "flush" else None  # kernel attributes outside capture
                 g = torch.cuda.CUDAGraph()
@@ -101,14 +95,6 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
                 res[kind] -= t_flush
             bs = bytes_model(n, n, nnz, B)
             rec = {"density": d, "nnz": nnz, "B": B}
-            if fused_ok:
-                # spmm_t + SDDMM/update of one layer, staged once in CSC order
-                sep = res["spmm_t"] + res["sddmm_update"]
-                rec["bwd_fused"] = {"us": round(res["bwd_fused"], 2),
-                                    "separate_us": round(sep, 2),
-                                    "speedup": round(sep / res["bwd_fused"], 3),
-                                    "l2_gather_frac": round(4 * nnz * B / (L2_GATHER * 1e9)
-                                                            / (res["bwd_fused"] * 1e-6), 3)}
             for (kind, us), b in zip(list(res.items())[:3], bs):
                 # t_roof = max(bytes / HBM, 2 z B / FP32 peak)
                 t_roof = max(b / (HBM * 1e9), 2 * nnz * B / (FP32_TFLOPS * 1e12))

@@ -25,7 +25,7 @@ def time_with(skip):
         model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=LAYERS, density=DENS,
                                                         batch_size=B, lr=0.01),
                                    large_patterns=large)
-        st = smb.FusedTrainStep(model, B, fuse_logits=os.environ.get("ABL_FUSE_LOGITS") == "1")
+        st = smb.FusedTrainStep(model, B)
         st.attach_dataset(ddata)
         st.set_epoch(np.arange(data.Xtrain.shape[1]))
         for _ in range(6): st.step(0.01)

@@ -291,47 +291,6 @@ def test_softmax_ce_gradient_tolerance():
     assert abs(smb.softmax_ce_loss(dev(y), dev(t)) - loss_want) <= 1e-4 * abs(loss_want)
 
 
-@pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("n", [1024, 100, 37, 1])
-@pytest.mark.parametrize("mask", [True, False])
-def test_tail_step_equals_unfused_ops(dtype, n, mask):
-    """smb_tail_step == smb_spmm(+bias) -> smb_softmax_ce_grad(/divisor) ->
-    smb_spmm_t(*mask), bit for bit; loss within fp64 summation-order noise."""
-    from paper_2407_17437_b200 import _lib
-
-    rng = np.random.default_rng(n + (7 if mask else 0))
-    m, k = 10, 300
-    rp, ci, v, _ = random_csr(rng, m, k, 0.4, dtype, empty_rows=True)
-    s = smb.CsrMatrix(m, k, rp, ci, v)
-    code = tc.dtype_code(s.values.dtype)
-    assert _lib.load().smb_tail_step_supported(code, s.pattern.handle) == 1
-    h = dev(np.maximum(rng.standard_normal((k, n)), 0).astype(dtype))
-    bias = dev(rng.standard_normal(m).astype(dtype))
-    lab = rng.integers(0, m, n)
-    t = np.zeros((m, n), dtype)
-    t[lab, np.arange(n)] = 1
-    t = dev(t)
-    divisor = float(n + 3)
-    # unfused reference path (the layer API's kernels)
-    y_ref = smb.spmm(s, h, bias=bias)
-    dy_ref, loss_ref = smb.nn._ce_call(y_ref, t, divisor)
-    dh_ref = smb.spmm_transposed(s, dy_ref, mask=h if mask else None)
-    # fused
-    T = s.values.dtype
-    y = torch.empty((m, n), dtype=T, device="cuda")
-    dy = torch.empty_like(y)
-    dh = torch.empty((k, n), dtype=T, device="cuda")
-    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ws = torch.zeros(int(_lib.load().smb_tail_step_workspace_bytes(n)), dtype=torch.uint8,
-                     device="cuda")
-    _lib.call("smb_tail_step", code, s.pattern.handle, tc.ptr(s.values), tc.ptr(h), n,
-              1 if mask else 0, tc.ptr(bias), tc.ptr(t), n, n, divisor, tc.ptr(y), n,
-              tc.ptr(dy), n, tc.ptr(dh), n, tc.ptr(loss), None, 0, tc.ptr(ws), tc.stream_ptr())
-    assert bits_equal(host(y), host(y_ref))
-    assert bits_equal(host(dy), host(dy_ref))
-    assert bits_equal(host(dh), host(dh_ref))
-    assert abs(float(loss) - float(loss_ref)) <= 1e-12 * max(1.0, abs(float(loss_ref)))
-    assert int(ws[:4].view(torch.int32)) == 0  # ticket reset for the next launch
 
 
 @pytest.mark.parametrize("relu", [True, False])
@@ -389,39 +348,6 @@ def test_few_long_rows_wide_batch_bit_exact(oracle, shape, density):
     assert bits_equal(smb.spmm_transposed(st, d, mask=dev(mk)), want)
 
 
-@pytest.mark.parametrize("m,k,n", [(10, 512, 1024), (12, 300, 37), (3, 100, 1), (10, 2000, 100)])
-def test_logits_softmax_step_equals_unfused(m, k, n):
-    """smb_logits_softmax_step == smb_spmm (+bias) -> smb_softmax_ce_grad
-    (/divisor), bit for bit; loss within fp64 summation-order noise."""
-    from paper_2407_17437_b200 import _lib
-
-    rng = np.random.default_rng(m * 1000 + n)
-    rp, ci, v, _ = random_csr(rng, m, k, 0.5, np.float32, empty_rows=True)
-    s = smb.CsrMatrix(m, k, rp, ci, v)
-    h = dev(np.maximum(rng.standard_normal((k, n)), 0).astype(np.float32))
-    bias = dev(rng.standard_normal(m).astype(np.float32))
-    t = np.zeros((m, n), np.float32)
-    t[rng.integers(0, m, n), np.arange(n)] = 1
-    t = dev(t)
-    divisor = float(n + 5)
-    y_ref = smb.spmm(s, h, bias=bias)
-    dy_ref, loss_ref = smb.nn._ce_call(y_ref, t, divisor)
-    y = torch.empty((m, n), device="cuda")
-    dy = torch.empty_like(y)
-    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
-    ws = torch.zeros(int(_lib.load().smb_logits_softmax_workspace_bytes(n)), dtype=torch.uint8,
-                     device="cuda")
-    _lib.call("smb_logits_softmax_step", _lib.SMB_F32, tc.ptr(s.row_ptr), tc.ptr(s.col_idx),
-              tc.ptr(s.values), m, k, tc.ptr(h), n, tc.ptr(bias), tc.ptr(t), n, n, divisor,
-              tc.ptr(y), n, tc.ptr(dy), n, tc.ptr(loss), tc.ptr(ws), tc.stream_ptr())
-    assert bits_equal(host(y), host(y_ref))
-    assert bits_equal(host(dy), host(dy_ref))
-    assert abs(float(loss) - float(loss_ref)) <= 1e-12 * max(1.0, abs(float(loss_ref)))
-    assert int(ws[:4].view(torch.int32)) == 0
-    with pytest.raises(smb.InvalidArgumentError):  # > 12 output rows
-        _lib.call("smb_logits_softmax_step", _lib.SMB_F32, tc.ptr(s.row_ptr), tc.ptr(s.col_idx),
-                  tc.ptr(s.values), 13, k, tc.ptr(h), n, None, tc.ptr(t), n, n, divisor, None, 0,
-                  tc.ptr(dy), n, tc.ptr(loss), tc.ptr(ws), tc.stream_ptr())
 
 
 @pytest.mark.parametrize("n", [1024, 100, 37])
@@ -570,3 +496,43 @@ def test_dense_forward_small_matches_blas(dtype, m, k, n):
     # rounding of a k-term fp32 sum grows ~sqrt(k) (cuBLAS / numpy BLAS alike)
     tol = (1e-5 if dtype == np.float32 else 1e-12) * max(1.0, np.sqrt(k) / 16)
     assert rel_err(y1, want) <= tol
+
+
+@pytest.mark.parametrize("m,k,n", [(10, 8192, 1024), (10, 512, 100), (3, 1000, 37),
+                                   (32, 700, 1), (17, 300, 64), (10, 65536, 8)])
+@pytest.mark.parametrize("kind", ["none", "nesterov"])
+def test_dense_grad_update_is_full_pattern_sddmm(oracle, m, k, n, kind):
+    """smb_dense_grad_update (the ER-saturated output layer's weight side,
+    DenseLinearLayer.backward + optimize, nn.py:241-264): every gradient
+    element is the SDDMM chain of _kernels.py:62-75 over a full pattern --
+    bit-identical to the oracle's sddmm of an all-ones CSR pattern -- and the
+    fused update follows the exact _step_vector sequence."""
+    rng = np.random.default_rng(m * 7 + k + n)
+    d = rng.standard_normal((m, n)).astype(np.float32)
+    x = rng.standard_normal((k, n)).astype(np.float32)
+    w = rng.standard_normal((m, k)).astype(np.float32)
+    v = (0.1 * rng.standard_normal((m, k))).astype(np.float32)
+    row_ptr = (np.arange(m + 1) * k).astype(np.int32)
+    col_idx = np.tile(np.arange(k, dtype=np.int32), m)
+    g_ref = oracle.sddmm(row_ptr, col_idx, d, x).reshape(m, k)
+    dt, xt = torch.from_numpy(d).cuda(), torch.from_numpy(x).cuda()
+    wt, vt = torch.from_numpy(w).cuda(), torch.from_numpy(v).cuda()
+    gt = torch.empty(m, k, device="cuda")
+    mu, eta = 0.9, 0.05
+    opt = _lib.SMB_OPT_NONE if kind == "none" else _lib.SMB_OPT_NESTEROV
+    _lib.call("smb_dense_grad_update", _lib.SMB_F32, tc.ptr(dt), n, m, tc.ptr(xt), n, k, n,
+              tc.ptr(wt), k, tc.ptr(vt), tc.ptr(gt), opt, mu, eta, tc.stream_ptr())
+    torch.cuda.synchronize()
+    assert bits_equal(gt.cpu().numpy(), g_ref)
+    # within tolerance of the reference's numpy BLAS product d @ x.T
+    assert rel_err(gt.cpu().numpy(), d @ x.T) <= 1e-4
+    if kind == "nesterov":
+        v_ref, w_ref = v.reshape(-1).copy(), w.reshape(-1).copy()
+        g = g_ref.reshape(-1)
+        oracle.axpby(mu, v_ref, 1.0, g)
+        oracle.axpby(1.0, w_ref, -eta * mu, v_ref)
+        oracle.axpby(1.0, w_ref, -eta, g)
+        assert bits_equal(vt.cpu().numpy().reshape(-1), v_ref)
+        assert bits_equal(wt.cpu().numpy().reshape(-1), w_ref)
+    else:  # OPT_NONE leaves the parameters alone
+        assert bits_equal(wt.cpu().numpy(), w) and bits_equal(vt.cpu().numpy(), v)

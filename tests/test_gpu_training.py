@@ -80,14 +80,12 @@ def test_initial_weights_bit_exact(oracle, chain, density, seed):
         assert np.array_equal(rp, rl.row_ptr) and np.array_equal(ci, rl.col_idx)
 
 
-def _fused_and_layerwise(chain, density, seed, B, steps, eta=0.05, fuse_tail=False,
-                         fuse_logits=False):
+def _fused_and_layerwise(chain, density, seed, B, steps, eta=0.05):
     data = smb.synthetic_dataset(seed=seed, n_samples=B * steps, features=chain[0])
     cfg = smb.ExperimentConfig(layer_dims=chain, density=density, seed=seed, batch_size=B, lr=eta)
     m_fused, _ = smb.build_model(cfg)
     m_layer, _ = smb.build_model(cfg)
-    step = smb.FusedTrainStep(m_fused, B, fuse_tail=fuse_tail, fuse_logits=fuse_logits)
-    assert step.fuse_tail == (fuse_tail and step.tail_ok)
+    step = smb.FusedTrainStep(m_fused, B)
     step.attach_dataset(smb.DeviceDataset(data))
     perm = np.random.default_rng(seed).permutation(B * steps)
     step.set_epoch(perm)
@@ -121,21 +119,6 @@ def test_fused_step_equals_layer_api_bitwise(chain, density, B):
         assert bits_equal(a, b), n1
 
 
-@pytest.mark.parametrize("chain,density,B", [
-    ([3072, 1024, 512, 10], 0.01, 1024),
-    ([3072, 1024, 512, 10], 0.01, 37),
-    ([200, 300, 10], 0.2, 100),
-])
-@pytest.mark.parametrize("variant", ["tail", "logits"])
-def test_fused_tail_step_equals_layer_api_bitwise(chain, density, B, variant):
-    """The opt-in output-layer fusions inside the step: smb_tail_step and
-    smb_logits_softmax_step."""
-    m_fused, m_layer = _fused_and_layerwise(chain, density, 5, B, steps=4,
-                                            fuse_tail=variant == "tail",
-                                            fuse_logits=variant == "logits")
-    for (n1, a), (n2, b) in zip(params_host(m_fused), params_host(m_layer)):
-        assert n1 == n2
-        assert bits_equal(a, b), n1
 
 
 def test_graph_replay_equals_eager():
