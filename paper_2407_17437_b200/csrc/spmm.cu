@@ -102,17 +102,27 @@ struct EpiArgs {
 template <int W>
 constexpr int max_threads_for() { return 256; }
 
+// A CTA holds rows_per_cta rows x (nwarps / rows_per_cta) warps per row; its
+// warps own consecutive 32*W-column chunks of the batch.  Launch order is
+// blockIdx.x fastest, so all rows of one column slice (blockIdx.y) run
+// before the next slice: when the dense operand is wider than L2, the slice
+// width is chosen so the slice's rows stay L2-resident while every output
+// row gathers from them (launch_rows).
 template <typename T, int W, int U, int EPI, bool PERM>
 __global__ void __launch_bounds__(max_threads_for<W>())
     row_spmm_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
                     const int32_t* __restrict__ perm, const T* __restrict__ vals,
                     const T* __restrict__ dense, int64_t ld_dense, int64_t n,
-                    T* __restrict__ out, int64_t ld_out, EpiArgs<T> epi) {
+                    T* __restrict__ out, int64_t ld_out, EpiArgs<T> epi, int rows_per_cta,
+                    int64_t n_rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int64_t row = blockIdx.x;
+  const int warp_in_cta = threadIdx.x >> 5;
+  const int wpr = (blockDim.x >> 5) / rows_per_cta;  // warps per row
+  const int warp = warp_in_cta % wpr;
+  const int nwarps = wpr;
+  const int64_t row = (int64_t)blockIdx.x * rows_per_cta + warp_in_cta / wpr;
+  if (row >= n_rows) return;  // (rows_per_cta > 1 never takes the fused row-sum path)
   const int64_t chunk = (int64_t)blockIdx.y * nwarps + warp;
   const int64_t col0 = chunk * (32 * W) + (int64_t)lane * W;
   const int valid = (int)imax(0, imin(W, n - col0));
@@ -507,20 +517,37 @@ __global__ void __launch_bounds__(32)
 }
 
 
+// L2 budget for the slice of the gathered dense operand (B200: 126 MB L2;
+// leave room for the output stream, indices and values)
+constexpr int64_t kL2SliceBytes = 48ll << 20;
+
 template <typename T, int W, int U, int EPI, bool PERM>
 bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm, const T* vals,
-                 int64_t n_rows, const T* dense, int64_t ld_dense, int64_t n, T* out,
-                 int64_t ld_out, EpiArgs<T> epi, cudaStream_t st) {
+                 int64_t n_rows, int64_t dense_rows, const T* dense, int64_t ld_dense, int64_t n,
+                 T* out, int64_t ld_out, EpiArgs<T> epi, cudaStream_t st) {
   const int64_t chunks = ceil_div(n, 32 * W);
   // The fused row-sum needs the whole row in one CTA; take that shape when
   // there are enough rows to fill the GPU, else narrow CTAs (<= 8 warps) and
   // the separate warp-per-row bias kernel.
+  const int64_t dense_bytes = dense_rows * n * (int64_t)sizeof(T);
   const bool fuse = EPI == kEpiMask && epi.rowsum && n_rows >= 2 * 148 &&
-                    chunks <= max_threads_for<W>() / 32;
+                    chunks <= max_threads_for<W>() / 32 && dense_bytes <= kL2SliceBytes;
   // unfused: narrow CTAs (as few as 1 warp) when rows are few, so the warps
   // of a short, wide layer still spread over all 148 SMs
   int warps = (int)imin(8, chunks);
   while (warps > 1 && n_rows * ceil_div(chunks, warps) < 2 * 148) warps >>= 1;
+  // dense operand wider than L2: column slices of `warps` chunks whose rows
+  // fit the L2 budget (all output rows gather from one slice before the next
+  // starts), the CTA filled with rows_per_cta rows of that slice (config 5:
+  // 65536 x 4096 fp32 = 1 GB gathered per SpMM)
+  int rpc = 1;
+  if (!fuse && dense_bytes > kL2SliceBytes) {
+    const int64_t slice_cols = imax(32 * W, kL2SliceBytes / (dense_rows * (int64_t)sizeof(T)));
+    const int wmax = (int)imax(1, imin(8, slice_cols / (32 * W)));
+    while (warps > wmax) warps >>= 1;
+    rpc = 8 / warps;
+    if (n_rows < 148 * 2 * rpc) rpc = 1;
+  }
   if (fuse) warps = (int)chunks;
   const int64_t gy = ceil_div(chunks, warps);
   size_t dyn = 0;
@@ -529,17 +556,18 @@ bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm
   auto kern = row_spmm_kernel<T, W, U, EPI, PERM>;
   if (dyn > 40 * 1024)
     ensure_smem(kern, dyn);
-  launch_k(kern, dim3((unsigned)n_rows, (unsigned)gy), dim3(warps * 32), dyn, st, seg_ptr, idx,
-           perm, vals, dense, ld_dense, n, out, ld_out, epi);
+  launch_k(kern, dim3((unsigned)ceil_div(n_rows, rpc), (unsigned)gy), dim3(warps * rpc * 32), dyn,
+           st, seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out, epi, rpc, n_rows);
   return epi.rowsum != 0;
 }
 
 // n_rows x n outputs; *rowsum_done tells whether the fused row-sum ran
 template <typename T, int EPI, bool PERM>
 int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm,
-                        const T* vals, int64_t n_rows, const T* dense, int64_t ld_dense,
-                        int64_t n, T* out, int64_t ld_out, EpiArgs<T> epi, cudaStream_t st,
-                        const char* name, bool* rowsum_done, double avg_len = -1.0) {
+                        const T* vals, int64_t n_rows, int64_t dense_rows, const T* dense,
+                        int64_t ld_dense, int64_t n, T* out, int64_t ld_out, EpiArgs<T> epi,
+                        cudaStream_t st, const char* name, bool* rowsum_done,
+                        double avg_len = -1.0) {
   if (rowsum_done) *rowsum_done = false;
   if (n_rows == 0 || n == 0) return SMB_OK;
   if (n == 1 && !epi.rowsum) {  // one batch column: warp-per-row SpMV
@@ -558,62 +586,39 @@ int launch_segment_spmm(const int32_t* seg_ptr, const int32_t* idx, const int32_
   // sizes -- lower register pressure, more resident warps); with few rows one
   // column per lane spreads each row over many more warps.
   auto enough = [&](int w) { return n >= 32 * w && n_rows * ceil_div(n, 32 * w) >= 148 * 8; };
-  static const int force_w = [] {  // tuning experiments only
-    const char* e = getenv("SMB_SPMM_W");
-    return e ? atoi(e) : 0;
-  }();
   bool done;
-  if (force_w == 1)
-    done = launch_rows<T, 1, 32, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                            out, ld_out, epi, st);
-  else if (force_w == 4 && vec_ok)
-    done = launch_rows<T, VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                            out, ld_out, epi, st);
-  else if (force_w == 8 && vec_ok)
-    done = launch_rows<T, 2 * VW, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
-                                                n, out, ld_out, epi, st);
-  else if (force_w == 11)
-    done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                           out, ld_out, epi, st);
-  else if (force_w == 12)
-    done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                            out, ld_out, epi, st);
-  else if ((force_w == 9 || (force_w == 0 && avg_len >= 0 && avg_len <= 32)) && vec_ok &&
-           enough(2 * VW))
+  if (avg_len >= 0 && avg_len <= 32 && vec_ok && enough(2 * VW))
     // short segments (<= 32 nonzeros on average; known when the pattern is):
     // two vectors per lane with a 2-deep ring halve the warps per row and
     // the per-column index / shuffle work (config 2: 1.2-1.3x); long
     // segments keep one vector and a 4-deep ring (1.2-1.5x better there)
-    done = launch_rows<T, 2 * VW, 2, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense,
-                                                n, out, ld_out, epi, st);
-  else if (force_w == 7 && vec_ok)
-    done = launch_rows<T, VW, 2, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                             out, ld_out, epi, st);
+    done = launch_rows<T, 2 * VW, 2, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense_rows,
+                                                dense, ld_dense, n, out, ld_out, epi, st);
   else if (vec_ok && enough(VW))
-    done = launch_rows<T, VW, 4, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                            out, ld_out, epi, st);
+    done = launch_rows<T, VW, 4, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense_rows, dense,
+                                            ld_dense, n, out, ld_out, epi, st);
   // one column per lane: ring depth by shape (measured on B200: many short
   // rows prefer a shallow ring -- more resident warps -- while a few long
   // rows over a wide batch need the deep one)
   else if (n_rows >= 148)
-    done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                           out, ld_out, epi, st);
-  else if (!(EPI == kEpiMask && epi.rowsum) && (n < 512 || force_w == 14) && force_w != 13) {
+    done = launch_rows<T, 1, 8, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense_rows, dense,
+                                           ld_dense, n, out, ld_out, epi, st);
+  else if (!(EPI == kEpiMask && epi.rowsum) && n < 512) {
     // few long rows, narrow batch: parallel products + serial sum
     launch_k(row_spmm_pp_kernel<T, EPI, PERM>, dim3((unsigned)n_rows, (unsigned)ceil_div(n, 32)),
              dim3(32 * kPpWarps), 0, st, seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out,
              epi);
     done = false;
-  } else if (!(EPI == kEpiMask && epi.rowsum) && force_w != 13) {
+  } else if (!(EPI == kEpiMask && epi.rowsum)) {
     launch_k(row_spmm_deep_kernel<T, EPI, PERM>, dim3((unsigned)n_rows, (unsigned)ceil_div(n, 32)),
              dim3(32), 0, st, seg_ptr, idx, perm, vals, dense, ld_dense, n, out, ld_out, epi);
     done = false;
   } else if (n < 512)
-    done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                            out, ld_out, epi, st);
+    done = launch_rows<T, 1, 16, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense_rows, dense,
+                                            ld_dense, n, out, ld_out, epi, st);
   else
-    done = launch_rows<T, 1, 32, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense, ld_dense, n,
-                                            out, ld_out, epi, st);
+    done = launch_rows<T, 1, 32, EPI, PERM>(seg_ptr, idx, perm, vals, n_rows, dense_rows, dense,
+                                            ld_dense, n, out, ld_out, epi, st);
   if (rowsum_done) *rowsum_done = done;
   return check_launch(name);
 }
@@ -647,11 +652,11 @@ int spmm_t_fused_impl(const smb_pattern* pat, const void* values, const void* de
   int rc = csc_values
                ? launch_segment_spmm<T, kEpiMask, false>(
                      pat->col_ptr, pat->row_idx, nullptr, static_cast<const T*>(values), pat->k,
-                     static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi,
+                     pat->m, static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi,
                      st, "smb_spmm_t_csc", &done, avg)
                : launch_segment_spmm<T, kEpiMask, true>(
                      pat->col_ptr, pat->row_idx, pat->perm, static_cast<const T*>(values), pat->k,
-                     static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi,
+                     pat->m, static_cast<const T*>(dense), ld_dense, n, static_cast<T*>(out), ld_out, epi,
                      st, "smb_spmm_t", &done, avg);
   if (rc != SMB_OK || !want_rows || done) return rc;
   return launch_bias_rows<T>(static_cast<const T*>(out), ld_out, pat->k, n, epi.rb_bias,
@@ -665,13 +670,14 @@ using namespace smb;
 namespace {
 template <typename T>
 int spmm_impl(const int32_t* row_ptr, const int32_t* col_idx, const void* values, int64_t m,
-              const void* dense, int64_t ld_dense, int64_t n, const void* bias, int epilogue,
-              void* out, int64_t ld_out, void* stream, double avg_len = -1.0) {
+              int64_t k, const void* dense, int64_t ld_dense, int64_t n, const void* bias,
+              int epilogue, void* out, int64_t ld_out, void* stream, double avg_len = -1.0) {
   EpiArgs<T> epi{};
   epi.bias = static_cast<const T*>(bias);
   epi.relu = epilogue == SMB_EPI_RELU;
   return launch_segment_spmm<T, kEpiBiasAct, false>(
-      row_ptr, col_idx, nullptr, static_cast<const T*>(values), m, static_cast<const T*>(dense),
+      row_ptr, col_idx, nullptr, static_cast<const T*>(values), m, k,
+      static_cast<const T*>(dense),
       ld_dense, n, static_cast<T*>(out), ld_out, epi, as_stream(stream), "smb_spmm", nullptr,
       avg_len);
 }
@@ -693,7 +699,6 @@ extern "C" int smb_spmm(int dtype, const int32_t* row_ptr, const int32_t* col_id
                         int64_t ld_dense, int64_t n, const void* bias, int epilogue, void* out,
                         int64_t ld_out, void* stream) {
   clear_error();
-  (void)k;
   SMB_REQUIRE(m >= 0 && k >= 0 && n >= 0, "smb_spmm: negative dimension");
   SMB_REQUIRE(ld_dense >= n && ld_out >= n, "smb_spmm: leading dimension smaller than n");
   SMB_REQUIRE(epilogue == SMB_EPI_NONE || epilogue == SMB_EPI_RELU, "smb_spmm: bad epilogue %d",
@@ -701,10 +706,10 @@ extern "C" int smb_spmm(int dtype, const int32_t* row_ptr, const int32_t* col_id
   SMB_REQUIRE(m == 0 || (row_ptr && out), "smb_spmm: null pointer");
   SMB_REQUIRE(m < (int64_t(1) << 31), "smb_spmm: too many rows");
   if (dtype == SMB_F32)
-    return spmm_impl<float>(row_ptr, col_idx, values, m, dense, ld_dense, n, bias, epilogue, out,
-                            ld_out, stream);
+    return spmm_impl<float>(row_ptr, col_idx, values, m, k, dense, ld_dense, n, bias, epilogue,
+                            out, ld_out, stream);
   if (dtype == SMB_F64)
-    return spmm_impl<double>(row_ptr, col_idx, values, m, dense, ld_dense, n, bias, epilogue,
+    return spmm_impl<double>(row_ptr, col_idx, values, m, k, dense, ld_dense, n, bias, epilogue,
                              out, ld_out, stream);
   set_error("smb_spmm: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
@@ -722,11 +727,11 @@ extern "C" int smb_spmm_p(int dtype, const smb_pattern* pat, const void* values,
   SMB_REQUIRE(pat->m == 0 || out != nullptr, "smb_spmm_p: null output");
   const double avg = pat->m > 0 ? (double)pat->nnz / (double)pat->m : -1.0;
   if (dtype == SMB_F32)
-    return spmm_impl<float>(pat->row_ptr, pat->col_idx, values, pat->m, dense, ld_dense, n, bias,
-                            epilogue, out, ld_out, stream, avg);
+    return spmm_impl<float>(pat->row_ptr, pat->col_idx, values, pat->m, pat->k, dense, ld_dense,
+                            n, bias, epilogue, out, ld_out, stream, avg);
   if (dtype == SMB_F64)
-    return spmm_impl<double>(pat->row_ptr, pat->col_idx, values, pat->m, dense, ld_dense, n,
-                             bias, epilogue, out, ld_out, stream, avg);
+    return spmm_impl<double>(pat->row_ptr, pat->col_idx, values, pat->m, pat->k, dense, ld_dense,
+                             n, bias, epilogue, out, ld_out, stream, avg);
   set_error("smb_spmm_p: unsupported dtype %d", dtype);
   return SMB_ERR_INVALID;
 }

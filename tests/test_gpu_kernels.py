@@ -13,6 +13,7 @@ from conftest import bits_equal, random_csr, rel_err
 pytestmark = pytest.mark.gpu
 
 import paper_2407_17437_b200 as smb  # noqa: E402
+from paper_2407_17437_b200 import _lib  # noqa: E402
 from paper_2407_17437_b200 import tensor_core as tc  # noqa: E402
 
 
