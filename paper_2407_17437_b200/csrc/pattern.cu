@@ -135,7 +135,6 @@ void free_pattern(smb_pattern* p) {
   cudaFree(p->row_idx);
   cudaFree(p->perm);
   cudaFree(p->tile_row0);
-  cudaFree(p->chain_acc);
   delete p;
 }
 
@@ -195,8 +194,7 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
   if (cudaMalloc(&p->col_ptr, sizeof(int32_t) * (k + 1)) != cudaSuccess ||
       cudaMalloc(&p->row_idx, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess ||
       cudaMalloc(&p->perm, sizeof(int32_t) * (nnz > 0 ? nnz : 1)) != cudaSuccess ||
-      cudaMalloc(&p->tile_row0, sizeof(int32_t) * (p->ngrains > 0 ? p->ngrains : 1)) != cudaSuccess ||
-      cudaMalloc(&p->chain_acc, sizeof(double) * (nnz > 0 ? nnz : 1)) != cudaSuccess)
+      cudaMalloc(&p->tile_row0, sizeof(int32_t) * (p->ngrains > 0 ? p->ngrains : 1)) != cudaSuccess)
     return fail_cuda("cudaMalloc");
 
   int32_t *counts = nullptr, *tmp_row = nullptr, *tmp_perm = nullptr;

@@ -17,10 +17,6 @@ struct smb_pattern {
   // most rows spanned by any tile of 32 / 64 / 128 / 512 consecutive nonzeros
   // (aligned; first row .. row of the last nonzero)
   int64_t span32 = 0, span64 = 0, span128 = 0, span512 = 0;
-  // [nnz] running sums of the SDDMM chains between batch phases (sddmm.cu),
-  // used when the caller passes no gradient / second value buffer to hold
-  // them (sized for double values)
-  void* chain_acc = nullptr;  // owned
 };
 
 namespace smb {

@@ -73,20 +73,6 @@ __device__ __forceinline__ int64_t tile_row_of(int64_t p, int32_t r0, const int3
   return lo;
 }
 
-// Batch phases: when x and d_out together are wider than L2 (config 5:
-// 2 x 1 GB at B = 4096), the batch is walked in slices, one launch per slice,
-// so the slice's rows stay L2-resident while every chain gathers from them.
-// Each chain carries its running sum from one phase to the next through
-// `acc` (fp32 stored and reloaded exactly, so the chain -- and the result --
-// is bit-identical to one pass); only the last phase produces the gradient
-// and applies the update.
-template <typename T>
-struct ChainIO {
-  T* acc;     // [nnz] running sums between phases (nullptr: a single pass)
-  int first;  // the chain starts here (acc not read)
-  int last;   // the chain ends here (gradient / update written, acc not)
-};
-
 // ALL: every tile's d_out rows fit the SLOTS staging rows (checked on the
 // host from the pattern's tile spans), so the hot loop has no fallback path.
 template <typename T, int TILE, int CH, int ST, int SD, bool VEC, bool ALL>
@@ -95,7 +81,7 @@ __global__ void __launch_bounds__(TILE)
                       const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
                       const T* __restrict__ d_out, int64_t ld_d, const T* __restrict__ x,
                       int64_t ld_x, int64_t n, const T* values, T* values_out, T* velocity,
-                      T* grad_out, OptConsts<T> opt, ChainIO<T> io) {
+                      T* grad_out, OptConsts<T> opt) {
   using C = SddmmCfg<T, TILE, CH, ST, SD>;
   constexpr int S = C::STAGES, VW = C::VW, VPR = C::VPR, LDS = C::LDS;
   constexpr int kChunk = C::kChunk;
@@ -157,10 +143,9 @@ __global__ void __launch_bounds__(TILE)
   pdl_wait();  // d_out / x are earlier kernels' outputs
   // the update's operands, loaded now so they arrive during the chain instead
   // of costing one more memory round trip after it
-  const bool upd = active && opt.kind != SMB_OPT_NONE && io.last;
+  const bool upd = active && opt.kind != SMB_OPT_NONE;
   T w_pre = upd ? values[p] : T(0);
   T v_pre = (upd && velocity) ? velocity[p] : T(0);
-  const T acc0 = (active && io.acc && !io.first) ? io.acc[p] : T(-0.0);
 
   // full chunks (copied without bounds when VEC) run a lean main loop; a
   // ragged last chunk (n % CH != 0) is copied and summed after it
@@ -193,9 +178,8 @@ __global__ void __launch_bounds__(TILE)
     cp_async_commit();
   }
   // -0.0 is the exact additive identity, so acc = -0 + a0*b0 == a0*b0 and the
-  // chain below is the reference's  acc = a0*b0; acc += a_t*b_t  verbatim
-  // (a later batch phase continues the stored running sum).
-  T acc = acc0;
+  // chain below is the reference's  acc = a0*b0; acc += a_t*b_t  verbatim.
+  T acc = T(-0.0);
   // inactive threads sum zero-filled rows (never stored) from slot 0
   const int rslot = active ? slot : 0;
   const T* drow = d_out + (active ? row : r0) * ld_d;
@@ -243,10 +227,6 @@ __global__ void __launch_bounds__(TILE)
   cp_async_wait<0>();
   pdl_trigger();
   if (!active) return;
-  if (!io.last) {  // an earlier batch phase: park the running sum
-    io.acc[p] = acc;
-    return;
-  }
   const T g = (n == 0) ? T(0) : acc;  // tensor_core.py:283-284: zero batch -> zeros
   if (grad_out) grad_out[p] = g;
   if (upd) {
@@ -281,7 +261,7 @@ __global__ void __launch_bounds__(128)
                       const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
                       const T* __restrict__ d_out, int64_t ld_d, const T* __restrict__ x,
                       int64_t ld_x, int64_t n, const T* values, T* values_out, T* velocity,
-                      T* grad_out, OptConsts<T> opt, ChainIO<T> io) {
+                      T* grad_out, OptConsts<T> opt) {
   using C = SddmmWarpCfg<T, CH, S>;
   constexpr int VW = C::VW, LDS = C::LDS, VPR = C::VPR;
   static_assert(kWarpDSlots * VPR <= 32, "one d_out copy per lane");
@@ -327,11 +307,9 @@ __global__ void __launch_bounds__(128)
   const unsigned ddst = (unsigned)(((32 + lane / VPR) * LDS + (lane % VPR) * VW) * sizeof(T));
   const unsigned sbase = smem_u32(wsm);
   pdl_wait();  // d_out / x are earlier kernels' outputs
-  // update operands loaded early
-  const bool upd = active && opt.kind != SMB_OPT_NONE && io.last;
+  const bool upd = active && opt.kind != SMB_OPT_NONE;  // update operands loaded early
   T w_pre = upd ? values[p] : T(0);
   T v_pre = (upd && velocity) ? velocity[p] : T(0);
-  const T acc0 = (active && io.acc && !io.first) ? io.acc[p] : T(-0.0);
   auto issue = [&](int ch) {
     const unsigned st = sbase + (unsigned)(ch % S) * kStageBytes;
     const int t0 = ch * CH;
@@ -354,7 +332,7 @@ __global__ void __launch_bounds__(128)
     if (c < n_chunks) issue(c);
     cp_async_commit();
   }
-  T acc = acc0;
+  T acc = T(-0.0);
   const T* drow = d_out + row * ld_d;
   using V = typename Vec16<T>::type;
   for (int ch = 0; ch < n_chunks; ++ch) {
@@ -395,10 +373,6 @@ __global__ void __launch_bounds__(128)
   cp_async_wait<0>();
   pdl_trigger();
   if (!active) return;
-  if (!io.last) {  // an earlier batch phase: park the running sum
-    io.acc[p] = acc;
-    return;
-  }
   const T g = (n == 0) ? T(0) : acc;  // tensor_core.py:283-284: zero batch -> zeros
   if (grad_out) grad_out[p] = g;
   if (upd) {
@@ -414,9 +388,6 @@ template <typename T>
 int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias, T* grad,
                      const OptConsts<T>& opt, cudaStream_t st);
 
-// L2 budget of one batch phase's x + d_out slice (B200: 126 MB L2)
-constexpr int64_t kSddmmL2Bytes = 64ll << 20;
-
 template <typename T>
 int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, const void* x,
                       int64_t ld_x, int64_t n, const void* values, void* values_out,
@@ -428,34 +399,13 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
   if (pat->ntiles > 0) {
     constexpr int VW = 16 / sizeof(T);
     const bool vec = aligned16(x) && aligned16(d_out) && ld_x % VW == 0 && ld_d % VW == 0;
-    // batch phases (ChainIO above) when x and d_out together exceed the L2
-    // budget: slices of a multiple of 32 columns whose x + d_out rows fit it
-    const int64_t col_bytes = (pat->m + pat->k) * (int64_t)sizeof(T);
-    int64_t slice = n;
-    if (n > 0 && col_bytes * n > kSddmmL2Bytes)
-      slice = imin(n, imax(64, kSddmmL2Bytes / col_bytes / 32 * 32));
-    ChainIO<T> io{nullptr, 1, 1};
-    if (slice < n) {
-      // the running sums live in the gradient output, else in the second
-      // value buffer (written only by the last phase), else in the pattern's
-      // scratch
-      io.acc = grad_out ? static_cast<T*>(grad_out)
-               : (values_out && values_out != values) ? static_cast<T*>(values_out)
-                                                       : static_cast<T*>(pat->chain_acc);
-    }
     auto go = [&](auto kernel, int tile, size_t bytes) {
       ensure_smem(kernel, bytes);
-      for (int64_t t0 = 0; t0 < n || t0 == 0; t0 += slice) {
-        const int64_t w = imin(slice, n - t0);
-        io.first = t0 == 0;
-        io.last = t0 + slice >= n;
-        launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, tile)), dim3(tile), bytes, st,
-                 pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz,
-                 static_cast<const T*>(d_out) + t0, ld_d, static_cast<const T*>(x) + t0, ld_x,
-                 w, static_cast<const T*>(values), static_cast<T*>(values_out),
-                 static_cast<T*>(velocity), static_cast<T*>(grad_out), opt, io);
-        if (io.last) break;
-      }
+      launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, tile)), dim3(tile), bytes, st,
+               pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz,
+               static_cast<const T*>(d_out), ld_d, static_cast<const T*>(x), ld_x, n,
+               static_cast<const T*>(values), static_cast<T*>(values_out),
+               static_cast<T*>(velocity), static_cast<T*>(grad_out), opt);
     };
     // every tile's d_out rows staged -> fallback-free kernel (a 256 / 512-tile's
     // span is bounded by its enclosing 512-tile's)
