@@ -348,6 +348,21 @@ SMB_API int smb_xavier_pcg64(int dtype, uint64_t state_hi, uint64_t state_lo, ui
                      uint64_t inc_lo, uint64_t offset, int64_t count, double limit, void* out,
                      void* stream);
 
+/* Scale-mode pattern sampler (the device counterpart of the reference's
+ * sample_pattern, sparsity.py:183-216 -- same distribution, a uniform
+ * size-nnz subset of the m x k grid, not the same numpy stream):
+ * candidates pos_i = floor(Philox4x32-10(seed, counter (i, stream_id)) * m*k
+ * / 2^64), the pattern = the first nnz distinct candidates (or, for
+ * nnz > m*k/2, every position but the first m*k - nnz distinct ones), written
+ * as CSR into row_ptr[m+1] / col_idx[nnz] (device, caller-owned).
+ * Deterministic in (m, k, nnz, seed, stream_id).  Setup-time call: allocates
+ * scratch and synchronises `stream`. */
+SMB_API int smb_sample_pattern(int64_t m, int64_t k, int64_t nnz, uint64_t seed,
+                               uint64_t stream_id, int32_t* row_ptr, int32_t* col_idx,
+                               void* stream);
+/* The sampler's 64-bit Philox draw i (host-callable, for checking). */
+SMB_API uint64_t smb_philox_u64(uint64_t seed, uint64_t stream_id, uint64_t i);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,7 +41,8 @@ _lib = None
 
 
 def build() -> Path:
-    if not LIB.exists() or LIB.stat().st_mtime < (HERE / "csr_oracle.c").stat().st_mtime:
+    srcs = [HERE / "csr_oracle.c", HERE / "pattern_oracle.c"]
+    if not LIB.exists() or LIB.stat().st_mtime < max(p.stat().st_mtime for p in srcs):
         subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB
 
@@ -58,10 +59,25 @@ def lib():
             getattr(L, f"orc_sddmm_{suf}").argtypes = [p, p, i64, p, p, i64, p]
             getattr(L, f"orc_axpby_{suf}").argtypes = [T, p, T, p, i64]
             getattr(L, f"orc_row_sums_{suf}").argtypes = [p, i64, i64, p]
+        L.orc_philox_u64.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
+        L.orc_philox_u64.restype = C.c_uint64
+        L.orc_sample_pattern.argtypes = [i64, i64, i64, C.c_uint64, C.c_uint64, p, p]
+        L.orc_sample_pattern.restype = C.c_int
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_max_threads.restype = C.c_int
         _lib = L
     return _lib
+
+
+def sample_pattern_device_spec(n_out, n_in, nnz, seed, stream_id=0):
+    """CPU restatement of the device sampler (csrc/sampler.cu): the first nnz
+    distinct Philox candidates of the grid, as CSR (row_ptr, col_idx)."""
+    rp = np.zeros(n_out + 1, np.int32)
+    ci = np.zeros(max(nnz, 1), np.int32)
+    rc = lib().orc_sample_pattern(n_out, n_in, nnz, seed, stream_id, _p(rp), _p(ci))
+    if rc != 0:
+        raise ValueError("orc_sample_pattern failed")
+    return rp, ci[:nnz]
 
 
 def set_threads(n: int) -> None:

@@ -88,6 +88,8 @@ SIGNATURES = {
     "smb_gather_columns_ahead": (_i32, [_i32, _p, _i64, _i64, _p, _p, _i32, _i32, _i64, _p, _i64,
                                         _p]),
     "smb_xavier_pcg64": (_i32, [_i32, _u64, _u64, _u64, _u64, _u64, _i64, _f64, _p, _p]),
+    "smb_sample_pattern": (_i32, [_i64, _i64, _i64, _u64, _u64, _p, _p, _p]),
+    "smb_philox_u64": (_u64, [_u64, _u64, _u64]),
 }
 
 _lock = threading.Lock()

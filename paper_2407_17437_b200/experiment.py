@@ -85,7 +85,8 @@ class ExperimentConfig:
         return d
 
 
-def build_model(config: ExperimentConfig, large_patterns: bool = False):
+def build_model(config: ExperimentConfig, large_patterns: bool = False,
+                pattern_sampler: str = "host"):
     """ER plan -> Sequential of Sparse (backend "sparse") or MaskedDense
     (backend "masked") layers, Dense where the density saturates, compiled
     with the config's seed (bench.py:127-151).  Returns (model, plan)."""
@@ -104,7 +105,7 @@ def build_model(config: ExperimentConfig, large_patterns: bool = False):
         else:
             model.add(MaskedDense(n_out, dens, activation=act, optimizer=opt, nnz=nnz))
     model.compile(input_size=config.layer_dims[0], batch_size=config.batch_size, seed=config.seed,
-                  large_patterns=large_patterns)
+                  large_patterns=large_patterns, pattern_sampler=pattern_sampler)
     return model, plan
 
 
