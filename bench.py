@@ -648,10 +648,24 @@ def run_ours(args):
             a.cpu_seconds = min(args.cpu_seconds, 6.0)
             r, m_, s_ = measure(a, ctx, ddata, data, steps, args.warmup, launches=False,
                                 cpu_min_steps=1)
+            del m_, s_
+            torch.cuda.empty_cache()
+            # model construction with every pattern drawn on the device
+            # (scale mode, sparsity.sample_pattern_device) next to the host
+            # sampler's time above (build_s)
+            import paper_2407_17437_b200 as smb_
+
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            m_, _ = smb_.build_model(smb_.ExperimentConfig(
+                layer_dims=[int(x) for x in a.layers.split(",")], density=a.density,
+                batch_size=a.batch, lr=a.lr, seed=a.seed), pattern_sampler="device")
+            torch.cuda.synchronize()
+            r["build_s_device_sampler"] = round(time.perf_counter() - t0, 3)
             r.pop("config", None)
             r["config"] = config_dict(a, ws)
             extras[name] = r
-            del m_, s_
+            del m_
             torch.cuda.empty_cache()
         line["extra_configs"] = extras
     if args.sweep and ws == 1:
