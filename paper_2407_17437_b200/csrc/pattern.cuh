@@ -23,3 +23,35 @@ namespace smb {
 constexpr int kSddmmTile = 128;  // nonzeros per SDDMM CTA (one per thread)
 constexpr int kTileGrain = 32;   // granularity of the tile -> first-row table
 }
+
+namespace smb {
+// Row of nonzero p inside a tile starting at row r0, through a shared window
+// s_rp[0..W] = row_ptr[r0 .. r0+W]; global binary search when the tile spans
+// more than W rows (long runs of empty rows).
+template <int W>
+__device__ __forceinline__ int64_t tile_row_of(int64_t p, int32_t r0, const int32_t* s_rp,
+                                               const int32_t* row_ptr, int64_t m) {
+  if (p < (int64_t)s_rp[W]) {
+    int lo = 0, hi = W;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if ((int64_t)s_rp[mid] <= p) lo = mid; else hi = mid;
+    }
+    return r0 + lo;
+  }
+  int64_t lo = r0 + W, hi = m;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)row_ptr[mid] <= p) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// SDDMM + update with TMA gather4 staging (sddmm_tma.cu), fp32
+bool sddmm_tma_supported(const smb_pattern* pat, const void* d_out, int64_t ld_d, const void* x,
+                         int64_t ld_x, int64_t n);
+int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, const float* x,
+                     int64_t ld_x, int64_t n, const float* values, float* values_out,
+                     float* velocity, float* grad_out, const OptConsts<float>& opt,
+                     cudaStream_t st, int stages);
+}  // namespace smb

@@ -51,28 +51,6 @@ struct SddmmCfg {
   static_assert(TILE % VPR == 0, "tile / vector split");
 };
 
-// Row of nonzero p inside a tile starting at row r0, through a shared window
-// s_rp[0..W] = row_ptr[r0 .. r0+W]; global binary search when the tile spans
-// more than W rows (long runs of empty rows).
-template <int W>
-__device__ __forceinline__ int64_t tile_row_of(int64_t p, int32_t r0, const int32_t* s_rp,
-                                               const int32_t* row_ptr, int64_t m) {
-  if (p < (int64_t)s_rp[W]) {
-    int lo = 0, hi = W;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if ((int64_t)s_rp[mid] <= p) lo = mid; else hi = mid;
-    }
-    return r0 + lo;
-  }
-  int64_t lo = r0 + W, hi = m;
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if ((int64_t)row_ptr[mid] <= p) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // ALL: every tile's d_out rows fit the SLOTS staging rows (checked on the
 // host from the pattern's tile spans), so the hot loop has no fallback path.
 template <typename T, int TILE, int CH, int ST, int SD, bool VEC, bool ALL>
@@ -457,7 +435,21 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
                        ceil_div(pat->nnz, 32) <= 9 * 148 && all_for(32, 4);
     bool warp_done = false;
     if constexpr (sizeof(T) == 4) {
-      if (!small32 && !small64 && !mid32 && warp_kernel) {
+      static const int tma_stages = [] {  // TEMPORARY A/B switch (lab only)
+        const char* e = getenv("SMB_SDDMM_TMA");
+        return e ? atoi(e) : 0;
+      }();
+      if (tma_stages > 0 && !small32 && !small64 && !mid32 &&
+          sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
+        const int rc = launch_sddmm_tma(pat, static_cast<const float*>(d_out), ld_d,
+                                        static_cast<const float*>(x), ld_x, n,
+                                        static_cast<const float*>(values),
+                                        static_cast<float*>(values_out),
+                                        static_cast<float*>(velocity),
+                                        static_cast<float*>(grad_out), opt, st, tma_stages);
+        if (rc != SMB_OK) return rc;
+        warp_done = true;
+      } else if (!small32 && !small64 && !mid32 && warp_kernel) {
         go(sddmm_warp_kernel<T, 32, 2>, 128, SddmmWarpCfg<T, 32, 2>::smem_bytes);
         warp_done = true;
       }

@@ -1,0 +1,253 @@
+// SDDMM + update with TMA row gathers (sm_100a).
+//
+// The same per-chain arithmetic as sddmm.cu (grad[p] = sum_t d_out[i,t] *
+// x[j,t], one sequential chain per nonzero, multiply and add rounded
+// separately, _kernels.py:62-75; then the sparse_combine update sequence of
+// nn.py:187-197), with the staging done by the Tensor Memory Accelerator
+// instead of per-thread cp.async:
+//
+//   * each warp owns 32 consecutive nonzeros (CSR order) and a private ring
+//     of S stages; a stage holds the 32 gathered x-row segments of one
+//     32-column batch chunk plus up to 4 d_out rows the warp's nonzeros span;
+//   * 9 lanes fill a stage with ONE `cp.async.bulk.tensor.2d.tile::gather4`
+//     each (4 arbitrary rows x 128 bytes per instruction, SASS
+//     UTMALDG.2D.GATHER4) and the stage's mbarrier counts the bytes in
+//     (complete_tx); the other lanes issue no copy instructions at all, so the
+//     MIO queue that throttled the LDGSTS version (ncu: mio_throttle the top
+//     stall at config 4) only carries the chains' shared-memory reads;
+//   * the tensor maps use the 128-byte swizzle: 16-byte chunk u of staged row
+//     r sits at chunk u ^ (r mod 8), so the 8 lanes of a quarter-warp reading
+//     chunk u of their own rows hit 8 different bank groups (conflict-free
+//     without padding, unlike the 144-byte padded rows of cp.async staging
+//     that split sectors on the global side).
+//
+// Valid for fp32 with 16-byte aligned operands and leading dimensions
+// (sddmm_tma_supported); the caller falls back to sddmm.cu otherwise.
+#include <cuda.h>
+
+#include "pattern.cuh"
+
+namespace smb {
+namespace {
+
+constexpr int kTmaRows = 40;                  // staged rows per stage: 32 x, 4 d, 4 spare
+constexpr int kTmaStageBytes = kTmaRows * 128;  // 5120: keeps every stage 1024-byte aligned
+constexpr int kTmaDSlots = 4;
+constexpr int kTmaTile = 128;  // nonzeros per CTA: 4 warps x 32 (the tile_row0 grain)
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// 4 rows (r0..r3) x 32 fp32 columns starting at column c of a 2-D tensor map
+__device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap* map, int c, int r0,
+                                            int r1, int r2, int r3, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(c), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+
+template <int S>
+__global__ void __launch_bounds__(128)
+    sddmm_tma_kernel(const __grid_constant__ CUtensorMap xmap,
+                     const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ row_ptr,
+                     const int32_t* __restrict__ col_idx, const int32_t* __restrict__ tile_row0,
+                     int64_t m, int64_t nnz, const float* __restrict__ d_out, int64_t ld_d, int n,
+                     const float* values, float* values_out, float* velocity, float* grad_out,
+                     OptConsts<float> opt) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ int32_t s_rp[kTmaTile + 1];
+  __shared__ __align__(8) unsigned long long s_full[4][S];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // dynamic smem rounded up to 1024 bytes (the 128-byte swizzle atom)
+  const unsigned raw = smem_addr(smem_raw);
+  const unsigned base = ((raw + 1023u) & ~1023u) + (unsigned)(warp * S * kTmaStageBytes);
+  const unsigned char* gbase = smem_raw + (base - raw);
+  const int64_t p0 = (int64_t)blockIdx.x * kTmaTile;
+  const int64_t pw = p0 + warp * 32;
+  const int nw = (int)imax(0, imin(32, nnz - pw));
+  const int64_t p = pw + lane;
+  const bool active = lane < nw;
+  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (kTmaTile / kTileGrain)];
+  s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
+  if (tid == 0) s_rp[kTmaTile] = (r0 + kTmaTile <= m) ? row_ptr[r0 + kTmaTile] : INT32_MAX;
+  const int32_t my_col = active ? col_idx[p] : 0;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(smem_addr(&s_full[warp][s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();  // the only CTA-wide barrier (row window + barrier init)
+  if (nw == 0) return;
+  const int64_t row = tile_row_of<kTmaTile>(active ? p : pw, r0, s_rp, row_ptr, m);
+  const int64_t row_first = __shfl_sync(0xffffffffu, row, 0);
+  const int64_t row_last = __shfl_sync(0xffffffffu, row, nw - 1);
+  const int span = (int)(row_last - row_first + 1);
+  const bool staged = span <= kTmaDSlots;  // warp-uniform
+  const int slot = (int)(row - row_first);
+  const int n_chunks = (n + 31) / 32;
+  // copy roles: lane g < 8 gathers x rows 4g..4g+3, lane 8 the d_out rows
+  int gr[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int src = (lane < 8) ? 4 * lane + q : 0;
+    gr[q] = __shfl_sync(0xffffffffu, my_col, src);
+  }
+  if (lane == 8) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) gr[q] = (int)imin(row_first + imin(q, span - 1), m - 1);
+  }
+  const bool copier = lane < 8 || (lane == 8 && staged);
+  const unsigned cdst = (lane < 8) ? (unsigned)(lane * 512) : (unsigned)(32 * 128);
+  const unsigned tx_bytes = 32 * 128 + (staged ? kTmaDSlots * 128 : 0);
+  pdl_wait();  // d_out / x are earlier kernels' outputs
+  const bool upd = active && opt.kind != SMB_OPT_NONE;
+  float w_pre = upd ? values[p] : 0.f;
+  float v_pre = (upd && velocity) ? velocity[p] : 0.f;
+  auto issue = [&](int ch) {
+    const int s = ch % S;
+    const unsigned bar = smem_addr(&s_full[warp][s]);
+    if (lane == 0) mbar_arrive_expect_tx(bar, tx_bytes);
+    __syncwarp();
+    if (copier)
+      tma_gather4(base + (unsigned)(s * kTmaStageBytes) + cdst, lane < 8 ? &xmap : &dmap, ch * 32,
+                  gr[0], gr[1], gr[2], gr[3], bar);
+  };
+  for (int c = 0; c < S && c < n_chunks; ++c) issue(c);
+  float acc = -0.0f;  // exact additive identity (sddmm.cu)
+  const float* drow = d_out + row * ld_d;
+  const int xsw = lane & 7;                 // swizzle of this lane's x row
+  const int dsw = (32 + slot) & 7;          // ... of its d_out row
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int s = ch % S;
+    mbar_wait(smem_addr(&s_full[warp][s]), (unsigned)((ch / S) & 1));
+    const unsigned char* st = gbase + s * kTmaStageBytes;
+    const float* xr = reinterpret_cast<const float*>(st + lane * 128);
+    const float* dr = reinterpret_cast<const float*>(st + (32 + slot) * 128);
+    const int t0 = ch * 32;
+    const int cnt = min(32, n - t0);
+    if (cnt == 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * (u ^ xsw));
+        float4 dv;
+        if (staged) {
+          dv = *reinterpret_cast<const float4*>(dr + 4 * (u ^ dsw));
+        } else {
+          dv = make_float4(drow[t0 + 4 * u], drow[t0 + 4 * u + 1], drow[t0 + 4 * u + 2],
+                           drow[t0 + 4 * u + 3]);
+        }
+        acc = add_rn(acc, mul_rn(dv.x, xv.x));
+        acc = add_rn(acc, mul_rn(dv.y, xv.y));
+        acc = add_rn(acc, mul_rn(dv.z, xv.z));
+        acc = add_rn(acc, mul_rn(dv.w, xv.w));
+      }
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        const int u = j >> 2, e = j & 3;
+        const float xv = xr[4 * (u ^ xsw) + e];
+        const float dv = staged ? dr[4 * (u ^ dsw) + e] : drow[t0 + j];
+        acc = add_rn(acc, mul_rn(dv, xv));
+      }
+    }
+    __syncwarp();  // every lane has read stage s: refill it
+    if (ch + S < n_chunks) issue(ch + S);
+  }
+  pdl_trigger();
+  if (!active) return;
+  const float g = (n == 0) ? 0.f : acc;  // tensor_core.py:283-284: zero batch -> zeros
+  if (grad_out) grad_out[p] = g;
+  if (upd) {
+    apply_update(opt, g, &w_pre, &v_pre);
+    values_out[p] = w_pre;
+    if (velocity) velocity[p] = v_pre;
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// rows x cols fp32 row-major with leading dimension ld; box = 1 row x 32 cols
+bool make_row_map(CUtensorMap* map, const float* ptr, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  const cuuint32_t box[2] = {32, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// The TMA variant applies to fp32, 16-byte aligned operands whose leading
+// dimensions are multiples of 4 elements, and rows < 2^31.
+bool sddmm_tma_supported(const smb_pattern* pat, const void* d_out, int64_t ld_d, const void* x,
+                         int64_t ld_x, int64_t n) {
+  return encode_fn() != nullptr && aligned16(d_out) && aligned16(x) && ld_d % 4 == 0 &&
+         ld_x % 4 == 0 && n >= 1 && n < (int64_t(1) << 31) && pat->m < (int64_t(1) << 31) &&
+         pat->k < (int64_t(1) << 31) && pat->nnz > 0;
+}
+
+int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, const float* x,
+                     int64_t ld_x, int64_t n, const float* values, float* values_out,
+                     float* velocity, float* grad_out, const OptConsts<float>& opt,
+                     cudaStream_t st, int stages) {
+  CUtensorMap xmap, dmap;
+  if (!make_row_map(&xmap, x, pat->k, n, ld_x) || !make_row_map(&dmap, d_out, pat->m, n, ld_d)) {
+    set_error("sddmm (TMA): tensor map encoding failed");
+    return SMB_ERR_CUDA;
+  }
+  const unsigned grid = (unsigned)ceil_div(pat->nnz, kTmaTile);
+  auto go = [&](auto kernel, int s) {
+    const size_t smem = (size_t)4 * s * kTmaStageBytes + 1024;
+    ensure_smem(kernel, smem);
+    launch_k(kernel, dim3(grid), dim3(128), smem, st, xmap, dmap, pat->row_ptr, pat->col_idx,
+             pat->tile_row0, pat->m, pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity,
+             grad_out, opt);
+  };
+  if (stages <= 2) go(sddmm_tma_kernel<2>, 2);
+  else if (stages == 3) go(sddmm_tma_kernel<3>, 3);
+  else go(sddmm_tma_kernel<4>, 4);
+  return check_launch("smb_sddmm_update (TMA)");
+}
+
+}  // namespace smb
