@@ -30,10 +30,16 @@
 namespace smb {
 namespace {
 
-constexpr int kTmaRows = 40;                  // staged rows per stage: 32 x, 4 d, 4 spare
-constexpr int kTmaStageBytes = kTmaRows * 128;  // 5120: keeps every stage 1024-byte aligned
+constexpr int kTmaXBytes = 32 * 128;  // x rows of one stage (1024-byte aligned blocks)
 constexpr int kTmaDSlots = 4;
-constexpr int kTmaTile = 128;  // nonzeros per CTA: 4 warps x 32 (the tile_row0 grain)
+constexpr int kTmaDBytes = kTmaDSlots * 128;  // d_out rows of one stage (512-byte blocks)
+// shared memory of one warp's ring: S x-blocks, then S d-blocks, rounded to
+// the 1024-byte swizzle atom (the hardware swizzle follows address bits
+// 7-9, so 512-byte aligned gather4 destinations are fine)
+template <int S>
+constexpr int warp_ring_bytes() {
+  return (S * (kTmaXBytes + kTmaDBytes) + 1023) / 1024 * 1024;
+}
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -66,30 +72,32 @@ __device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap* map
       : "memory");
 }
 
-template <int S>
-__global__ void __launch_bounds__(128)
+template <int S, int WPC>
+__global__ void __launch_bounds__(32 * WPC)
     sddmm_tma_kernel(const __grid_constant__ CUtensorMap xmap,
                      const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ row_ptr,
                      const int32_t* __restrict__ col_idx, const int32_t* __restrict__ tile_row0,
                      int64_t m, int64_t nnz, const float* __restrict__ d_out, int64_t ld_d, int n,
                      const float* values, float* values_out, float* velocity, float* grad_out,
                      OptConsts<float> opt) {
+  constexpr int kTile = 32 * WPC;  // nonzeros per CTA (a multiple of the tile_row0 grain)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ int32_t s_rp[kTmaTile + 1];
-  __shared__ __align__(8) unsigned long long s_full[4][S];
+  __shared__ int32_t s_rp[kTile + 1];
+  __shared__ __align__(8) unsigned long long s_full[WPC][S];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // dynamic smem rounded up to 1024 bytes (the 128-byte swizzle atom)
   const unsigned raw = smem_addr(smem_raw);
-  const unsigned base = ((raw + 1023u) & ~1023u) + (unsigned)(warp * S * kTmaStageBytes);
+  const unsigned base = ((raw + 1023u) & ~1023u) + (unsigned)(warp * warp_ring_bytes<S>());
+  const unsigned dbase = base + S * kTmaXBytes;
   const unsigned char* gbase = smem_raw + (base - raw);
-  const int64_t p0 = (int64_t)blockIdx.x * kTmaTile;
+  const int64_t p0 = (int64_t)blockIdx.x * kTile;
   const int64_t pw = p0 + warp * 32;
   const int nw = (int)imax(0, imin(32, nnz - pw));
   const int64_t p = pw + lane;
   const bool active = lane < nw;
-  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (kTmaTile / kTileGrain)];
+  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (kTile / kTileGrain)];
   s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
-  if (tid == 0) s_rp[kTmaTile] = (r0 + kTmaTile <= m) ? row_ptr[r0 + kTmaTile] : INT32_MAX;
+  if (tid == 0) s_rp[kTile] = (r0 + kTile <= m) ? row_ptr[r0 + kTile] : INT32_MAX;
   const int32_t my_col = active ? col_idx[p] : 0;
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(smem_addr(&s_full[warp][s]), 1);
@@ -97,7 +105,7 @@ __global__ void __launch_bounds__(128)
   }
   __syncthreads();  // the only CTA-wide barrier (row window + barrier init)
   if (nw == 0) return;
-  const int64_t row = tile_row_of<kTmaTile>(active ? p : pw, r0, s_rp, row_ptr, m);
+  const int64_t row = tile_row_of<kTile>(active ? p : pw, r0, s_rp, row_ptr, m);
   const int64_t row_first = __shfl_sync(0xffffffffu, row, 0);
   const int64_t row_last = __shfl_sync(0xffffffffu, row, nw - 1);
   const int span = (int)(row_last - row_first + 1);
@@ -116,7 +124,6 @@ __global__ void __launch_bounds__(128)
     for (int q = 0; q < 4; ++q) gr[q] = (int)imin(row_first + imin(q, span - 1), m - 1);
   }
   const bool copier = lane < 8 || (lane == 8 && staged);
-  const unsigned cdst = (lane < 8) ? (unsigned)(lane * 512) : (unsigned)(32 * 128);
   const unsigned tx_bytes = 32 * 128 + (staged ? kTmaDSlots * 128 : 0);
   pdl_wait();  // d_out / x are earlier kernels' outputs
   const bool upd = active && opt.kind != SMB_OPT_NONE;
@@ -128,20 +135,21 @@ __global__ void __launch_bounds__(128)
     if (lane == 0) mbar_arrive_expect_tx(bar, tx_bytes);
     __syncwarp();
     if (copier)
-      tma_gather4(base + (unsigned)(s * kTmaStageBytes) + cdst, lane < 8 ? &xmap : &dmap, ch * 32,
-                  gr[0], gr[1], gr[2], gr[3], bar);
+      tma_gather4(lane < 8 ? base + (unsigned)(s * kTmaXBytes + lane * 512)
+                           : dbase + (unsigned)(s * kTmaDBytes),
+                  lane < 8 ? &xmap : &dmap, ch * 32, gr[0], gr[1], gr[2], gr[3], bar);
   };
   for (int c = 0; c < S && c < n_chunks; ++c) issue(c);
   float acc = -0.0f;  // exact additive identity (sddmm.cu)
   const float* drow = d_out + row * ld_d;
-  const int xsw = lane & 7;                 // swizzle of this lane's x row
-  const int dsw = (32 + slot) & 7;          // ... of its d_out row
+  const int xsw = lane & 7;  // swizzle of this lane's x row (1024-aligned x blocks)
   for (int ch = 0; ch < n_chunks; ++ch) {
     const int s = ch % S;
     mbar_wait(smem_addr(&s_full[warp][s]), (unsigned)((ch / S) & 1));
-    const unsigned char* st = gbase + s * kTmaStageBytes;
-    const float* xr = reinterpret_cast<const float*>(st + lane * 128);
-    const float* dr = reinterpret_cast<const float*>(st + (32 + slot) * 128);
+    const float* xr = reinterpret_cast<const float*>(gbase + s * kTmaXBytes + lane * 128);
+    const unsigned doff = S * kTmaXBytes + s * kTmaDBytes + slot * 128;
+    const float* dr = reinterpret_cast<const float*>(gbase + doff);
+    const int dsw = (int)(((base + doff) >> 7) & 7);  // swizzle of this lane's d_out row
     const int t0 = ch * 32;
     const int cnt = min(32, n - t0);
     if (cnt == 32) {
@@ -236,17 +244,23 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
     set_error("sddmm (TMA): tensor map encoding failed");
     return SMB_ERR_CUDA;
   }
-  const unsigned grid = (unsigned)ceil_div(pat->nnz, kTmaTile);
-  auto go = [&](auto kernel, int s) {
-    const size_t smem = (size_t)4 * s * kTmaStageBytes + 1024;
+  auto go = [&](auto kernel, int s, int wpc, int ring) {
+    const size_t smem = (size_t)wpc * ring + 1024;
     ensure_smem(kernel, smem);
-    launch_k(kernel, dim3(grid), dim3(128), smem, st, xmap, dmap, pat->row_ptr, pat->col_idx,
-             pat->tile_row0, pat->m, pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity,
-             grad_out, opt);
+    launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, 32 * wpc)), dim3(32 * wpc), smem, st,
+             xmap, dmap, pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz, d_out,
+             ld_d, (int)n, values, values_out, velocity, grad_out, opt);
   };
-  if (stages <= 2) go(sddmm_tma_kernel<2>, 2);
-  else if (stages == 3) go(sddmm_tma_kernel<3>, 3);
-  else go(sddmm_tma_kernel<4>, 4);
+  const int wpc = stages / 10, s = stages % 10;
+  if (wpc <= 1 && s <= 2) go(sddmm_tma_kernel<2, 1>, 2, 1, warp_ring_bytes<2>());
+  else if (wpc <= 1 && s == 3) go(sddmm_tma_kernel<3, 1>, 3, 1, warp_ring_bytes<3>());
+  else if (wpc <= 1) go(sddmm_tma_kernel<4, 1>, 4, 1, warp_ring_bytes<4>());
+  else if (wpc <= 2 && s <= 2) go(sddmm_tma_kernel<2, 2>, 2, 2, warp_ring_bytes<2>());
+  else if (wpc <= 2 && s == 3) go(sddmm_tma_kernel<3, 2>, 3, 2, warp_ring_bytes<3>());
+  else if (wpc <= 2) go(sddmm_tma_kernel<4, 2>, 4, 2, warp_ring_bytes<4>());
+  else if (s <= 2) go(sddmm_tma_kernel<2, 4>, 2, 4, warp_ring_bytes<2>());
+  else if (s == 3) go(sddmm_tma_kernel<3, 4>, 3, 4, warp_ring_bytes<3>());
+  else go(sddmm_tma_kernel<4, 4>, 4, 4, warp_ring_bytes<4>());
   return check_launch("smb_sddmm_update (TMA)");
 }
 
