@@ -37,7 +37,7 @@ constexpr int kTmaDBytes = kTmaDSlots * 128;  // d_out rows of one stage (512-by
 // the 1024-byte swizzle atom (the hardware swizzle follows address bits
 // 7-9, so 512-byte aligned gather4 destinations are fine)
 template <int S>
-constexpr int warp_ring_bytes() {
+__host__ __device__ constexpr int warp_ring_bytes() {
   return (S * (kTmaXBytes + kTmaDBytes) + 1023) / 1024 * 1024;
 }
 
