@@ -439,8 +439,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
         const char* e = getenv("SMB_SDDMM_TMA");
         return e ? atoi(e) : 0;
       }();
-      if (tma_stages > 0 && !small32 && !small64 && !mid32 &&
-          sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
+      if (tma_stages > 0 && sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
         const int rc = launch_sddmm_tma(pat, static_cast<const float*>(d_out), ld_d,
                                         static_cast<const float*>(x), ld_x, n,
                                         static_cast<const float*>(values),

@@ -253,14 +253,10 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
   };
   const int wpc = stages / 10, s = stages % 10;
   if (wpc <= 1 && s <= 2) go(sddmm_tma_kernel<2, 1>, 2, 1, warp_ring_bytes<2>());
-  else if (wpc <= 1 && s == 3) go(sddmm_tma_kernel<3, 1>, 3, 1, warp_ring_bytes<3>());
-  else if (wpc <= 1) go(sddmm_tma_kernel<4, 1>, 4, 1, warp_ring_bytes<4>());
-  else if (wpc <= 2 && s <= 2) go(sddmm_tma_kernel<2, 2>, 2, 2, warp_ring_bytes<2>());
-  else if (wpc <= 2 && s == 3) go(sddmm_tma_kernel<3, 2>, 3, 2, warp_ring_bytes<3>());
-  else if (wpc <= 2) go(sddmm_tma_kernel<4, 2>, 4, 2, warp_ring_bytes<4>());
-  else if (s <= 2) go(sddmm_tma_kernel<2, 4>, 2, 4, warp_ring_bytes<2>());
-  else if (s == 3) go(sddmm_tma_kernel<3, 4>, 3, 4, warp_ring_bytes<3>());
-  else go(sddmm_tma_kernel<4, 4>, 4, 4, warp_ring_bytes<4>());
+  else if (wpc <= 1 && s <= 3) go(sddmm_tma_kernel<3, 1>, 3, 1, warp_ring_bytes<3>());
+  else if (wpc <= 1 && s <= 4) go(sddmm_tma_kernel<4, 1>, 4, 1, warp_ring_bytes<4>());
+  else if (wpc <= 1 && s <= 6) go(sddmm_tma_kernel<6, 1>, 6, 1, warp_ring_bytes<6>());
+  else go(sddmm_tma_kernel<8, 1>, 8, 1, warp_ring_bytes<8>());
   return check_launch("smb_sddmm_update (TMA)");
 }
 

@@ -16,9 +16,13 @@ from oracle import oracle as O
 O.build()
 O.set_threads(os.cpu_count() or 1)
 tag = os.environ.get("SMB_SDDMM_TMA", "0")
-for (m, k, d, B) in [(8192, 8192, 0.0084, 1024), (8192, 3072, 0.0154, 1024),
-                     (8192, 8192, 0.01, 512), (8192, 8192, 0.1, 512),
-                     (65536, 65536, 0.000587, 512), (1024, 3072, 0.0078, 1024)]:
+SHAPES = [(8192, 8192, 0.0084, 1024), (8192, 3072, 0.0154, 1024),
+          (8192, 8192, 0.01, 512), (8192, 8192, 0.1, 512),
+          (65536, 65536, 0.000587, 512), (1024, 3072, 0.0078, 1024)]
+if os.environ.get("LAB_SMALL"):
+    SHAPES = [(1024, 3072, 0.0078, 1024), (512, 1024, 0.0175, 1024), (10, 512, 0.609, 1024),
+              (1024, 3072, 0.0078, 100), (512, 1024, 0.0175, 100)]
+for (m, k, d, B) in SHAPES:
     nnz = int(round(d * m * k))
     pat = smb.sample_pattern(m, k, nnz, smb.Rng(0).stream("pattern"), large=m * k >= 2**31)
     rng = np.random.default_rng(1)
