@@ -53,5 +53,5 @@ bool sddmm_tma_supported(const smb_pattern* pat, const void* d_out, int64_t ld_d
 int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, const float* x,
                      int64_t ld_x, int64_t n, const float* values, float* values_out,
                      float* velocity, float* grad_out, const OptConsts<float>& opt,
-                     cudaStream_t st, int stages);
+                     cudaStream_t st);
 }  // namespace smb

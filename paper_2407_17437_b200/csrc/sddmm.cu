@@ -435,17 +435,21 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
                        ceil_div(pat->nnz, 32) <= 9 * 148 && all_for(32, 4);
     bool warp_done = false;
     if constexpr (sizeof(T) == 4) {
-      static const int tma_stages = [] {  // TEMPORARY A/B switch (lab only)
-        const char* e = getenv("SMB_SDDMM_TMA");
-        return e ? atoi(e) : 0;
-      }();
-      if (tma_stages > 0 && sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
+      // many-wave layers: one warp per CTA, its 32 chains fed by TMA gather4
+      // into a 2-stage swizzled ring (sddmm_tma.cu).  Measured on B200
+      // against the cp.async warp / pipe kernels (scripts/lab_sddmm_tma.py):
+      // config-4 hidden layer 238 -> 211 us, config-5 hidden layer (B=512)
+      // 677 -> 485 us, config 3 d=0.1 1364 -> 1236 us; more stages or warps
+      // per CTA lower the resident warps and run slower.  Few-wave layers keep
+      // the cp.async kernels: one warp's TMA chunks do not overlap well
+      // (config-2 layers 10-15 us -> 21-24 us with any ring depth).
+      if (!small32 && !small64 && !mid32 && sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
         const int rc = launch_sddmm_tma(pat, static_cast<const float*>(d_out), ld_d,
                                         static_cast<const float*>(x), ld_x, n,
                                         static_cast<const float*>(values),
                                         static_cast<float*>(values_out),
                                         static_cast<float*>(velocity),
-                                        static_cast<float*>(grad_out), opt, st, tma_stages);
+                                        static_cast<float*>(grad_out), opt, st);
         if (rc != SMB_OK) return rc;
         warp_done = true;
       } else if (!small32 && !small64 && !mid32 && warp_kernel) {

@@ -238,7 +238,7 @@ bool sddmm_tma_supported(const smb_pattern* pat, const void* d_out, int64_t ld_d
 int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, const float* x,
                      int64_t ld_x, int64_t n, const float* values, float* values_out,
                      float* velocity, float* grad_out, const OptConsts<float>& opt,
-                     cudaStream_t st, int stages) {
+                     cudaStream_t st) {
   CUtensorMap xmap, dmap;
   if (!make_row_map(&xmap, x, pat->k, n, ld_x) || !make_row_map(&dmap, d_out, pat->m, n, ld_d)) {
     set_error("sddmm (TMA): tensor map encoding failed");
@@ -251,12 +251,7 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
              xmap, dmap, pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz, d_out,
              ld_d, (int)n, values, values_out, velocity, grad_out, opt);
   };
-  const int wpc = stages / 10, s = stages % 10;
-  if (wpc <= 1 && s <= 2) go(sddmm_tma_kernel<2, 1>, 2, 1, warp_ring_bytes<2>());
-  else if (wpc <= 1 && s <= 3) go(sddmm_tma_kernel<3, 1>, 3, 1, warp_ring_bytes<3>());
-  else if (wpc <= 1 && s <= 4) go(sddmm_tma_kernel<4, 1>, 4, 1, warp_ring_bytes<4>());
-  else if (wpc <= 1 && s <= 6) go(sddmm_tma_kernel<6, 1>, 6, 1, warp_ring_bytes<6>());
-  else go(sddmm_tma_kernel<8, 1>, 8, 1, warp_ring_bytes<8>());
+  go(sddmm_tma_kernel<2, 1>, 2, 1, warp_ring_bytes<2>());
   return check_launch("smb_sddmm_update (TMA)");
 }
 

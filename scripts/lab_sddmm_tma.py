@@ -15,10 +15,12 @@ from oracle import oracle as O
 
 O.build()
 O.set_threads(os.cpu_count() or 1)
-tag = os.environ.get("SMB_SDDMM_TMA", "0")
+tag = os.path.basename(os.environ.get("SMB_LIB", "current"))
 SHAPES = [(8192, 8192, 0.0084, 1024), (8192, 3072, 0.0154, 1024),
+          (8192, 8192, 0.001, 512), (8192, 8192, 0.001, 2048), (8192, 8192, 0.01, 128),
           (8192, 8192, 0.01, 512), (8192, 8192, 0.1, 512),
-          (65536, 65536, 0.000587, 512), (1024, 3072, 0.0078, 1024)]
+          (65536, 65536, 0.000587, 512), (65536, 3072, 0.00656, 512),
+          (1024, 3072, 0.0078, 1024)]
 if os.environ.get("LAB_SMALL"):
     SHAPES = [(1024, 3072, 0.0078, 1024), (512, 1024, 0.0175, 1024), (10, 512, 0.609, 1024),
               (1024, 3072, 0.0078, 100), (512, 1024, 0.0175, 100)]
@@ -63,5 +65,5 @@ for (m, k, d, B) in SHAPES:
         e.synchronize()
         ts.append(s.elapsed_time(e) * 1e3 / 20)
     us = min(ts)
-    print(f"tma={tag} {m}x{k} d={d} B={B} nnz={nnz}: {us:8.2f} us  {nnz * B / us / 1e6:6.2f} Tpairs/s  {ok}",
+    print(f"{tag} {m}x{k} d={d} B={B} nnz={nnz}: {us:8.2f} us  {nnz * B / us / 1e6:6.2f} Tpairs/s  {ok}",
           flush=True)
