@@ -443,7 +443,12 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       // per CTA lower the resident warps and run slower.  Few-wave layers keep
       // the cp.async kernels: one warp's TMA chunks do not overlap well
       // (config-2 layers 10-15 us -> 21-24 us with any ring depth).
-      if (!small32 && !small64 && !mid32 && sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
+      // (rows of >= 16 nonzeros on average: a warp's 32 nonzeros then span
+      // <= 4 rows and read d_out from the ring; very sparse rows -- config 3
+      // d = 0.001, 8 per row -- keep the cp.async pipe with a d_out row per
+      // nonzero: 20 vs 27 us there)
+      if (!small32 && !small64 && !mid32 && pat->nnz >= 16 * pat->m &&
+          sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
         const int rc = launch_sddmm_tma(pat, static_cast<const float*>(d_out), ld_d,
                                         static_cast<const float*>(x), ld_x, n,
                                         static_cast<const float*>(values),

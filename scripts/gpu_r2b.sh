@@ -8,3 +8,5 @@ j=json.loads(sys.stdin.read())
 print(j['value'], j['ms_per_step'], j['e2e']['value'], j['roofline']['kernel'], j['roofline']['frac'])
 for n,e in j['extra_configs'].items(): print(n, e['value'], e['ms_per_step'], e['kernel_us'])
 "
+timeout 600 python scripts/kernel_bench.py > gpurun_out/kernel_bench.log 2>&1; echo "kb exit $?" >> gpurun_out/kernel_bench.log
+tail -10 gpurun_out/kernel_bench.log
