@@ -117,12 +117,15 @@ __global__ void __launch_bounds__(max_threads_for<W>())
                     int64_t n_rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  const int warp_in_cta = threadIdx.x >> 5;
-  const int wpr = (blockDim.x >> 5) / rows_per_cta;  // warps per row
-  const int warp = warp_in_cta % wpr;
-  const int nwarps = wpr;
-  const int64_t row = (int64_t)blockIdx.x * rows_per_cta + warp_in_cta / wpr;
-  if (row >= n_rows) return;  // (rows_per_cta > 1 never takes the fused row-sum path)
+  int warp = threadIdx.x >> 5;
+  int nwarps = blockDim.x >> 5;
+  int64_t row = blockIdx.x;
+  if (rows_per_cta > 1) {  // (never with the fused row-sum epilogue)
+    nwarps /= rows_per_cta;  // warps per row
+    row = (int64_t)blockIdx.x * rows_per_cta + warp / nwarps;
+    warp %= nwarps;
+    if (row >= n_rows) return;
+  }
   const int64_t chunk = (int64_t)blockIdx.y * nwarps + warp;
   const int64_t col0 = chunk * (32 * W) + (int64_t)lane * W;
   const int valid = (int)imax(0, imin(W, n - col0));
