@@ -108,7 +108,7 @@ constexpr int max_threads_for() { return 256; }
 // before the next slice: when the dense operand is wider than L2, the slice
 // width is chosen so the slice's rows stay L2-resident while every output
 // row gathers from them (launch_rows).
-template <typename T, int W, int U, int EPI, bool PERM>
+template <typename T, int W, int U, int EPI, bool PERM, bool MULTI = false>
 __global__ void __launch_bounds__(max_threads_for<W>())
     row_spmm_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
                     const int32_t* __restrict__ perm, const T* __restrict__ vals,
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(max_threads_for<W>())
   int warp = threadIdx.x >> 5;
   int nwarps = blockDim.x >> 5;
   int64_t row = blockIdx.x;
-  if (rows_per_cta > 1) {  // (never with the fused row-sum epilogue)
+  if constexpr (MULTI) {  // several rows per CTA (never with the fused row-sum epilogue)
     nwarps /= rows_per_cta;  // warps per row
     row = (int64_t)blockIdx.x * rows_per_cta + warp / nwarps;
     warp %= nwarps;
@@ -556,7 +556,8 @@ bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm
   size_t dyn = 0;
   if (fuse) dyn = sizeof(T) * (size_t)(((n + 3) & ~int64_t(3)) + warp_pairwise_leaves((int)n));
   epi.rowsum = fuse ? 1 : 0;
-  auto kern = row_spmm_kernel<T, W, U, EPI, PERM>;
+  auto kern = rpc > 1 ? row_spmm_kernel<T, W, U, EPI, PERM, true>
+                      : row_spmm_kernel<T, W, U, EPI, PERM, false>;
   if (dyn > 40 * 1024)
     ensure_smem(kern, dyn);
   launch_k(kern, dim3((unsigned)ceil_div(n_rows, rpc), (unsigned)gy), dim3(warps * rpc * 32), dyn,
