@@ -46,6 +46,19 @@ REPO = Path(__file__).resolve().parent
 sys.path.insert(0, str(REPO))
 
 METRIC = "sparse-MLP train samples/sec vs density; SpMM/SDDMM GB/s vs B200 HBM peak"
+L2_NOTE = ("flushed before every timed step (untimed): a 512 MB write, then a 512 MB read so the "
+           "flush's own dirty lines are written back before the step starts; dataset 614 MB > L2")
+
+
+def flush_l2(buf, sink, i: int) -> None:
+    """Evict L2 before a timed step: write a buffer 4x the 126 MB L2, then read
+    it back, so L2 holds only clean lines of the flush buffer (without the
+    read, ~126 MB of the flush's dirty lines would be written back to HBM
+    during the timed step -- traffic of the flush, not of the workload)."""
+    import torch
+
+    buf.fill_(float(i))
+    torch.sum(buf, out=sink)
 UNIT = "samples/s"
 FALLBACK_HBM_GBS = 6650.0
 
@@ -305,7 +318,7 @@ def config_dict(args, ws):
             "batch_per_gpu": args.batch, "global_batch": args.batch * ws,
             "train_samples": args.samples,
             "parallelism": f"dp{ws}" + (" (data-parallel step structure, forced)" if args.force_dp else ""),
-            "l2": "flushed (512 MB write) before every timed step; dataset 614 MB > L2"}
+            "l2": L2_NOTE}
 
 
 def cpu_step_sample(args, global_batch, budget_s, min_steps=3, max_steps=200):
@@ -397,6 +410,7 @@ class Ctx:
             dist.init_process_group("nccl", device_id=self.dev)
             self.pg = dist.group.WORLD
         self.flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=self.dev)
+        self.sink = torch.empty((), dtype=torch.float32, device=self.dev)
         self.nvml = nvml_index(self.local)
 
     def barrier(self):
@@ -530,7 +544,7 @@ def measure(args, ctx, ddata, data, steps, warmup, e2e=True, launches=True, cloc
         if clk:
             clk.mark_start()
         for i in range(steps):
-            ctx.flush.fill_(float(i))
+            flush_l2(ctx.flush, ctx.sink, i)
             starts[i].record()
             step.step(eta)
             ends[i].record()
@@ -725,6 +739,7 @@ def density_sweep(args, steps=20):
                                  classes=chain[-1])
     ddata = smb.DeviceDataset(data)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device="cuda")
+    sink = torch.empty((), dtype=torch.float32, device="cuda")
     def time_backend(d, B, backend):
         model, plan = smb.build_model(smb.ExperimentConfig(
             layer_dims=chain, density=d, batch_size=B, lr=args.lr, seed=args.seed,
@@ -736,7 +751,7 @@ def density_sweep(args, steps=20):
             st.step(args.lr)
         tot = 0.0
         for i in range(steps):
-            flush.fill_(float(i))
+            flush_l2(flush, sink, i)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
             st.step(args.lr)
