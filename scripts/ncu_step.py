@@ -41,8 +41,13 @@ st.timer = rec
 st.step(0.01)
 torch.cuda.synchronize()
 st.timer = None
-tags = [t for t, name, _ in rec.calls
-        if not t.startswith(("counter", "update")) and name != "smb_step_counter_advance"]
+# C-ABI calls that launch two kernels (both match the profile regex)
+TWO = {"smb_dense_forward_small": (".part", ".sum")}
+tags = []
+for t, name, _ in rec.calls:
+    if t.startswith(("counter", "update")) or name == "smb_step_counter_advance":
+        continue
+    tags += [t + suf for suf in TWO[name]] if name in TWO else [t]
 if tags_file:
     open(tags_file, "w").write(",".join(tags))
 print("ok", len(tags), "tags")

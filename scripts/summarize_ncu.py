@@ -38,7 +38,12 @@ def short(name: str) -> str:
 
 
 def launches(args):
-    rows = [r for r in csv.reader(open(args.src)) if len(r) > 10 and r[0].isdigit()]
+    allrows = [r for r in csv.reader(open(args.src))]
+    hdr = next((r for r in allrows if "Kernel Name" in r), None)
+    kn = hdr.index("Kernel Name") if hdr else 4
+    gs = hdr.index("Grid Size") if hdr else 8
+    bs = hdr.index("Block Size") if hdr else 7
+    rows = [r for r in allrows if len(r) > 10 and r[0].isdigit()]
     rows = [r for r in rows if r[-3] == "gpu__time_duration.sum"]
     if args.per_step:
         rows = rows[-args.per_step:]
@@ -47,10 +52,10 @@ def launches(args):
     lines = ["| # | kernel | grid | block | µs | share |", "|---|---|---|---|---|---|"]
     for i, r in enumerate(rows):
         ns = float(r[-1])
-        lines.append(f"| {i} | `{short(r[4])}` | {r[8]} | {r[7]} | {ns / 1e3:.2f} | "
+        lines.append(f"| {i} | `{short(r[kn])}` | {r[gs]} | {r[bs]} | {ns / 1e3:.2f} | "
                      f"{100 * ns / total:.1f}% |")
-        agg.setdefault(short(r[4]), 0.0)
-        agg[short(r[4])] += ns
+        agg.setdefault(short(r[kn]), 0.0)
+        agg[short(r[kn])] += ns
     lines.append(f"\nserialised sum: {total / 1e3:.2f} µs over {len(rows)} launches "
                  "(ncu: cold caches, serialised, --clock-control none)\n")
     Path(args.out).write_text(args.header + "\n\n" + "\n".join(lines) + "\n")
@@ -89,6 +94,7 @@ def full(args):
         return v * {"ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(u, 1)
 
     tags = args.tags.split(",") if args.tags else [str(i) for i in range(len(data))]
+    kname, grid, block = col.get("Kernel Name", 4), col.get("Grid Size", 8), col.get("Block Size", 7)
     lines = ["| tag | kernel | grid×block | µs | DRAM rd+wr MB | DRAM % | L2→L1 MB | L2 % | L1 % | "
              "inst % (active) | warps/SM | regs | top stalls (per issue) |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
@@ -103,7 +109,7 @@ def full(args):
         st.sort(reverse=True)
         top = ", ".join(f"{s} {v:.2f}" for v, s in st[:3])
         lines.append(
-            f"| {tag} | `{short(r[4])}` | {r[8]}×{r[7]} | {usec(r):.2f} | "
+            f"| {tag} | `{short(r[kname])}` | {r[grid]}×{r[block]} | {usec(r):.2f} | "
             f"{(rd + wr) / 1e6:.2f} | {g(r, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
             f"{nbytes(r, 'l1tex__m_xbar2l1tex_read_bytes.sum') / 1e6:.1f} | "
             f"{g(r, 'lts__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
