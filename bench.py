@@ -58,7 +58,7 @@ def flush_l2(buf, sink, i: int) -> None:
     import torch
 
     buf.fill_(float(i))
-    torch.sum(buf, out=sink)
+    torch.sum(buf, 0, out=sink)
 UNIT = "samples/s"
 FALLBACK_HBM_GBS = 6650.0
 

@@ -10,7 +10,7 @@ timeout 300 $CMD > gpurun_out/${NAME}_plain.log 2>&1 || { echo "plain failed"; c
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k "$RX" \
   --nvtx --nvtx-include "prof/" --log-file gpurun_out/${NAME}_launches.csv $CMD > gpurun_out/${NAME}_ncu1.log 2>&1
 echo "launch list exit $?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k "$RX" \
+timeout 1500 ncu -f --set full --clock-control none --import-source on -k "$RX" \
   --nvtx --nvtx-include "prof/" -o /tmp/${NAME}_full $CMD > gpurun_out/${NAME}_ncu2.log 2>&1
 echo "full exit $?"
 TAGS=$(cat gpurun_out/${NAME}_tags.txt)
