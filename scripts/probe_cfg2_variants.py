@@ -15,11 +15,14 @@ B, L, D = 1024, [3072, 1024, 512, 10], 0.01
 data = smb.synthetic_dataset(seed=0, n_samples=20480, features=L[0], classes=L[-1])
 dd = smb.DeviceDataset(data)
 flush = torch.empty(512 * 2**20 // 4, device="cuda")
+sink = torch.empty((), device="cuda")
 
 
-def run(tag, **kw):
+def run(tag, lab=None, **kw):
     model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=L, density=D, batch_size=B))
     st = smb.FusedTrainStep(model, B, **kw)
+    for k, v in (lab or {}).items():
+        setattr(st, k, v)
     st.attach_dataset(dd)
     st.set_epoch(np.arange(20480))
     for _ in range(6):
@@ -37,6 +40,7 @@ def run(tag, **kw):
     fl = []
     for i in range(40):
         flush.fill_(float(i))
+        torch.sum(flush, 0, out=sink)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         st.step(0.01)
@@ -69,9 +73,9 @@ def timeline(st, steps=4):
 
 if __name__ == "__main__":
     st = run("baseline")
-    timeline(st)
+    st2 = run("sddmm at end", lab={"_lab_sddmm_at_end": True})
     hint = _lib.SMB_HINT_CONCURRENT
     _lib.SMB_HINT_CONCURRENT = 0
-    st2 = run("no concurrent hint")
-    timeline(st2)
+    st3 = run("sddmm at end, no hint", lab={"_lab_sddmm_at_end": True})
     _lib.SMB_HINT_CONCURRENT = hint
+    timeline(st2)
