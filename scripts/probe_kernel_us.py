@@ -14,7 +14,8 @@ L = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3072,1024,512,10").
 D = float(sys.argv[2]) if len(sys.argv) > 2 else 0.01
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
 data = smb.synthetic_dataset(seed=0, n_samples=8 * B, features=L[0], classes=L[-1])
-model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=L, density=D, batch_size=B))
+model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=L, density=D, batch_size=B),
+                          large_patterns=any(a * b >= 2**31 for a, b in zip(L[:-1], L[1:])))
 st = smb.FusedTrainStep(model, B)
 st.attach_dataset(smb.DeviceDataset(data))
 st.set_epoch(np.arange(8 * B))
