@@ -117,15 +117,13 @@ __global__ void __launch_bounds__(max_threads_for<W>())
                     int64_t n_rows) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
-  int warp = threadIdx.x >> 5;
-  int nwarps = blockDim.x >> 5;
-  int64_t row = blockIdx.x;
-  if constexpr (MULTI) {  // several rows per CTA (never with the fused row-sum epilogue)
-    nwarps /= rows_per_cta;  // warps per row
-    row = (int64_t)blockIdx.x * rows_per_cta + warp / nwarps;
-    warp %= nwarps;
-    if (row >= n_rows) return;
-  }
+  const int warp_in_cta = threadIdx.x >> 5;
+  // MULTI: several rows per CTA (never with the fused row-sum epilogue)
+  const int nwarps = MULTI ? (blockDim.x >> 5) / rows_per_cta : (blockDim.x >> 5);  // per row
+  const int warp = MULTI ? warp_in_cta % nwarps : warp_in_cta;
+  const int64_t row =
+      MULTI ? (int64_t)blockIdx.x * rows_per_cta + warp_in_cta / nwarps : (int64_t)blockIdx.x;
+  if (MULTI && row >= n_rows) return;
   const int64_t chunk = (int64_t)blockIdx.y * nwarps + warp;
   const int64_t col0 = chunk * (32 * W) + (int64_t)lane * W;
   const int valid = (int)imax(0, imin(W, n - col0));
