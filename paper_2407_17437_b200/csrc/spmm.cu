@@ -49,31 +49,17 @@ __device__ __forceinline__ void load_frag_full(Frag<T, W>& f, const T* p) {
   }
 }
 
-template <typename T, int W, bool STREAM = false>
+template <typename T, int W>
 __device__ __forceinline__ void load_frag(Frag<T, W>& f, const T* p, int valid) {
   if (valid == W) {
-    if constexpr (STREAM && W > 1) {
-      using V = typename Vec16<T>::type;
-      constexpr int VW = Vec16<T>::N;
-#pragma unroll
-      for (int h = 0; h < W / VW; ++h) {
-        const V v = __ldcs(reinterpret_cast<const V*>(p) + h);
-#pragma unroll
-        for (int j = 0; j < VW; ++j) f.v[h * VW + j] = VecOps<T>::get(v, j);
-      }
-    } else {
-      load_frag_full<T, W>(f, p);
-    }
+    load_frag_full<T, W>(f, p);
     return;
   }
 #pragma unroll
   for (int j = 0; j < W; ++j) f.v[j] = (j < valid) ? __ldg(p + j) : T(0);
 }
 
-// STREAM: evict-first (.cs) accesses for the data that is touched once, so
-// it does not push the L2-resident slice of the gathered operand out
-// (column-sliced launches over operands wider than L2)
-template <typename T, int W, bool STREAM = false>
+template <typename T, int W>
 __device__ __forceinline__ void store_frag(const Frag<T, W>& f, T* p, int valid) {
   if constexpr (W > 1) {
     using V = typename Vec16<T>::type;
@@ -84,8 +70,7 @@ __device__ __forceinline__ void store_frag(const Frag<T, W>& f, T* p, int valid)
         V v;
 #pragma unroll
         for (int j = 0; j < VW; ++j) VecOps<T>::set(v, j, f.v[h * VW + j]);
-        if constexpr (STREAM) __stcs(reinterpret_cast<V*>(p) + h, v);
-        else reinterpret_cast<V*>(p)[h] = v;
+        reinterpret_cast<V*>(p)[h] = v;
       }
       return;
     }
@@ -189,7 +174,7 @@ __global__ void __launch_bounds__(max_threads_for<W>())
   T rb_w = T(0), rb_v = T(0);  // bias state of the fused row-sum update
   if constexpr (EPI == kEpiMask) {
     if (epi.mask != nullptr && valid > 0)
-      load_frag<T, W, MULTI>(mk, epi.mask + row * epi.ld_mask + col0, valid);
+      load_frag<T, W>(mk, epi.mask + row * epi.ld_mask + col0, valid);
     if (epi.rowsum && threadIdx.x == 0 && epi.opt.kind != SMB_OPT_NONE && epi.rb_bias) {
       rb_w = epi.rb_bias[row];
       if (epi.rb_vbias) rb_v = epi.rb_vbias[row];
@@ -258,14 +243,14 @@ __global__ void __launch_bounds__(max_threads_for<W>())
 #pragma unroll
       for (int j = 0; j < W; ++j) acc.v[j] = relu_np(acc.v[j]);
     }
-    store_frag<T, W, MULTI>(acc, out + row * ld_out + col0, valid);
+    store_frag<T, W>(acc, out + row * ld_out + col0, valid);
   } else {
     if (valid > 0) {
       if (epi.mask != nullptr) {
 #pragma unroll
         for (int j = 0; j < W; ++j) acc.v[j] = mask_np(acc.v[j], mk.v[j]);
       }
-      store_frag<T, W, MULTI>(acc, out + row * ld_out + col0, valid);
+      store_frag<T, W>(acc, out + row * ld_out + col0, valid);
     }
     if (!epi.rowsum) return;
     // whole row in this CTA: stage it, pairwise-sum it, update this row's bias
