@@ -195,3 +195,55 @@ def test_l2_sliced_spmm_bit_exact(orc, B):
     _lib.call("smb_spmm_t", 0, pat.handle, ptr(vals), ptr(dY), B, B, ptr(X), B, ptr(out), B, st)
     ref_t = orc.spmm_t(rp, ci, vals_h, k, dy_h) * (x_h > 0)
     assert bits_equal(out.cpu().numpy(), ref_t.astype(np.float32)), "spmm_t + mask"
+
+
+def _pattern_from_row_lengths(lengths, k, rng):
+    rows = [np.sort(rng.choice(k, size=int(L), replace=False)) for L in lengths]
+    row_ptr = np.zeros(len(lengths) + 1, np.int32)
+    np.cumsum(lengths, out=row_ptr[1:])
+    col_idx = np.concatenate(rows).astype(np.int32)
+    return row_ptr, col_idx
+
+
+@pytest.mark.parametrize("n", [1, 37, 100, 1000, 1024])
+@pytest.mark.parametrize("shape", ["uniform", "mixed_rows"])
+def test_tma_sddmm_edge_cases_bit_exact(orc, n, shape):
+    """The TMA gather4 SDDMM (many-wave layers, >= 16 nonzeros per row on
+    average): ragged batch widths (the last 32-column chunk partly out of the
+    tensor map, zero-filled by TMA and never summed), one column, and warps
+    whose 32 nonzeros span more than the 4 staged d_out rows (short rows
+    between long ones: d_out read from global memory) -- bit-exact with the
+    oracle's sddmm + Nesterov sequence (_kernels.py:62-83, nn.py:189-193)."""
+    rng = np.random.default_rng(n)
+    m, k = 6144, 4096
+    if shape == "uniform":
+        lengths = np.full(m, 24)
+    else:  # three 2-nonzero rows, then a 90-nonzero row: average 24
+        lengths = np.tile([2, 2, 2, 90], m // 4)
+    rp, ci = _pattern_from_row_lengths(lengths, k, rng)
+    pat = smb.SparsityPattern(m, k, rp, ci)
+    nnz = ci.shape[0]
+    vals_h = rng.standard_normal(nnz).astype(np.float32)
+    vel_h = (0.1 * rng.standard_normal(nnz)).astype(np.float32)
+    x_h = rng.standard_normal((k, n)).astype(np.float32)
+    dy_h = rng.standard_normal((m, n)).astype(np.float32)
+    dev = torch.device("cuda")
+    ld = (n + 3) // 4 * 4  # 16-byte rows (the TMA path's requirement)
+    X = torch.zeros(k, ld, device=dev)
+    dY = torch.zeros(m, ld, device=dev)
+    X[:, :n] = torch.from_numpy(x_h)
+    dY[:, :n] = torch.from_numpy(dy_h)
+    vals = torch.from_numpy(vals_h).to(dev)
+    vel = torch.from_numpy(vel_h).to(dev)
+    vout = torch.empty_like(vals)
+    mu, eta = 0.9, 1e-3
+    _lib.call("smb_sddmm_update_into", 0, pat.handle, ptr(dY), ld, ptr(X), ld, n, ptr(vals),
+              ptr(vout), ptr(vel), None, None, None, None, _lib.SMB_OPT_NESTEROV, mu, eta,
+              stream_ptr())
+    g = orc.sddmm(rp, ci, dy_h, x_h)
+    v_ref, w_ref = vel_h.copy(), vals_h.copy()
+    orc.axpby(mu, v_ref, 1.0, g)
+    orc.axpby(1.0, w_ref, -eta * mu, v_ref)
+    orc.axpby(1.0, w_ref, -eta, g)
+    assert bits_equal(vel.cpu().numpy(), v_ref)
+    assert bits_equal(vout.cpu().numpy(), w_ref)
