@@ -4,6 +4,8 @@
 // _kernels.spmm_t_kernel, _kernels.py:40-59) and the SDDMM tile index.
 #include <vector>
 
+#include <cmath>
+
 #include "pattern.cuh"
 
 namespace smb {
@@ -135,6 +137,8 @@ void free_pattern(smb_pattern* p) {
   cudaFree(p->row_idx);
   cudaFree(p->perm);
   cudaFree(p->tile_row0);
+  cudaFree(p->ord_p);
+  cudaFree(p->ord_row);
   delete p;
 }
 
@@ -250,6 +254,41 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
     p->span64 = span(64 / kTileGrain);
     p->span128 = span(128 / kTileGrain);
     p->span512 = span(512 / kTileGrain);
+  }
+  if (m >= kBlockedMinDim && k >= kBlockedMinDim && nnz >= 4 * kBlockNnz) {
+    // L2-blocked order: b x b (row band, column band) blocks of ~kBlockNnz
+    // nonzeros (about one wave of resident SDDMM warps), stable counting sort
+    // of the CSR order by block
+    std::vector<int32_t> rp(m + 1), ci(nnz);
+    if (cudaMemcpy(rp.data(), row_ptr, sizeof(int32_t) * (m + 1), cudaMemcpyDeviceToHost) !=
+            cudaSuccess ||
+        cudaMemcpy(ci.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+      return fail_cuda("blocked order readback");
+    const int b = (int)imin(16, imax(2, llround(std::sqrt((double)nnz / (double)kBlockNnz))));
+    const int nblk = b * b;
+    std::vector<int64_t> start(nblk + 1, 0);
+    auto block_of = [&](int64_t r, int64_t c) {
+      return (int)((r * b) / m) * b + (int)((c * b) / k);
+    };
+    for (int64_t r = 0; r < m; ++r)
+      for (int32_t q = rp[r]; q < rp[r + 1]; ++q) start[block_of(r, ci[q]) + 1]++;
+    for (int i = 0; i < nblk; ++i) start[i + 1] += start[i];
+    std::vector<int32_t> op(nnz), orow(nnz);
+    for (int64_t r = 0; r < m; ++r)
+      for (int32_t q = rp[r]; q < rp[r + 1]; ++q) {
+        const int64_t dst = start[block_of(r, ci[q])]++;
+        op[dst] = q;
+        orow[dst] = (int32_t)r;
+      }
+    if (cudaMalloc(&p->ord_p, sizeof(int32_t) * nnz) != cudaSuccess ||
+        cudaMalloc(&p->ord_row, sizeof(int32_t) * nnz) != cudaSuccess ||
+        cudaMemcpy(p->ord_p, op.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice) !=
+            cudaSuccess ||
+        cudaMemcpy(p->ord_row, orow.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice) !=
+            cudaSuccess)
+      return fail_cuda("blocked order");
+    p->bands = b;
   }
   *out = p;
   return SMB_OK;

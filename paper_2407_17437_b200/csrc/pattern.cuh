@@ -17,11 +17,20 @@ struct smb_pattern {
   // most rows spanned by any tile of 32 / 64 / 128 / 512 consecutive nonzeros
   // (aligned; first row .. row of the last nonzero)
   int64_t span32 = 0, span64 = 0, span128 = 0, span512 = 0;
+  // L2-blocked nonzero order for the SDDMM of very wide layers (m, k >= 16384):
+  // the nonzeros grouped by (row band, column band) blocks of about one wave
+  // of resident warps, CSR order inside a block (sddmm_tma.cu).  ord_p[q] is
+  // the CSR index of the q-th nonzero in that order, ord_row[q] its row.
+  int32_t* ord_p = nullptr;    // owned, [nnz] or null
+  int32_t* ord_row = nullptr;  // owned, [nnz] or null
+  int bands = 0;
 };
 
 namespace smb {
 constexpr int kSddmmTile = 128;  // nonzeros per SDDMM CTA (one per thread)
 constexpr int kTileGrain = 32;   // granularity of the tile -> first-row table
+constexpr int64_t kBlockedMinDim = 16384;  // layers that get the L2-blocked SDDMM order
+constexpr int64_t kBlockNnz = 104000;      // ~ 148 SMs x 22 resident warps x 32 nonzeros
 }
 
 namespace smb {
@@ -54,4 +63,7 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
                      int64_t ld_x, int64_t n, const float* values, float* values_out,
                      float* velocity, float* grad_out, const OptConsts<float>& opt,
                      cudaStream_t st);
+// the batch is so wide that x and d_out overflow L2 many times over: walk
+// the nonzeros in the pattern's blocked order (when it has one)
+bool sddmm_use_blocked_order(const smb_pattern* pat, int64_t n);
 }  // namespace smb

@@ -81,11 +81,19 @@ __device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap* map
       : "memory");
 }
 
-template <int S, int WPC>
+// ORD: the warps walk the pattern's L2-blocked nonzero order (ord_p /
+// ord_row, pattern.cu) instead of CSR order: a wave of resident warps then
+// gathers the x and d_out rows of one (row band, column band) block, so each
+// row segment is fetched from HBM about once per block instead of once per
+// wave (config 5 at B = 4096: x and d_out are 1 GB each).  The chains, their
+// order over the batch and the update are unchanged; results land at the
+// nonzero's CSR index.
+template <int S, int WPC, bool ORD>
 __global__ void __launch_bounds__(32 * WPC)
     sddmm_tma_kernel(const __grid_constant__ CUtensorMap xmap,
                      const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ row_ptr,
                      const int32_t* __restrict__ col_idx, const int32_t* __restrict__ tile_row0,
+                     const int32_t* __restrict__ ord_p, const int32_t* __restrict__ ord_row,
                      int64_t m, int64_t nnz, const float* __restrict__ d_out, int64_t ld_d, int n,
                      const float* values, float* values_out, float* velocity, float* grad_out,
                      OptConsts<float> opt) {
@@ -102,11 +110,15 @@ __global__ void __launch_bounds__(32 * WPC)
   const int64_t p0 = (int64_t)blockIdx.x * kTile;
   const int64_t pw = p0 + warp * 32;
   const int nw = (int)imax(0, imin(32, nnz - pw));
-  const int64_t p = pw + lane;
   const bool active = lane < nw;
-  const int32_t r0 = tile_row0[(int64_t)blockIdx.x * (kTile / kTileGrain)];
-  s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
-  if (tid == 0) s_rp[kTile] = (r0 + kTile <= m) ? row_ptr[r0 + kTile] : INT32_MAX;
+  // p: the CSR index of this lane's nonzero
+  const int64_t p = ORD ? (active ? (int64_t)ord_p[pw + lane] : 0) : pw + lane;
+  int32_t r0 = 0;
+  if constexpr (!ORD) {
+    r0 = tile_row0[(int64_t)blockIdx.x * (kTile / kTileGrain)];
+    s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
+    if (tid == 0) s_rp[kTile] = (r0 + kTile <= m) ? row_ptr[r0 + kTile] : INT32_MAX;
+  }
   const int32_t my_col = active ? col_idx[p] : 0;
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(smem_addr(&s_full[warp][s]), 1);
@@ -114,12 +126,35 @@ __global__ void __launch_bounds__(32 * WPC)
   }
   __syncthreads();  // the only CTA-wide barrier (row window + barrier init)
   if (nw == 0) return;
-  const int64_t row = tile_row_of<kTile>(active ? p : pw, r0, s_rp, row_ptr, m);
-  const int64_t row_first = __shfl_sync(0xffffffffu, row, 0);
-  const int64_t row_last = __shfl_sync(0xffffffffu, row, nw - 1);
-  const int span = (int)(row_last - row_first + 1);
-  const bool staged = span <= kTmaDSlots;  // warp-uniform
-  const int slot = (int)(row - row_first);
+  int64_t row;
+  int slot, n_slots;
+  int64_t slot_row[kTmaDSlots];
+  if constexpr (ORD) {
+    // d_out slots = runs of equal rows among the warp's nonzeros (rows are
+    // non-decreasing inside a block)
+    row = active ? (int64_t)ord_row[pw + lane] : (int64_t)ord_row[pw];
+    const int64_t prev = __shfl_up_sync(0xffffffffu, row, 1);
+    const unsigned runs = __ballot_sync(0xffffffffu, active && (lane == 0 || row != prev));
+    slot = __popc(runs & (0xffffffffu >> (31 - lane))) - 1;
+    n_slots = __popc(runs);
+    unsigned rest = runs;
+#pragma unroll
+    for (int q = 0; q < kTmaDSlots; ++q) {
+      const int src = rest ? __ffs(rest) - 1 : 0;
+      const int64_t r = __shfl_sync(0xffffffffu, row, src);
+      slot_row[q] = rest ? r : (q > 0 ? slot_row[q - 1] : r);
+      rest &= rest - 1;
+    }
+  } else {
+    row = tile_row_of<kTile>(active ? p : pw, r0, s_rp, row_ptr, m);
+    const int64_t row_first = __shfl_sync(0xffffffffu, row, 0);
+    const int64_t row_last = __shfl_sync(0xffffffffu, row, nw - 1);
+    n_slots = (int)(row_last - row_first + 1);
+    slot = (int)(row - row_first);
+#pragma unroll
+    for (int q = 0; q < kTmaDSlots; ++q) slot_row[q] = imin(row_first + imin(q, n_slots - 1), m - 1);
+  }
+  const bool staged = n_slots <= kTmaDSlots;  // warp-uniform
   const int n_chunks = (n + 31) / 32;
   // copy roles: lane g < 8 gathers x rows 4g..4g+3, lane 8 the d_out rows
   int gr[4];
@@ -130,7 +165,7 @@ __global__ void __launch_bounds__(32 * WPC)
   }
   if (lane == 8) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) gr[q] = (int)imin(row_first + imin(q, span - 1), m - 1);
+    for (int q = 0; q < 4; ++q) gr[q] = (int)slot_row[q];
   }
   const bool copier = lane < 8 || (lane == 8 && staged);
   const unsigned tx_bytes = 32 * 128 + (staged ? kTmaDSlots * 128 : 0);
@@ -235,6 +270,11 @@ bool make_row_map(CUtensorMap* map, const float* ptr, int64_t rows, int64_t cols
 
 }  // namespace
 
+bool sddmm_use_blocked_order(const smb_pattern* pat, int64_t n) {
+  // x + d_out at least 4x the 126 MB L2
+  return pat->ord_p != nullptr && (pat->m + pat->k) * n * (int64_t)sizeof(float) > (512ll << 20);
+}
+
 // The TMA variant applies to fp32, 16-byte aligned operands whose leading
 // dimensions are multiples of 4 elements, and rows < 2^31.
 bool sddmm_tma_supported(const smb_pattern* pat, const void* d_out, int64_t ld_d, const void* x,
@@ -257,10 +297,13 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
     const size_t smem = (size_t)wpc * ring + 1024;
     ensure_smem(kernel, smem);
     launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, 32 * wpc)), dim3(32 * wpc), smem, st,
-             xmap, dmap, pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz, d_out,
-             ld_d, (int)n, values, values_out, velocity, grad_out, opt);
+             xmap, dmap, pat->row_ptr, pat->col_idx, pat->tile_row0, pat->ord_p, pat->ord_row,
+             pat->m, pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity, grad_out, opt);
   };
-  go(sddmm_tma_kernel<2, 1>, 2, 1, warp_ring_bytes<2>());
+  if (sddmm_use_blocked_order(pat, n))
+    go(sddmm_tma_kernel<2, 1, true>, 2, 1, warp_ring_bytes<2>());
+  else
+    go(sddmm_tma_kernel<2, 1, false>, 2, 1, warp_ring_bytes<2>());
   return check_launch("smb_sddmm_update (TMA)");
 }
 

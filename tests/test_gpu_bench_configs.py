@@ -247,3 +247,44 @@ def test_tma_sddmm_edge_cases_bit_exact(orc, n, shape):
     orc.axpby(1.0, w_ref, -eta, g)
     assert bits_equal(vel.cpu().numpy(), v_ref)
     assert bits_equal(vout.cpu().numpy(), w_ref)
+
+
+def test_blocked_order_sddmm_bit_exact(orc):
+    """Very wide layers (m, k >= 16384) whose x and d_out overflow L2 many
+    times at the batch width walk their nonzeros in the pattern's L2-blocked
+    order (row band x column band blocks, CSR order inside); each chain and
+    the update are unchanged and land at the CSR index: bit-exact with the
+    oracle, ragged batch width included."""
+    m = k = 30000
+    n = 2300  # (m + k) * n * 4 bytes > 512 MB -> blocked order
+    nnz = int(0.0005 * m * k)
+    pat = smb.sample_pattern(m, k, nnz, smb.Rng(2).stream("pattern"))
+    rp, ci = pat.host_arrays()
+    rng = np.random.default_rng(5)
+    vals_h = rng.standard_normal(nnz).astype(np.float32)
+    vel_h = (0.1 * rng.standard_normal(nnz)).astype(np.float32)
+    x_h = rng.standard_normal((k, n)).astype(np.float32)
+    dy_h = rng.standard_normal((m, n)).astype(np.float32)
+    dev = torch.device("cuda")
+    ld = (n + 3) // 4 * 4
+    X = torch.zeros(k, ld, device=dev)
+    dY = torch.zeros(m, ld, device=dev)
+    X[:, :n] = torch.from_numpy(x_h)
+    dY[:, :n] = torch.from_numpy(dy_h)
+    vals = torch.from_numpy(vals_h).to(dev)
+    vel = torch.from_numpy(vel_h).to(dev)
+    vout = torch.empty_like(vals)
+    gout = torch.empty_like(vals)
+    mu, eta = 0.9, 1e-3
+    _lib.call("smb_sddmm", 0, pat.handle, ptr(dY), ld, ptr(X), ld, n, ptr(gout), stream_ptr())
+    _lib.call("smb_sddmm_update_into", 0, pat.handle, ptr(dY), ld, ptr(X), ld, n, ptr(vals),
+              ptr(vout), ptr(vel), None, None, None, None, _lib.SMB_OPT_NESTEROV, mu, eta,
+              stream_ptr())
+    g = orc.sddmm(rp, ci, dy_h, x_h)
+    assert bits_equal(gout.cpu().numpy(), g)
+    v_ref, w_ref = vel_h.copy(), vals_h.copy()
+    orc.axpby(mu, v_ref, 1.0, g)
+    orc.axpby(1.0, w_ref, -eta * mu, v_ref)
+    orc.axpby(1.0, w_ref, -eta, g)
+    assert bits_equal(vel.cpu().numpy(), v_ref)
+    assert bits_equal(vout.cpu().numpy(), w_ref)
