@@ -40,14 +40,14 @@ namespace smb {
 namespace {
 
 constexpr int kTmaXBytes = 32 * 128;  // x rows of one stage (1024-byte aligned blocks)
-constexpr int kTmaDSlots = 4;
-constexpr int kTmaDBytes = kTmaDSlots * 128;  // d_out rows of one stage (512-byte blocks)
+// d_out rows staged per stage: 4 (one gather4) in CSR order, 8 (two) in the
+// blocked order, where a warp's 32 nonzeros span more rows
 // shared memory of one warp's ring: S x-blocks, then S d-blocks, rounded to
 // the 1024-byte swizzle atom (the hardware swizzle follows address bits
 // 7-9, so 512-byte aligned gather4 destinations are fine)
-template <int S>
+template <int S, int DS>
 __host__ __device__ constexpr int warp_ring_bytes() {
-  return (S * (kTmaXBytes + kTmaDBytes) + 1023) / 1024 * 1024;
+  return (S * (kTmaXBytes + DS * 128) + 1023) / 1024 * 1024;
 }
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -88,7 +88,7 @@ __device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap* map
 // wave (config 5 at B = 4096: x and d_out are 1 GB each).  The chains, their
 // order over the batch and the update are unchanged; results land at the
 // nonzero's CSR index.
-template <int S, int WPC, bool ORD>
+template <int S, int WPC, bool ORD, int DS = ORD ? 8 : 4>
 __global__ void __launch_bounds__(32 * WPC)
     sddmm_tma_kernel(const __grid_constant__ CUtensorMap xmap,
                      const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ row_ptr,
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32 * WPC)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // dynamic smem rounded up to 1024 bytes (the 128-byte swizzle atom)
   const unsigned raw = smem_addr(smem_raw);
-  const unsigned base = ((raw + 1023u) & ~1023u) + (unsigned)(warp * warp_ring_bytes<S>());
+  const unsigned base = ((raw + 1023u) & ~1023u) + (unsigned)(warp * warp_ring_bytes<S, DS>());
   const unsigned dbase = base + S * kTmaXBytes;
   const unsigned char* gbase = smem_raw + (base - raw);
   const int64_t p0 = (int64_t)blockIdx.x * kTile;
@@ -128,6 +128,8 @@ __global__ void __launch_bounds__(32 * WPC)
   if (nw == 0) return;
   int64_t row;
   int slot, n_slots;
+  constexpr int kTmaDSlots = DS;
+  constexpr int kTmaDBytes = DS * 128;
   int64_t slot_row[kTmaDSlots];
   if constexpr (ORD) {
     // d_out slots = runs of equal rows among the warp's nonzeros (rows are
@@ -163,11 +165,14 @@ __global__ void __launch_bounds__(32 * WPC)
     const int src = (lane < 8) ? 4 * lane + q : 0;
     gr[q] = __shfl_sync(0xffffffffu, my_col, src);
   }
-  if (lane == 8) {
+  // lanes 8 (and 9) gather the staged d_out rows 0-3 (4-7)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) gr[q] = (int)slot_row[q];
-  }
-  const bool copier = lane < 8 || (lane == 8 && staged);
+  for (int g = 0; g < DS / 4; ++g)
+    if (lane == 8 + g) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) gr[q] = (int)slot_row[4 * g + q];
+    }
+  const bool copier = lane < 8 || (staged && lane < 8 + DS / 4);
   const unsigned tx_bytes = 32 * 128 + (staged ? kTmaDSlots * 128 : 0);
   pdl_wait();  // d_out / x are earlier kernels' outputs
   const bool upd = active && opt.kind != SMB_OPT_NONE;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(32 * WPC)
     __syncwarp();
     if (copier)
       tma_gather4(lane < 8 ? base + (unsigned)(s * kTmaXBytes + lane * 512)
-                           : dbase + (unsigned)(s * kTmaDBytes),
+                           : dbase + (unsigned)(s * kTmaDBytes + (lane - 8) * 512),
                   lane < 8 ? &xmap : &dmap, ch * 32, gr[0], gr[1], gr[2], gr[3], bar);
   };
   for (int c = 0; c < S && c < n_chunks; ++c) issue(c);
@@ -301,9 +306,9 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
              pat->m, pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity, grad_out, opt);
   };
   if (sddmm_use_blocked_order(pat, n))
-    go(sddmm_tma_kernel<2, 1, true>, 2, 1, warp_ring_bytes<2>());
+    go(sddmm_tma_kernel<2, 1, true>, 2, 1, warp_ring_bytes<2, 8>());
   else
-    go(sddmm_tma_kernel<2, 1, false>, 2, 1, warp_ring_bytes<2>());
+    go(sddmm_tma_kernel<2, 1, false>, 2, 1, warp_ring_bytes<2, 4>());
   return check_launch("smb_sddmm_update (TMA)");
 }
 
