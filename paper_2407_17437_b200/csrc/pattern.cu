@@ -265,6 +265,8 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
         cudaMemcpy(ci.data(), col_idx, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost) !=
             cudaSuccess)
       return fail_cuda("blocked order readback");
+    // (measured at config 5, B = 4096: 3 / 4 / 5 / 7 / 10 bands -> 6.27 / 6.05 /
+    // 6.05 / 6.16 / 9.56 ms; CSR order 7.02 ms)
     const int b = (int)imin(16, imax(2, llround(std::sqrt((double)nnz / (double)kBlockNnz))));
     const int nblk = b * b;
     std::vector<int64_t> start(nblk + 1, 0);
