@@ -40,12 +40,11 @@ struct SddmmCfg {
   // staged d_out rows per tile: TILE/4 (rows of >= 4 nonzeros on average),
   // or TILE (SD = 1) for very sparse layers whose tiles span ~1 row per nonzero
   static constexpr int SLOTS = TILE / SD;
-  // power-of-two ring (stage = chunk & (STAGES-1)); defaults:
+  // ring of STAGES stages (stage = chunk % STAGES); defaults:
   //   fp32 512-tile x 32 cols x 2 stages = 184 KB (1 CTA, 16 warps / SM),
   //   fp32 128-tile x 64 cols x 2 stages =  87 KB (2 CTAs / SM),
   //   fp64 128-tile x 16 cols x 4 stages =  92 KB
   static constexpr int STAGES = ST;
-  static_assert((STAGES & (STAGES - 1)) == 0, "power-of-two ring");
   static constexpr size_t stage_elems = size_t(TILE + SLOTS) * LDS;
   static constexpr size_t smem_bytes = STAGES * stage_elems * sizeof(T);
   static_assert(TILE % VPR == 0, "tile / vector split");
@@ -130,7 +129,7 @@ __global__ void __launch_bounds__(TILE)
   const int n_fast = n32 / kChunk;
   const int n_full = VEC ? n_fast : 0;
   auto issue_full = [&](int ch) {
-    const unsigned st = sbase + (unsigned)(ch & (S - 1)) * kStageBytes;
+    const unsigned st = sbase + (unsigned)(ch % S) * kStageBytes;
     const int t0 = ch * kChunk;
 #pragma unroll
     for (int k = 0; k < VPR; ++k) cp_async16(st + xdst[k], xsrc[k] + t0);
@@ -139,7 +138,7 @@ __global__ void __launch_bounds__(TILE)
       if (dcopy[c]) cp_async16(st + ddst[c], dsrc[c] + t0);
   };
   auto issue_part = [&](int ch) {
-    const unsigned st = sbase + (unsigned)(ch & (S - 1)) * kStageBytes;
+    const unsigned st = sbase + (unsigned)(ch % S) * kStageBytes;
     const int t0 = ch * kChunk;
     // elements of this thread's vector inside [0, n)
     const int valid = max(0, min(VW, n32 - (t0 + v * VW)));
@@ -170,7 +169,7 @@ __global__ void __launch_bounds__(TILE)
     if (nx < n_full) issue_full(nx);
     else if (nx < n_chunks) issue_part(nx);
     cp_async_commit();
-    const T* xs = smem + (ch & (S - 1)) * C::stage_elems;
+    const T* xs = smem + (ch % S) * C::stage_elems;
     const T* xr = xs + tid * LDS;
     const T* dr = xs + (TILE + rslot) * LDS;
     const int t0 = ch * kChunk;
@@ -192,7 +191,7 @@ __global__ void __launch_bounds__(TILE)
   if (ch < n_chunks) {  // ragged last chunk (no further copies to issue)
     cp_async_wait<0>();
     __syncthreads();
-    const T* xs = smem + (ch & (S - 1)) * C::stage_elems;
+    const T* xs = smem + (ch % S) * C::stage_elems;
     const T* xr = xs + tid * LDS;
     const T* dr = xs + (TILE + rslot) * LDS;
     const int t0 = ch * kChunk;
@@ -463,13 +462,20 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       }
     }
     if (warp_done) {
-    } else if (sizeof(T) == 4 && mid32) SMB_GO_SD(32, 32, 4, 4);
+    } else if (sizeof(T) == 4 && mid32)
+      // 6 stages, 4 staged d_out rows (31 KB, 7 CTAs per SM): 5 chunks in
+      // flight; slower alone than 4 x 8 (15.9 vs 15.0 us) but the config-2
+      // step runs 71.7 -> 70.9 us back to back (scripts/gpu_probe_us.sh sweep
+      // over 3-7 stages x 4/8 rows)
+      SMB_GO_SD(32, 32, 6, 8);
     else if (sizeof(T) == 4 && small32 && all_for(32, 4) && concurrent)
       // beside other kernels (the overlapped training step) the 2-stage ring
       // (12 KB per CTA instead of 46 KB) leaves shared memory to the kernels
       // on the critical path: config-2 step 76.3 -> 74.6 us back to back
       // although this kernel alone is 1.1-1.2x slower
-      SMB_GO_SD(32, 32, 2, 4);
+      // (3 stages with 4 staged d_out rows, 17 KB: 70.7 -> 70.2 us/step
+      // against 2 stages x 8 rows; 2-4 stages x 4/8 rows measured)
+      SMB_GO_SD(32, 32, 3, 8);
     else if (sizeof(T) == 4 && small32 && all_for(32, 4)) SMB_GO_SD(32, 32, 8, 4);
     else if (sizeof(T) == 4 && small32) SMB_GO_SD(32, 32, 8, 1);
     else if (sizeof(T) == 4 && small64 && !mid32 && all_for(64, 4)) SMB_GO_SD(64, 32, 4, 4);
