@@ -101,3 +101,52 @@ def test_two_rank_engine_matches_global_batch(tmp_path, chain, density, bucketed
     for n, t in model.parameters():
         err = rel_err(ranks[0][n], t.detach().cpu().numpy().reshape(-1))
         assert err <= 1e-5, (n, err)
+
+
+def _nccl_worker(rank, port, outdir):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    import paper_2407_17437_b200 as smb
+
+    data = _data()
+    model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=CHAIN, density=DENS, seed=SEED,
+                                                    batch_size=B_GLOBAL, lr=ETA))
+    step = smb.FusedTrainStep(model, B_GLOBAL, process_group=dist.group.WORLD)
+    assert step.dp and step.bucketed and step.graph_comm and step.use_graph
+    step.attach_dataset(smb.DeviceDataset(data))
+    step.set_epoch(np.random.default_rng(7).permutation(B_GLOBAL * STEPS))
+    for _ in range(STEPS):
+        step.step(ETA)  # from the 2nd step on: graph replays with the captured NCCL buckets
+    torch.cuda.synchronize()
+    params = {n: t.detach().cpu().numpy().reshape(-1) for n, t in model.parameters()}
+    np.savez(os.path.join(outdir, "nccl.npz"), **params)
+    dist.destroy_process_group()
+
+
+def test_nccl_world_of_one_graph_captured_buckets_equal_fused(tmp_path):
+    """The per-layer NCCL all-reduce buckets captured into the step's CUDA
+    graph (the bench's multi-GPU path), run over a world of one: the
+    collectives are the identity, so the parameters must equal the plain
+    fused single-GPU step bit for bit -- the capture, the stream joins and the
+    per-layer update placement are exercised exactly as at N GPUs."""
+    import torch.multiprocessing as mp
+
+    import paper_2407_17437_b200 as smb
+
+    mp.start_processes(_nccl_worker, args=(_free_port(), str(tmp_path)), nprocs=1, join=True,
+                       start_method="spawn")
+    got = np.load(tmp_path / "nccl.npz")
+    data = _data()
+    model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=CHAIN, density=DENS, seed=SEED,
+                                                    batch_size=B_GLOBAL, lr=ETA))
+    step = smb.FusedTrainStep(model, B_GLOBAL)
+    step.attach_dataset(smb.DeviceDataset(data))
+    step.set_epoch(np.random.default_rng(7).permutation(B_GLOBAL * STEPS))
+    for _ in range(STEPS):
+        step.step(ETA)
+    torch.cuda.synchronize()
+    for n, t in model.parameters():
+        assert bits_equal(got[n], t.detach().cpu().numpy().reshape(-1)), n
