@@ -114,7 +114,9 @@ def _nccl_worker(rank, port, outdir):
     data = _data()
     model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=CHAIN, density=DENS, seed=SEED,
                                                     batch_size=B_GLOBAL, lr=ETA))
-    step = smb.FusedTrainStep(model, B_GLOBAL, process_group=dist.group.WORLD)
+    # (a world of one runs the single-GPU step unless the data-parallel
+    # structure is forced -- bench.py --force-dp does the same)
+    step = smb.FusedTrainStep(model, B_GLOBAL, process_group=dist.group.WORLD, force_dp=True)
     assert step.dp and step.bucketed and step.graph_comm and step.use_graph
     step.attach_dataset(smb.DeviceDataset(data))
     step.set_epoch(np.random.default_rng(7).permutation(B_GLOBAL * STEPS))
