@@ -62,8 +62,16 @@ class ExperimentConfig:
     eval_metrics: bool = True
     shuffle: bool = True
     augment: bool = False
+    # B200 additions (no reference counterpart): data-parallel world size the
+    # batch is sharded over (sgd_train's process_group must match) and the
+    # CUDA device the model lives on
+    world_size: int = 1
+    device: str = "cuda"
 
     def __post_init__(self):
+        if self.world_size < 1 or self.batch_size % self.world_size:
+            raise ConfigurationError(
+                f"batch_size {self.batch_size} must be divisible by world_size {self.world_size}")
         if not 0.0 < self.density <= 1.0:
             raise ConfigurationError(f"density must be in (0, 1], got {self.density}")
         if self.backend not in ("sparse", "masked"):
@@ -104,8 +112,15 @@ def build_model(config: ExperimentConfig, large_patterns: bool = False,
             model.add(Sparse(n_out, dens, activation=act, optimizer=opt, nnz=nnz))
         else:
             model.add(MaskedDense(n_out, dens, activation=act, optimizer=opt, nnz=nnz))
-    model.compile(input_size=config.layer_dims[0], batch_size=config.batch_size, seed=config.seed,
-                  large_patterns=large_patterns, pattern_sampler=pattern_sampler)
+    import torch
+
+    dev = torch.device(config.device)
+    if dev.type != "cuda":
+        raise ConfigurationError(f"the B200 path runs on CUDA devices, got {config.device!r}")
+    with torch.cuda.device(dev.index if dev.index is not None else torch.cuda.current_device()):
+        model.compile(input_size=config.layer_dims[0], batch_size=config.batch_size,
+                      seed=config.seed, large_patterns=large_patterns,
+                      pattern_sampler=pattern_sampler)
     return model, plan
 
 
