@@ -17,7 +17,8 @@ batch = int(sys.argv[3]) if len(sys.argv) > 3 else 1024
 warm = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 tags_file = sys.argv[5] if len(sys.argv) > 5 else None
 model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=layers, density=density,
-                                                batch_size=batch, lr=0.01))
+                                                batch_size=batch, lr=0.01),
+                           large_patterns=any(a * b >= 2**31 for a, b in zip(layers[:-1], layers[1:])))
 n = max(8192, 2 * batch)
 data = smb.synthetic_dataset(seed=0, n_samples=n, features=layers[0], classes=layers[-1])
 st = smb.FusedTrainStep(model, batch, use_graph=False)
