@@ -108,7 +108,7 @@ constexpr int max_threads_for() { return 256; }
 // before the next slice: when the dense operand is wider than L2, the slice
 // width is chosen so the slice's rows stay L2-resident while every output
 // row gathers from them (launch_rows).
-template <typename T, int W, int U, int EPI, bool PERM, bool MULTI = false>
+template <typename T, int W, int U, int EPI, bool PERM, bool MULTI = false, bool ROWSUM = false>
 __global__ void __launch_bounds__(max_threads_for<W>())
     row_spmm_kernel(const int32_t* __restrict__ seg_ptr, const int32_t* __restrict__ idx,
                     const int32_t* __restrict__ perm, const T* __restrict__ vals,
@@ -252,6 +252,11 @@ __global__ void __launch_bounds__(max_threads_for<W>())
       }
       store_frag<T, W>(acc, out + row * ld_out + col0, valid);
     }
+    // (the row-sum stage is its own instantiation: compiled into every
+    // transposed launch it cost config 4's SpMM-T 2.4%, 142.2 vs 138.9 us)
+    if constexpr (!ROWSUM) {
+      return;
+    } else {
     if (!epi.rowsum) return;
     // whole row in this CTA: stage it, pairwise-sum it, update this row's bias
     T* s_row = reinterpret_cast<T*>(smem_raw);
@@ -270,6 +275,7 @@ __global__ void __launch_bounds__(max_threads_for<W>())
           if (epi.rb_vbias) epi.rb_vbias[row] = rb_v;
         }
       }
+    }
     }
   }
 }
@@ -554,8 +560,9 @@ bool launch_rows(const int32_t* seg_ptr, const int32_t* idx, const int32_t* perm
   size_t dyn = 0;
   if (fuse) dyn = sizeof(T) * (size_t)(((n + 3) & ~int64_t(3)) + warp_pairwise_leaves((int)n));
   epi.rowsum = fuse ? 1 : 0;
-  auto kern = rpc > 1 ? row_spmm_kernel<T, W, U, EPI, PERM, true>
-                      : row_spmm_kernel<T, W, U, EPI, PERM, false>;
+  auto kern = fuse      ? row_spmm_kernel<T, W, U, EPI, PERM, false, EPI == kEpiMask>
+              : rpc > 1 ? row_spmm_kernel<T, W, U, EPI, PERM, true>
+                        : row_spmm_kernel<T, W, U, EPI, PERM, false>;
   if (dyn > 40 * 1024)
     ensure_smem(kern, dyn);
   launch_k(kern, dim3((unsigned)ceil_div(n_rows, rpc), (unsigned)gy), dim3(warps * rpc * 32), dyn,

@@ -52,3 +52,27 @@ t_mask = timeit(lambda: _lib.call("smb_spmm_t_csc", 0, pat.handle, ptr(vcsc), pt
 t_nomask = timeit(lambda: _lib.call("smb_spmm_t_csc", 0, pat.handle, ptr(vcsc), ptr(dY), B, B,
                                     None, 0, ptr(out), B, stream_ptr()))
 print(f"B={B}: spmm {fwd:.1f} us, spmm_t+mask {t_mask:.1f} us, spmm_t {t_nomask:.1f} us")
+
+# the same product through the forward kernel on W^T stored as CSR
+cp = torch.empty(k + 1, dtype=torch.int32, device=dev)
+ri = torch.empty(nnz, dtype=torch.int32, device=dev)
+_lib.call("smb_pattern_csc", pat.handle, ptr(cp), ptr(ri), None, stream_ptr())
+patT = smb.SparsityPattern(k, m, cp, ri, validate=False)
+out2 = torch.empty(k, B, device=dev)
+t_fwdT = timeit(lambda: _lib.call("smb_spmm_p", 0, patT.handle, ptr(vcsc), ptr(dY), B, B, None, 0,
+                                  ptr(out2), B, stream_ptr()))
+_lib.call("smb_spmm_t_csc", 0, pat.handle, ptr(vcsc), ptr(dY), B, B, None, 0, ptr(out), B,
+          stream_ptr())
+torch.cuda.synchronize()
+print(f"B={B}: forward kernel on W^T (CSR) {t_fwdT:.1f} us, equal: {torch.equal(out, out2)}")
+
+# order / buffer swap check: the two launches alternate and swap outputs
+for rep in range(2):
+    a = timeit(lambda: _lib.call("smb_spmm_p", 0, patT.handle, ptr(vcsc), ptr(dY), B, B, None, 0,
+                                 ptr(out), B, stream_ptr()))
+    b = timeit(lambda: _lib.call("smb_spmm_t_csc", 0, pat.handle, ptr(vcsc), ptr(dY), B, B, None,
+                                 0, ptr(out2), B, stream_ptr()))
+    print(f"rep {rep}: forward kernel on W^T -> out {a:.1f} us, spmm_t_csc -> out2 {b:.1f} us")
+ri2 = pat.col_ptr_dev if hasattr(pat, "col_ptr_dev") else None
+print("pattern handle fields equal:",
+      bool(torch.equal(cp, cp)), "nnz", nnz)
