@@ -18,9 +18,13 @@
 // (LDGSTS) copies of the gathered x rows and of the few d_out rows the tile
 // touches; one barrier per chunk.  Every thread owns a fixed set of copy
 // slots (row base pointer + smem offset computed once), so a copy costs ~4
-// instructions.  Rows are padded to 16 + 16/sizeof(T) elements so each
-// thread's 16-byte LDS of its own x row and the (broadcast) LDS of its d_out
-// row are bank-conflict free.
+// instructions.  Staged rows are unpadded, 128-byte aligned lines whose
+// 16-byte vectors are XOR-swizzled (vector v of row r at slot v ^ (r & 7)), so
+// each thread's 16-byte LDS of its own x row is bank-conflict free.  (Rows
+// padded to 144 bytes were conflict free too, but a 128-byte copy into a line
+// straddling two 128-byte smem lines is split by the LSU: ncu counted 24 L2
+// sectors per 16-sector warp copy, 162 MB instead of 106 MB for the config-2
+// layer-0 SDDMM.)
 // (A TMA variant -- one cp.async.bulk per 128-byte row, producer warp +
 // mbarrier ring -- measured 4x slower on B200: 128-byte bulk copies are
 // request-rate bound at ~1.1 TB/s.  See DESIGN.md.)
@@ -30,13 +34,26 @@
 namespace smb {
 namespace {
 
+// element offset of 16-byte vector v of staged row r (rows of LDS elements,
+// vectors XOR-swizzled inside each aligned 8-vector group)
+template <int LDS, int VW>
+__device__ __forceinline__ int swz(int r, int v) {
+  return r * LDS + ((v ^ (r & 7)) * VW);
+}
+// first 128-byte boundary of the dynamic shared memory (the allocation adds
+// 128 bytes)
+__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
+  return p + ((128u - (smem_u32(p) & 127u)) & 127u);
+}
+
 // TILE nonzeros per CTA, CH batch columns per pipeline stage
 template <typename T, int TILE, int CH, int ST, int SD = 4>
 struct SddmmCfg {
   static constexpr int kChunk = CH;
   static constexpr int VW = 16 / sizeof(T);  // elements per 16 B
-  static constexpr int LDS = kChunk + VW;    // padded smem row (elements)
+  static constexpr int LDS = kChunk;         // smem row (elements), swizzled
   static constexpr int VPR = kChunk / VW;    // 16 B vectors per staged row
+  static_assert(VPR % 8 == 0, "swizzle spans 8 vectors");
   // staged d_out rows per tile: TILE/4 (rows of >= 4 nonzeros on average),
   // or TILE (SD = 1) for very sparse layers whose tiles span ~1 row per nonzero
   static constexpr int SLOTS = TILE / SD;
@@ -46,7 +63,8 @@ struct SddmmCfg {
   //   fp64 128-tile x 16 cols x 4 stages =  92 KB
   static constexpr int STAGES = ST;
   static constexpr size_t stage_elems = size_t(TILE + SLOTS) * LDS;
-  static constexpr size_t smem_bytes = STAGES * stage_elems * sizeof(T);
+  // + 128: the ring starts at the first 128-byte boundary of dynamic smem
+  static constexpr size_t smem_bytes = STAGES * stage_elems * sizeof(T) + 128;
   static_assert(TILE % VPR == 0, "tile / vector split");
 };
 
@@ -63,7 +81,7 @@ __global__ void __launch_bounds__(TILE)
   constexpr int S = C::STAGES, VW = C::VW, VPR = C::VPR, LDS = C::LDS;
   constexpr int kChunk = C::kChunk;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* smem = reinterpret_cast<T*>(smem_raw);
+  T* smem = reinterpret_cast<T*>(align128(smem_raw));
   __shared__ int32_t s_col[TILE];
   __shared__ int32_t s_rp[TILE + 1];
   const int tid = threadIdx.x;
@@ -98,7 +116,7 @@ __global__ void __launch_bounds__(TILE)
     const int r = tid / VPR + k * (TILE / VPR);
     xok[k] = r < n_active;
     xsrc[k] = x + (int64_t)s_col[r] * ld_x + v * VW;
-    xdst[k] = (unsigned)((r * LDS + v * VW) * sizeof(T));
+    xdst[k] = (unsigned)(swz<LDS, VW>(r, v) * sizeof(T));
   }
   // d_out rows of the tile: SLOTS*VPR copies, DC per thread; copy e = tid +
   // c*TILE stages vector v of slot row e/VPR (TILE % VPR == 0 keeps v fixed)
@@ -113,7 +131,7 @@ __global__ void __launch_bounds__(TILE)
     const int e = tid + c * TILE;
     dcopy[c] = e < n_staged * VPR;
     dsrc[c] = d_out + (int64_t)(r0 + (dcopy[c] ? e / VPR : 0)) * ld_d + v * VW;
-    ddst[c] = (unsigned)(((TILE + e / VPR) * LDS + v * VW) * sizeof(T));
+    ddst[c] = (unsigned)(swz<LDS, VW>(TILE + e / VPR, v) * sizeof(T));
   }
   const unsigned sbase = smem_u32(smem);
   constexpr unsigned kStageBytes = (unsigned)(C::stage_elems * sizeof(T));
@@ -170,15 +188,13 @@ __global__ void __launch_bounds__(TILE)
     else if (nx < n_chunks) issue_part(nx);
     cp_async_commit();
     const T* xs = smem + (ch % S) * C::stage_elems;
-    const T* xr = xs + tid * LDS;
-    const T* dr = xs + (TILE + rslot) * LDS;
     const int t0 = ch * kChunk;
 #pragma unroll
     for (int u = 0; u < VPR; ++u) {
-      const V xv = *reinterpret_cast<const V*>(xr + u * VW);
+      const V xv = *reinterpret_cast<const V*>(xs + swz<LDS, VW>(tid, u));
       V dv;
       if (ALL || rslot < C::SLOTS) {
-        dv = *reinterpret_cast<const V*>(dr + u * VW);
+        dv = *reinterpret_cast<const V*>(xs + swz<LDS, VW>(TILE + rslot, u));
       } else {
 #pragma unroll
         for (int j = 0; j < VW; ++j) VecOps<T>::set(dv, j, drow[t0 + u * VW + j]);
@@ -192,13 +208,12 @@ __global__ void __launch_bounds__(TILE)
     cp_async_wait<0>();
     __syncthreads();
     const T* xs = smem + (ch % S) * C::stage_elems;
-    const T* xr = xs + tid * LDS;
-    const T* dr = xs + (TILE + rslot) * LDS;
     const int t0 = ch * kChunk;
     const int cnt = n32 - t0;
     for (int j = 0; j < cnt; ++j) {
-      const T dv = (ALL || rslot < C::SLOTS) ? dr[j] : drow[t0 + j];
-      acc = add_rn(acc, mul_rn(dv, xr[j]));
+      const T dv = (ALL || rslot < C::SLOTS) ? xs[swz<LDS, VW>(TILE + rslot, j / VW) + j % VW]
+                                             : drow[t0 + j];
+      acc = add_rn(acc, mul_rn(dv, xs[swz<LDS, VW>(tid, j / VW) + j % VW]));
     }
   }
   cp_async_wait<0>();
@@ -226,10 +241,11 @@ constexpr int kWarpDSlots = 4;
 template <typename T, int CH, int S>
 struct SddmmWarpCfg {
   static constexpr int VW = 16 / sizeof(T);
-  static constexpr int LDS = CH + VW;  // padded row (conflict-free 16-byte reads)
+  static constexpr int LDS = CH;  // swizzled 128-byte-aligned rows (see sddmm_pipe_kernel)
   static constexpr int VPR = CH / VW;
+  static_assert(VPR % 8 == 0, "swizzle spans 8 vectors");
   static constexpr size_t warp_elems = size_t(S) * (32 + kWarpDSlots) * LDS;
-  static constexpr size_t smem_bytes = 4 * warp_elems * sizeof(T);  // 4 warps per CTA
+  static constexpr size_t smem_bytes = 4 * warp_elems * sizeof(T) + 128;  // 4 warps per CTA
 };
 
 template <typename T, int CH, int S>
@@ -246,7 +262,7 @@ __global__ void __launch_bounds__(128)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int32_t s_rp[kSddmmTile + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  T* wsm = reinterpret_cast<T*>(smem_raw) + warp * C::warp_elems;
+  T* wsm = reinterpret_cast<T*>(align128(smem_raw)) + warp * C::warp_elems;
   const int64_t p0 = (int64_t)blockIdx.x * kSddmmTile;
   const int64_t pw = p0 + warp * 32;             // first nonzero of this warp
   const int nw = (int)imax(0, imin(32, nnz - pw));  // nonzeros of this warp
@@ -276,12 +292,12 @@ __global__ void __launch_bounds__(128)
     const int32_t c = __shfl_sync(0xffffffffu, my_col, r);
     xok[k] = r < nw ? 16 : 0;
     xsrc[k] = x + (int64_t)c * ld_x + v * VW;
-    xdst[k] = (unsigned)((r * LDS + v * VW) * sizeof(T));
+    xdst[k] = (unsigned)(swz<LDS, VW>(r, v) * sizeof(T));
   }
   // d_out rows: vector e = lane (kWarpDSlots * VPR <= 32 for CH <= 32 fp32)
   const bool dcopy = staged && lane < span * VPR;
   const T* dsrc = d_out + (row_first + (dcopy ? lane / VPR : 0)) * ld_d + (lane % VPR) * VW;
-  const unsigned ddst = (unsigned)(((32 + lane / VPR) * LDS + (lane % VPR) * VW) * sizeof(T));
+  const unsigned ddst = (unsigned)(swz<LDS, VW>(32 + lane / VPR, lane % VPR) * sizeof(T));
   const unsigned sbase = smem_u32(wsm);
   pdl_wait();  // d_out / x are earlier kernels' outputs
   const bool upd = active && opt.kind != SMB_OPT_NONE;  // update operands loaded early
@@ -319,17 +335,15 @@ __global__ void __launch_bounds__(128)
     cp_async_commit();
     if (active) {
       const T* xs = wsm + (ch % S) * (kStageBytes / sizeof(T));
-      const T* xr = xs + lane * LDS;
-      const T* dr = xs + (32 + slot) * LDS;
       const int t0 = ch * CH;
       const int cnt = min(CH, n32 - t0);
       if (cnt == CH) {
 #pragma unroll
         for (int u = 0; u < VPR; ++u) {
-          const V xv = *reinterpret_cast<const V*>(xr + u * VW);
+          const V xv = *reinterpret_cast<const V*>(xs + swz<LDS, VW>(lane, u));
           V dv;
           if (staged) {
-            dv = *reinterpret_cast<const V*>(dr + u * VW);
+            dv = *reinterpret_cast<const V*>(xs + swz<LDS, VW>(32 + slot, u));
           } else {
 #pragma unroll
             for (int j = 0; j < VW; ++j) VecOps<T>::set(dv, j, drow[t0 + u * VW + j]);
@@ -340,8 +354,8 @@ __global__ void __launch_bounds__(128)
         }
       } else {
         for (int j = 0; j < cnt; ++j) {
-          const T dv = staged ? dr[j] : drow[t0 + j];
-          acc = add_rn(acc, mul_rn(dv, xr[j]));
+          const T dv = staged ? xs[swz<LDS, VW>(32 + slot, j / VW) + j % VW] : drow[t0 + j];
+          acc = add_rn(acc, mul_rn(dv, xs[swz<LDS, VW>(lane, j / VW) + j % VW]));
         }
       }
     }
@@ -364,6 +378,18 @@ __global__ void __launch_bounds__(128)
 template <typename T>
 int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* vbias, T* grad,
                      const OptConsts<T>& opt, cudaStream_t st);
+
+// ring shapes of the few-wave (config-2) tile kernels; compile-time knobs
+// for tuning sweeps (scripts/build_variant.sh)
+#ifndef SMB_SD_MID_STAGES
+#define SMB_SD_MID_STAGES 6
+#endif
+#ifndef SMB_SD_SMALL_STAGES
+#define SMB_SD_SMALL_STAGES 3
+#endif
+#ifndef SMB_SD_SMALL_CHUNK
+#define SMB_SD_SMALL_CHUNK 32
+#endif
 
 template <typename T>
 int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, const void* x,
@@ -467,7 +493,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       // flight; slower alone than 4 x 8 (15.9 vs 15.0 us) but the config-2
       // step runs 71.7 -> 70.9 us back to back (scripts/gpu_probe_us.sh sweep
       // over 3-7 stages x 4/8 rows)
-      SMB_GO_SD(32, 32, 6, 8);
+      SMB_GO_SD(32, 32, SMB_SD_MID_STAGES, 8);
     else if (sizeof(T) == 4 && small32 && all_for(32, 4) && concurrent)
       // beside other kernels (the overlapped training step) the 2-stage ring
       // (12 KB per CTA instead of 46 KB) leaves shared memory to the kernels
@@ -475,7 +501,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       // although this kernel alone is 1.1-1.2x slower
       // (3 stages with 4 staged d_out rows, 17 KB: 70.7 -> 70.2 us/step
       // against 2 stages x 8 rows; 2-4 stages x 4/8 rows measured)
-      SMB_GO_SD(32, 32, 3, 8);
+      SMB_GO_SD(32, SMB_SD_SMALL_CHUNK, SMB_SD_SMALL_STAGES, 8);
     else if (sizeof(T) == 4 && small32 && all_for(32, 4)) SMB_GO_SD(32, 32, 8, 4);
     else if (sizeof(T) == 4 && small32) SMB_GO_SD(32, 32, 8, 1);
     else if (sizeof(T) == 4 && small64 && !mid32 && all_for(64, 4)) SMB_GO_SD(64, 32, 4, 4);
@@ -484,7 +510,7 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     else if (sizeof(T) == 4 && wave) SMB_GO_SD(128, 64, 2, 4);
     else if (sizeof(T) == 4 && sparse_rows) SMB_GO_SD(128, 32, 2, 1);
     else if (sizeof(T) == 4) SMB_GO_SD(128, 32, 2, 4);
-    else SMB_GO_SD(128, 16, 4, 4);
+    else SMB_GO_SD(128, (int)(128 / sizeof(T)), 4, 4);  // fp64: 16-column chunks
 #undef SMB_GO_SD
     const int rc = check_launch(name);
     if (rc != SMB_OK) return rc;
