@@ -25,6 +25,21 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Staged rows of the cp.async rings: unpadded lines of LDS elements (a
+// multiple of 128 bytes) starting on 128-byte boundaries, 16-byte vector v of
+// row r at slot v ^ (r & 7).  Threads reading 16 bytes of their own rows are
+// then bank-conflict free, and a warp's 128-byte row copy lands in one smem
+// line (a padded 144-byte row straddles two, and the LSU splits the copy:
+// 1.5x the L2 sectors, measured with ncu).
+template <int LDS, int VW>
+__device__ __forceinline__ int swz(int r, int v) {
+  return r * LDS + ((v ^ (r & 7)) * VW);
+}
+// first 128-byte boundary of the dynamic shared memory (allocations add 128)
+__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
+  return p + ((128u - (smem_u32(p) & 127u)) & 127u);
+}
+
 // Copy `bytes` (<= 16) of a 16-byte vector; VEC: one cp.async with zero fill,
 // else element-wise (unaligned operands).
 template <typename T, bool VEC>

@@ -15,9 +15,9 @@
 //
 // Mapping: CTA = 64 columns c (one x row per thread) x one group of MR output
 // rows.  The batch is walked in 32-column chunks through a 4-stage cp.async
-// ring holding the CTA's 64 x rows (padded to 36 floats: each thread's
-// 16-byte read of its own row is bank-conflict free) and the group's d_out
-// rows (read as broadcasts); every thread runs MR independent chains, so the
+// ring holding the CTA's 64 x rows (swizzled 128-byte lines, async_copy.cuh:
+// each thread's 16-byte read of its own row is bank-conflict free) and the
+// group's d_out rows (read as broadcasts); every thread runs MR independent chains, so the
 // FADD latency is hidden inside the thread.  x is streamed from HBM once per
 // row group.
 #include <type_traits>
@@ -34,8 +34,9 @@ constexpr int kDgStages = 4;
 template <typename T>
 struct DgCfg {
   static constexpr int VW = 16 / sizeof(T);
-  static constexpr int LDS = kDgChunk + VW;  // padded row
+  static constexpr int LDS = kDgChunk;       // swizzled row (swz)
   static constexpr int VPR = kDgChunk / VW;  // 16-byte vectors per staged row
+  static_assert(VPR % 8 == 0, "swizzle spans 8 vectors");
 };
 
 template <typename T, int MR, bool VEC>
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(kDgCols)
   constexpr int ROWS = kDgCols + MR;  // staged rows per stage: x rows, then d rows
   constexpr unsigned kStage = (unsigned)(ROWS * LDS * sizeof(T));
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* sm = reinterpret_cast<T*>(align128(smem_raw));
   const int tid = threadIdx.x;
   const int row0 = blockIdx.x * MR;
   const int nr = (int)imin(MR, m - row0);
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(kDgCols)
     const int e = tid + kDgCols * q, r = e / VPR, v = e % VPR;
     xok[q] = c0 + r < k;
     xsrc[q] = x + (xok[q] ? c0 + r : 0) * ld_x + v * VW;
-    xdst[q] = (unsigned)((r * LDS + v * VW) * sizeof(T));
+    xdst[q] = (unsigned)(swz<LDS, VW>(r, v) * sizeof(T));
   }
   constexpr int DV = (MR * VPR + kDgCols - 1) / kDgCols;
   const T* dsrc[DV];
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kDgCols)
     const int e = tid + kDgCols * q, r = e / VPR, v = e % VPR;
     dok[q] = r < nr;
     dsrc[q] = d + (int64_t)(row0 + (dok[q] ? r : 0)) * ld_d + v * VW;
-    ddst[q] = (unsigned)(((kDgCols + r) * LDS + v * VW) * sizeof(T));
+    ddst[q] = (unsigned)(swz<LDS, VW>(kDgCols + r, v) * sizeof(T));
   }
   // update operands (independent of the previous kernel's output)
   T w_pre[MR], v_pre[MR];
@@ -122,16 +123,14 @@ __global__ void __launch_bounds__(kDgCols)
     if (ch + kDgStages - 1 < n_chunks) issue(ch + kDgStages - 1);
     cp_async_commit();
     const T* st = sm + (ch % kDgStages) * (kStage / sizeof(T));
-    const T* xr = st + tid * LDS;
-    const T* dr = st + kDgCols * LDS;
     const int cnt = min(kDgChunk, n32 - ch * kDgChunk);
     if (cnt == kDgChunk) {
 #pragma unroll
       for (int u = 0; u < VPR; ++u) {
-        const V xv = *reinterpret_cast<const V*>(xr + u * VW);
+        const V xv = *reinterpret_cast<const V*>(st + swz<LDS, VW>(tid, u));
 #pragma unroll
         for (int r = 0; r < MR; ++r) {
-          const V dv = *reinterpret_cast<const V*>(dr + r * LDS + u * VW);
+          const V dv = *reinterpret_cast<const V*>(st + swz<LDS, VW>(kDgCols + r, u));
 #pragma unroll
           for (int j = 0; j < VW; ++j)
             acc[r] = add_rn(acc[r], mul_rn(VecOps<T>::get(dv, j), VecOps<T>::get(xv, j)));
@@ -139,9 +138,10 @@ __global__ void __launch_bounds__(kDgCols)
       }
     } else {
       for (int j = 0; j < cnt; ++j) {
-        const T xv = xr[j];
+        const T xv = st[swz<LDS, VW>(tid, j / VW) + j % VW];
 #pragma unroll
-        for (int r = 0; r < MR; ++r) acc[r] = add_rn(acc[r], mul_rn(dr[r * LDS + j], xv));
+        for (int r = 0; r < MR; ++r)
+          acc[r] = add_rn(acc[r], mul_rn(st[swz<LDS, VW>(kDgCols + r, j / VW) + j % VW], xv));
       }
     }
   }
@@ -194,7 +194,7 @@ extern "C" int smb_dense_grad_update(int dtype, const void* d_out, int64_t ld_d,
     auto go = [&](auto mr_tag) {
       constexpr int MR = decltype(mr_tag)::value;
       const dim3 grid((unsigned)ceil_div(m, MR), (unsigned)cb);
-      const size_t smem = (size_t)kDgStages * (kDgCols + MR) * DgCfg<T>::LDS * sizeof(T);
+      const size_t smem = (size_t)kDgStages * (kDgCols + MR) * DgCfg<T>::LDS * sizeof(T) + 128;
       auto launch = [&](auto kernel) {
         ensure_smem(kernel, smem);
         launch_k(kernel, grid, dim3(kDgCols), smem, as_stream(stream),
@@ -205,6 +205,10 @@ extern "C" int smb_dense_grad_update(int dtype, const void* d_out, int64_t ld_d,
       if (vec) launch(dense_grad_kernel<T, MR, true>);
       else launch(dense_grad_kernel<T, MR, false>);
     };
+#ifdef SMB_DG_FORCE_MR  // tuning sweeps (scripts/build_variant.sh)
+    if (true) go(std::integral_constant<int, SMB_DG_FORCE_MR>{});
+    else
+#endif
     if (m == 10 && cb >= 296) go(std::integral_constant<int, 10>{});
     else if (cb * ceil_div(m, 16) >= 296) go(std::integral_constant<int, 16>{});
     else if (cb * ceil_div(m, 8) >= 296) go(std::integral_constant<int, 8>{});

@@ -34,18 +34,6 @@
 namespace smb {
 namespace {
 
-// element offset of 16-byte vector v of staged row r (rows of LDS elements,
-// vectors XOR-swizzled inside each aligned 8-vector group)
-template <int LDS, int VW>
-__device__ __forceinline__ int swz(int r, int v) {
-  return r * LDS + ((v ^ (r & 7)) * VW);
-}
-// first 128-byte boundary of the dynamic shared memory (the allocation adds
-// 128 bytes)
-__device__ __forceinline__ unsigned char* align128(unsigned char* p) {
-  return p + ((128u - (smem_u32(p) & 127u)) & 127u);
-}
-
 // TILE nonzeros per CTA, CH batch columns per pipeline stage
 template <typename T, int TILE, int CH, int ST, int SD = 4>
 struct SddmmCfg {
