@@ -40,6 +40,22 @@ __device__ __forceinline__ unsigned char* align128(unsigned char* p) {
   return p + ((128u - (smem_u32(p) & 127u)) & 127u);
 }
 
+// 16-byte shared-memory read as a volatile asm: a batch of these stays a
+// batch (ptxas otherwise sinks each read next to its first use to save
+// registers, exposing the LDS latency once per vector)
+__device__ __forceinline__ float4 lds16(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ double2 lds16(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+
 // Copy `bytes` (<= 16) of a 16-byte vector; VEC: one cp.async with zero fill,
 // else element-wise (unaligned operands).
 template <typename T, bool VEC>

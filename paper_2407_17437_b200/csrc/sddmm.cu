@@ -167,29 +167,82 @@ __global__ void __launch_bounds__(TILE)
   const int rslot = active ? slot : 0;
   const T* drow = d_out + (active ? row : r0) * ld_d;
   using V = typename Vec16<T>::type;
-  int ch = 0;
-  for (; ch < n_fast; ++ch) {
+  // smem offsets of this thread's x-row / d_out-row vectors w < 8 (the
+  // swizzle permutes the vectors inside each aligned group of 8)
+  int xo[8], dof[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    xo[w] = swz<LDS, VW>(tid, w);
+    dof[w] = swz<LDS, VW>(TILE + rslot, w);
+  }
+  // chunk ch landed for everyone (then stage (ch-1) % S is free: refill it)
+  auto landed = [&](int ch) {
     cp_async_wait<S - 2>();
-    __syncthreads();  // chunk ch landed for everyone; stage (ch-1)&(S-1) is free
+    __syncthreads();
     const int nx = ch + S - 1;
     if (nx < n_full) issue_full(nx);
     else if (nx < n_chunks) issue_part(nx);
     cp_async_commit();
+  };
+  // vectors g*8 .. g*8+7 of chunk ch: this thread's x row and d_out row
+  auto load8 = [&](int ch, int g, V* xv, V* dv) {
     const T* xs = smem + (ch % S) * C::stage_elems;
     const int t0 = ch * kChunk;
 #pragma unroll
-    for (int u = 0; u < VPR; ++u) {
-      const V xv = *reinterpret_cast<const V*>(xs + swz<LDS, VW>(tid, u));
-      V dv;
+    for (int w = 0; w < 8; ++w) {
+      xv[w] = lds16(xs + xo[w] + g * 8 * VW);
       if (ALL || rslot < C::SLOTS) {
-        dv = *reinterpret_cast<const V*>(xs + swz<LDS, VW>(TILE + rslot, u));
+        dv[w] = lds16(xs + dof[w] + g * 8 * VW);
       } else {
 #pragma unroll
-        for (int j = 0; j < VW; ++j) VecOps<T>::set(dv, j, drow[t0 + u * VW + j]);
+        for (int j = 0; j < VW; ++j) VecOps<T>::set(dv[w], j, drow[t0 + (g * 8 + w) * VW + j]);
       }
+    }
+  };
+  auto sum8 = [&](const V* xv, const V* dv) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w)
 #pragma unroll
       for (int j = 0; j < VW; ++j)
-        acc = add_rn(acc, mul_rn(VecOps<T>::get(dv, j), VecOps<T>::get(xv, j)));
+        acc = add_rn(acc, mul_rn(VecOps<T>::get(dv[w], j), VecOps<T>::get(xv[w], j)));
+  };
+  int ch = 0;
+  if constexpr (VPR == 8) {
+    // Chunk ch's shared-memory reads are issued before chunk ch-1's chain
+    // runs (two register sets, loop unrolled by two): ptxas otherwise sinks
+    // every read next to its first use and the chain stalls on the LDS
+    // latency once per vector.
+    V xa[8], da[8], xb[8], db[8];
+    if (n_fast > 0) {
+      landed(0);
+      load8(0, 0, xa, da);
+    }
+    for (ch = 1; ch + 1 < n_fast; ch += 2) {
+      landed(ch);
+      load8(ch, 0, xb, db);
+      sum8(xa, da);
+      landed(ch + 1);
+      load8(ch + 1, 0, xa, da);
+      sum8(xb, db);
+    }
+    if (ch < n_fast) {
+      landed(ch);
+      load8(ch, 0, xb, db);
+      sum8(xa, da);
+      sum8(xb, db);
+    } else if (n_fast > 0) {
+      sum8(xa, da);
+    }
+    ch = n_fast;
+  } else {
+    for (; ch < n_fast; ++ch) {
+      landed(ch);
+#pragma unroll
+      for (int g = 0; g < VPR / 8; ++g) {
+        V xv[8], dv[8];
+        load8(ch, g, xv, dv);
+        sum8(xv, dv);
+      }
     }
   }
   if (ch < n_chunks) {  // ragged last chunk (no further copies to issue)
@@ -370,10 +423,10 @@ int launch_bias_rows(const T* d, int64_t ld, int64_t m, int64_t n, T* bias, T* v
 // ring shapes of the few-wave (config-2) tile kernels; compile-time knobs
 // for tuning sweeps (scripts/build_variant.sh)
 #ifndef SMB_SD_MID_STAGES
-#define SMB_SD_MID_STAGES 6
+#define SMB_SD_MID_STAGES 8
 #endif
 #ifndef SMB_SD_SMALL_STAGES
-#define SMB_SD_SMALL_STAGES 3
+#define SMB_SD_SMALL_STAGES 4
 #endif
 #ifndef SMB_SD_SMALL_CHUNK
 #define SMB_SD_SMALL_CHUNK 32
@@ -477,18 +530,18 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
     }
     if (warp_done) {
     } else if (sizeof(T) == 4 && mid32)
-      // 6 stages, 4 staged d_out rows (31 KB, 7 CTAs per SM): 5 chunks in
-      // flight; slower alone than 4 x 8 (15.9 vs 15.0 us) but the config-2
-      // step runs 71.7 -> 70.9 us back to back (scripts/gpu_probe_us.sh sweep
-      // over 3-7 stages x 4/8 rows)
+      // 8 stages, 4 staged d_out rows (37 KB, 6 CTAs per SM: the layer's
+      // tiles stay one wave): config-2 step 68.3 -> 66.6 us back to back
+      // against 6 stages; 3-5 and 10-16 stages slower (10+ stages: two waves)
+      // (scripts/sweep_variants.sh)
       SMB_GO_SD(32, 32, SMB_SD_MID_STAGES, 8);
     else if (sizeof(T) == 4 && small32 && all_for(32, 4) && concurrent)
       // beside other kernels (the overlapped training step) the 2-stage ring
       // (12 KB per CTA instead of 46 KB) leaves shared memory to the kernels
       // on the critical path: config-2 step 76.3 -> 74.6 us back to back
       // although this kernel alone is 1.1-1.2x slower
-      // (3 stages with 4 staged d_out rows, 17 KB: 70.7 -> 70.2 us/step
-      // against 2 stages x 8 rows; 2-4 stages x 4/8 rows measured)
+      // (4 stages with 4 staged d_out rows, 18 KB: 66.6 -> 65.9 us/step
+      // against 3 stages; 2-8 stages and 64-column chunks measured)
       SMB_GO_SD(32, SMB_SD_SMALL_CHUNK, SMB_SD_SMALL_STAGES, 8);
     else if (sizeof(T) == 4 && small32 && all_for(32, 4)) SMB_GO_SD(32, 32, 8, 4);
     else if (sizeof(T) == 4 && small32) SMB_GO_SD(32, 32, 8, 1);
