@@ -363,6 +363,45 @@ SMB_API int smb_sample_pattern(int64_t m, int64_t k, int64_t nnz, uint64_t seed,
 /* The sampler's 64-bit Philox draw i (host-callable, for checking). */
 SMB_API uint64_t smb_philox_u64(uint64_t seed, uint64_t stream_id, uint64_t i);
 
+/* Column-chain step (B200 addition, no single reference counterpart): the
+ * batch-column-parallel middle of one training step in one cluster launch --
+ * the forward products of layers 1..L-1 with bias / ReLU (nn.py:169-176,
+ * 86-87), the softmax cross-entropy gradient and loss (nn.py:385-417,
+ * train.py:399), and the input gradients d_{l-1} = (W_l^T d_l) * (a_{l-1} > 0)
+ * for l = L-1..1 (nn.py:178-185, 89-91; train.py:216-220) -- with the same
+ * arithmetic, bit for bit, as smb_spmm_p / smb_softmax_ce_step /
+ * smb_spmm_t_csc.  Layer 0's forward product and all weight-side work
+ * (SDDMM, updates, bias row sums) stay separate launches.
+ *
+ * smb_chain_plan_create: setup-time (synchronises the device); patterns[l]
+ * of the L sparse layers (W_0 first), relu[l] = activation after layer l
+ * (relu[L-1] must be 0), batch width n, leading dimension ld (multiple of 4).
+ * Returns SMB_ERR_INVALID with a "chain: unsupported" message when the model
+ * does not fit the kernel (more than 16 classes, operands over shared
+ * memory, ...); the caller then runs the separate kernels.
+ * smb_chain_plan_info: info4 = {CTAs per cluster, column groups, shared
+ * memory bytes, layers}.
+ * smb_chain_run: host arrays of L device pointers each (index = layer;
+ * values / values_csc / bias of layer 0 are not read): values (CSR order),
+ * values_csc (CSC order, smb_values_to_csc), bias, acts[l] = a_l [m_l x ld]
+ * (acts[0] is read, acts[1..] written), dys[l] = d_l (written); t the
+ * one-hot targets [classes x ld_t]; loss_out (device float64, may be NULL)
+ * needs workspace (smb_chain_workspace_bytes(n) bytes, zeroed once). */
+typedef struct smb_chain_plan smb_chain_plan;
+SMB_API int smb_chain_plan_create(int nlayers, const smb_pattern* const* patterns,
+                                  const int* relu, int64_t n, int64_t ld, smb_chain_plan** out);
+SMB_API int smb_chain_plan_destroy(smb_chain_plan* plan);
+SMB_API int smb_chain_plan_info(const smb_chain_plan* plan, int64_t* info4);
+/* Diagnostics: later runs of the plan record %globaltimer stamps of their
+ * phases (thread 0 of every CTA, 32 slots per CTA) into `stamps` (device,
+ * uint64[CTAs x 32]); NULL turns it off. */
+SMB_API int smb_chain_plan_profile(smb_chain_plan* plan, void* stamps);
+SMB_API size_t smb_chain_workspace_bytes(int64_t n);
+SMB_API int smb_chain_run(const smb_chain_plan* plan, const void* const* values,
+                          const void* const* values_csc, const void* const* bias,
+                          void* const* acts, void* const* dys, const void* t, int64_t ld_t,
+                          double divisor, double* loss_out, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,12 @@ SIGNATURES = {
     "smb_xavier_pcg64": (_i32, [_i32, _u64, _u64, _u64, _u64, _u64, _i64, _f64, _p, _p]),
     "smb_sample_pattern": (_i32, [_i64, _i64, _i64, _u64, _u64, _p, _p, _p]),
     "smb_philox_u64": (_u64, [_u64, _u64, _u64]),
+    "smb_chain_plan_create": (_i32, [_i32, _p, _p, _i64, _i64, C.POINTER(_p)]),
+    "smb_chain_plan_destroy": (_i32, [_p]),
+    "smb_chain_plan_info": (_i32, [_p, _p]),
+    "smb_chain_plan_profile": (_i32, [_p, _p]),
+    "smb_chain_workspace_bytes": (C.c_size_t, [_i64]),
+    "smb_chain_run": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _f64, _p, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -35,6 +35,7 @@
 #include <cuda.h>
 
 #include "pattern.cuh"
+#include "tma.cuh"
 
 namespace smb {
 namespace {
@@ -239,26 +240,6 @@ __global__ void __launch_bounds__(32 * WPC)
   }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no
-// link-time dependency on libcuda)
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return reinterpret_cast<EncodeTiledFn>(f);
-  }();
-  return fn;
-}
-
 // rows x cols fp32 row-major with leading dimension ld; box = 1 row x 32 cols
 bool make_row_map(CUtensorMap* map, const float* ptr, int64_t rows, int64_t cols, int64_t ld) {
   EncodeTiledFn enc = encode_fn();
@@ -274,6 +255,21 @@ bool make_row_map(CUtensorMap* map, const float* ptr, int64_t rows, int64_t cols
 }
 
 }  // namespace
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda)
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
 
 bool sddmm_use_blocked_order(const smb_pattern* pat, int64_t n) {
   // x + d_out at least 4x the 126 MB L2 (at 2x -- config 5, B = 512 -- the

@@ -170,6 +170,19 @@ def flat_layout(units):
     return layout, off
 
 
+class _ChainPlan:
+    """Owns an smb_chain_plan handle."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            _lib.load().smb_chain_plan_destroy(self.h)
+        except Exception:
+            pass
+
+
 class _Unit:
     __slots__ = ("layer", "relu", "sparse", "m", "k", "grad_off", "bias_off", "nvals", "index",
                  "vals", "vals_csc", "seen")
@@ -187,7 +200,7 @@ class _Unit:
 class FusedTrainStep:
     def __init__(self, model, batch_size: int, global_batch: int | None = None,
                  process_group=None, use_graph: bool = True, force_dp: bool = False,
-                 bucketed: bool | None = None):
+                 bucketed: bool | None = None, chain: bool = True):
         self.units = self._parse(model)
         self.model = model
         self.B = int(batch_size)
@@ -298,7 +311,50 @@ class FusedTrainStep:
                 # update on the same stream
                 c = torch.empty_like(u.layer.weights.values)
                 u.vals_csc = [c, c]
+        # column-chain kernel (csrc/chain.cu): layers 1..L-1 forward, the
+        # softmax step and the input-gradient chain in one cluster launch,
+        # when the model fits it (all layers sparse, ReLU between them, at
+        # most 16 classes, operands within shared memory)
+        self._chain = None
+        self._chain_ws = None
+        if chain and self.overlap and not self.dp:
+            self._chain = self._make_chain_plan()
         self.sync_weights()
+
+    def _make_chain_plan(self):
+        import ctypes as C
+
+        us = self.units
+        if len(us) < 2 or not all(u.sparse for u in us):
+            return None
+        if not all(u.relu for u in us[:-1]) or us[-1].relu:
+            return None
+        if any(u.vals_csc is None for u in us[1:]):
+            return None
+        lib = _lib.load()
+        L = len(us)
+        pats = (C.c_void_p * L)(*[u.layer.weights.pattern.handle for u in us])
+        relu = (C.c_int * L)(*[int(u.relu) for u in us])
+        out = C.c_void_p()
+        rc = lib.smb_chain_plan_create(L, pats, relu, self.B, self.ld, C.byref(out))
+        if rc != _lib.SMB_OK:
+            msg = lib.smb_last_error().decode(errors="replace")
+            if rc == _lib.SMB_ERR_INVALID and "unsupported" in msg:
+                return None  # the separate kernels run this model
+            _lib.check(rc, "smb_chain_plan_create")
+        self._chain_ws = torch.zeros(int(lib.smb_chain_workspace_bytes(self.B)), dtype=torch.uint8,
+                                     device=self.dev)
+        return _ChainPlan(out.value)
+
+    def chain_info(self):
+        """{cluster, groups, smem, layers} of the column-chain plan, or None."""
+        if self._chain is None:
+            return None
+        import ctypes as C
+
+        info = (C.c_int64 * 4)()
+        _lib.call("smb_chain_plan_info", self._chain.h, info)
+        return dict(zip(("cluster", "groups", "smem", "layers"), list(info)))
 
     def sync_weights(self) -> None:
         """Re-derive the CSC-ordered value copies from the layers' current
@@ -522,6 +578,13 @@ class FusedTrainStep:
             with torch.cuda.stream(fork("prefetch")) if overlap else _nullctx():
                 self._gather_into(1 - self._slot, stream_ptr(), ahead=True)
 
+        if self._chain is not None and fuse_update and overlap:
+            self._launch_chain_step(eta, x_in, t_in, fork, main)
+            if gather:
+                prefetch()
+            for s_ in forked:
+                main.wait_stream(s_)
+            return
         # forward: a_l = act(W_l a_{l-1} + b_l)
         x = x_in
         for li, (u, a) in enumerate(zip(self.units, self.acts)):
@@ -640,6 +703,40 @@ class FusedTrainStep:
             prefetch()
         for s_ in forked:
             main.wait_stream(s_)  # join: the step ends when every update has
+
+    def _launch_chain_step(self, eta, x_in, t_in, fork, main) -> None:
+        """Single-GPU step through the column-chain kernel: layer 0's forward
+        SpMM, then ONE cluster launch for layers 1..L-1 forward, the softmax
+        step and every input gradient (csrc/chain.cu), then every layer's
+        weight side (bias row sums + update, SDDMM + update) concurrently on
+        the layers' side streams, the first layer's (the longest SDDMM) first."""
+        import ctypes as C
+
+        st = stream_ptr()
+        B, ld, F32 = self.B, self.ld, _lib.SMB_F32
+        us = self.units
+        L = len(us)
+        u0 = us[0]
+        self._call("spmm[0]", "smb_spmm_p", F32, u0.layer.weights.pattern.handle,
+                   ptr(self._vals(u0)), ptr(x_in), ld, B, ptr(u0.layer.bias),
+                   _lib.SMB_EPI_RELU if u0.relu else _lib.SMB_EPI_NONE, ptr(self.acts[0]), ld, st)
+        arr = C.c_void_p * L
+        vals = arr(*[ptr(self._vals(u)) for u in us])
+        vcsc = arr(*[ptr(u.vals_csc[self._parity]) if u.vals_csc is not None else None
+                     for u in us])
+        bias = arr(*[ptr(u.layer.bias) for u in us])
+        acts = arr(*[ptr(a) for a in self.acts])
+        dys = arr(*[ptr(d) for d in self.dys])
+        self._call("chain", "smb_chain_run", self._chain.h, vals, vcsc, bias, acts, dys,
+                   ptr(t_in), ld, float(self.B_global), ptr(self.loss), ptr(self._chain_ws), st)
+        for li in [0] + list(range(L - 1, 0, -1)):
+            u = us[li]
+            x_prev = self.acts[li - 1] if li > 0 else x_in
+            b, vb, gb, kind, mu = self._bias_target(u, True)
+            with torch.cuda.stream(fork(("weights", li))):
+                self._weight_side(u, self.dys[li], x_prev, eta, True, stream_ptr())
+                self._call(f"bias[{li}]", "smb_bias_grad_update", F32, ptr(self.dys[li]), ld,
+                           u.m, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
 
     def _side_stream(self, key):
         s_ = self._sides.get(key)

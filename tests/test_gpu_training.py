@@ -37,14 +37,15 @@ def max_rel(model, ref):
     return max(rel_err(a, b) for (_, a), (_, b) in zip(params_host(model), oracle_params(ref)))
 
 
-def test_kernel_durations_time_every_sparse_launch():
+@pytest.mark.parametrize("use_chain", [True, False])
+def test_kernel_durations_time_every_sparse_launch(use_chain):
     """bench.py's per-kernel durations (KernelTimer.kernel_durations): one
     entry per C-ABI launch of the step, each a positive graph-timed duration."""
     chain, B = [3072, 1024, 512, 10], 256
     data = smb.synthetic_dataset(seed=2, n_samples=B * 4, features=chain[0])
     model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=chain, density=0.01, seed=4,
                                                     batch_size=B))
-    st = smb.FusedTrainStep(model, B)
+    st = smb.FusedTrainStep(model, B, chain=use_chain)
     st.attach_dataset(smb.DeviceDataset(data))
     st.set_epoch(np.arange(B * 4))
     for _ in range(2):
@@ -56,8 +57,9 @@ def test_kernel_durations_time_every_sparse_launch():
     # the timing pass replays in-place updates; it must leave the model as it was
     for (n1, a), (n2, b) in zip(before, params_host(model)):
         assert n1 == n2 and bits_equal(a, b), n1
-    for tag in ("spmm[0]", "spmm[1]", "spmm[2]", "softmax_ce", "spmm_t[2]", "spmm_t[1]",
-                "sddmm_update[0]", "sddmm_update[1]", "sddmm_update[2]"):
+    middle = (("chain",) if use_chain else
+              ("spmm[1]", "spmm[2]", "softmax_ce", "spmm_t[2]", "spmm_t[1]"))
+    for tag in ("spmm[0]",) + middle + ("sddmm_update[0]", "sddmm_update[1]", "sddmm_update[2]"):
         cnt, ms = out[tag]
         assert cnt == 8 and 0.0 < ms / cnt < 5.0, (tag, cnt, ms)
     assert st.timer is None and st.use_graph and st.overlap  # restored
