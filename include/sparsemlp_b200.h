@@ -376,17 +376,21 @@ SMB_API uint64_t smb_philox_u64(uint64_t seed, uint64_t stream_id, uint64_t i);
  * smb_chain_plan_create: setup-time (synchronises the device); patterns[l]
  * of the L sparse layers (W_0 first), relu[l] = activation after layer l
  * (relu[L-1] must be 0), batch width n, leading dimension ld (multiple of 4).
- * Returns SMB_ERR_INVALID with a "chain: unsupported" message when the model
- * does not fit the kernel (more than 16 classes, operands over shared
- * memory, ...); the caller then runs the separate kernels.
+ * The plan owns quad-padded copies of layers 1..L-1 (CSR and CSC order; a
+ * pad is an exact no-op: value -0.0 times a zero operand row).  Returns
+ * SMB_ERR_INVALID with a "chain: unsupported" message when the model does not
+ * fit the kernel (more than 16 classes, operands over shared memory, ...);
+ * the caller then runs the separate kernels.
+ * smb_chain_refresh: re-derive the plan's padded value copies of layer
+ * `layer` (1..L-1) from its values (CSR order); call after every change of
+ * the values, stream-ordered before the next smb_chain_run.
  * smb_chain_plan_info: info4 = {CTAs per cluster, column groups, shared
  * memory bytes, layers}.
  * smb_chain_run: host arrays of L device pointers each (index = layer;
- * values / values_csc / bias of layer 0 are not read): values (CSR order),
- * values_csc (CSC order, smb_values_to_csc), bias, acts[l] = a_l [m_l x ld]
- * (acts[0] is read, acts[1..] written), dys[l] = d_l (written); t the
- * one-hot targets [classes x ld_t]; loss_out (device float64, may be NULL)
- * needs workspace (smb_chain_workspace_bytes(n) bytes, zeroed once). */
+ * entry 0 of bias is not read): bias, acts[l] = a_l [m_l x ld] (acts[0] is
+ * read, acts[1..] written), dys[l] = d_l (written); t the one-hot targets
+ * [classes x ld_t]; loss_out (device float64, may be NULL) needs workspace
+ * (smb_chain_workspace_bytes(n) bytes, zeroed once). */
 typedef struct smb_chain_plan smb_chain_plan;
 SMB_API int smb_chain_plan_create(int nlayers, const smb_pattern* const* patterns,
                                   const int* relu, int64_t n, int64_t ld, smb_chain_plan** out);
@@ -396,11 +400,12 @@ SMB_API int smb_chain_plan_info(const smb_chain_plan* plan, int64_t* info4);
  * phases (thread 0 of every CTA, 32 slots per CTA) into `stamps` (device,
  * uint64[CTAs x 32]); NULL turns it off. */
 SMB_API int smb_chain_plan_profile(smb_chain_plan* plan, void* stamps);
+SMB_API int smb_chain_refresh(const smb_chain_plan* plan, int layer, const void* values,
+                              void* stream);
 SMB_API size_t smb_chain_workspace_bytes(int64_t n);
-SMB_API int smb_chain_run(const smb_chain_plan* plan, const void* const* values,
-                          const void* const* values_csc, const void* const* bias,
-                          void* const* acts, void* const* dys, const void* t, int64_t ld_t,
-                          double divisor, double* loss_out, void* workspace, void* stream);
+SMB_API int smb_chain_run(const smb_chain_plan* plan, const void* const* bias, void* const* acts,
+                          void* const* dys, const void* t, int64_t ld_t, double divisor,
+                          double* loss_out, void* workspace, void* stream);
 
 #ifdef __cplusplus
 }

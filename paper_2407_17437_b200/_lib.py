@@ -95,7 +95,8 @@ SIGNATURES = {
     "smb_chain_plan_info": (_i32, [_p, _p]),
     "smb_chain_plan_profile": (_i32, [_p, _p]),
     "smb_chain_workspace_bytes": (C.c_size_t, [_i64]),
-    "smb_chain_run": (_i32, [_p, _p, _p, _p, _p, _p, _p, _i64, _f64, _p, _p, _p]),
+    "smb_chain_refresh": (_i32, [_p, _i32, _p, _p]),
+    "smb_chain_run": (_i32, [_p, _p, _p, _p, _p, _i64, _f64, _p, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -11,20 +11,32 @@
 // (layer indices 0-based as in engine.py: W_0 is the first layer).  Each of
 // these was its own latency-bound launch (config 2: two SpMMs, the output
 // layer, the softmax step and two transposed SpMMs, ~28 us of kernels for
-// 36 K nonzeros).  Here a thread-block cluster owns 32 batch columns
-// (lane = column) and its C CTAs split the output rows of every product; the
+// 36 K nonzeros).  Here a thread-block cluster owns 32 batch columns and its C
+// CTAs split the output rows of every product (balanced by nonzeros).  The
 // dense operand of a product (all rows of a_{l-1} or d_l for the cluster's 32
-// columns) is staged in shared memory by TMA as [rows][32] fp32, 128 bytes per
-// row, so lane c reading element (r, c) is conflict-free for any r.  Between
-// products the CTAs write their rows to global memory (the step needs every
-// activation and gradient there anyway: masks, SDDMMs, bias row sums), meet at
-// a cluster barrier (release/acquire), and re-load the full operand with one
-// 2-D tensor copy per 256 rows.  The index/value segments of each CTA's rows
-// (CSR for the forward products, CSC for the transposed ones) are staged once
-// at launch with cp.async, before the programmatic-dependency wait, so they
-// overlap the previous kernel's tail; the inner loop reads 4 (index, value)
-// pairs with two broadcast 16-byte shared loads and gathers 4 operand
-// elements.
+// columns) is staged in shared memory by TMA as [rows][32] fp32, 128 bytes
+// per row, plus one all-zero row.  Between products the CTAs write their rows
+// to global memory (the step needs every activation and gradient there
+// anyway: masks, SDDMMs, bias row sums), meet at a cluster barrier
+// (release/acquire), and re-load the full operand with 2-D tensor copies; the
+// output layer's logits go to every CTA of the cluster through distributed
+// shared memory.
+//
+// Segments are PADDED to whole quads of 4 (index, value) pairs: a pad points
+// at the operand's zero row with value -0.0, so its product is -0.0 and
+// acc + (-0.0) == acc bit for bit for every acc (including -0.0 and NaN): the
+// inner loop has no masks, no head or tail.  The padded index arrays are
+// built once per plan; the padded value copies are refreshed from the
+// layer's values after every update (smb_chain_refresh, the counterpart of
+// smb_values_to_csc).  Each CTA's padded segments are staged with 1-D bulk
+// copies before the programmatic-dependency wait.
+//
+// Mapping: a warp runs up to 4 rows at a time, one per 8-lane group; lane l8
+// of a group owns columns 4 l8 .. 4 l8 + 3, so a group reads one 128-byte
+// operand row per element (16-byte loads, conflict-free); rows are taken
+// longest first so a warp's rows end together.  Layers with long rows (the
+// output layer: ~300 nonzeros per row at config 2) run one row per warp with
+// one column per lane instead.
 //
 // Arithmetic is exactly the separate kernels' (and the reference's): each
 // output element sums its segment in ascending source index from 0 with
@@ -36,8 +48,8 @@
 #include "pattern.cuh"
 #include "tma.cuh"
 
-#include <climits>
 #include <algorithm>
+#include <climits>
 #include <cstring>
 #include <vector>
 
@@ -47,31 +59,31 @@ namespace {
 constexpr int kChainMaxL = 6;
 constexpr int kChainWarps = 16;
 constexpr int kChainThreads = 32 * kChainWarps;
-constexpr int kBoxRows = 256;
 constexpr int kChainMaxClasses = 16;
 constexpr int kChainMaxC = 8;
 
 // one staged sparse product (a forward layer or a transposed one)
 struct ChainPhase {
-  const int32_t* ptr;  // segment pointers (row_ptr / col_ptr), [rows + 1]
-  const int32_t* idx;  // col_idx / row_idx
-  const float* val;    // CSR values / CSC-ordered values
-  const float* bias;   // forward: per-row bias, or null
-  float* out;          // [rows x ld]
-  int rows;            // output rows
-  int nnz;
-  int split[kChainMaxC + 1];  // the cluster's CTAs' row ranges (balanced by nonzeros)
-  int act;             // forward: np.maximum(., 0); backward: ReLU mask of the layer below
-  int meta_off;        // shared-memory byte offset of the staged segment
-  int ptr_words;       // staged pointer words (multiple of 4)
-  int nz_words;        // staged index words = value words (multiple of 4)
-  int epi_off;         // forward: staged bias slice; backward: mask bits (byte offset)
+  const int32_t* ptr;    // padded segment pointers [rows + 1] (multiples of 4)
+  const int32_t* idx;    // padded operand rows (pads: zero_row)
+  const float* val;      // padded values (pads: -0.0)
   const int32_t* order;  // [rows]: each CTA's rows, longest segment first
-  int order_off;       // shared-memory byte offset of the staged order slice
-  int in_map;          // tensor map that reloads the operand into region A, -1: none
-  int in_boxes;        // 256-row boxes of that reload
+  const float* bias;     // forward: per-row bias, or null
+  float* out;            // [rows x ld]
+  int rows;              // output rows
+  int nnzp;              // padded segment total
+  int split[kChainMaxC + 1];  // the cluster's CTAs' row ranges (balanced by nonzeros)
+  int act;               // forward: np.maximum(., 0); backward: ReLU mask of the layer below
+  int zero_row;          // the operand's all-zero row
+  int meta_off;          // shared-memory byte offset of the staged segment
+  int ptr_words;         // staged pointer words (multiple of 4)
+  int nz_words;          // staged index words = value words (multiple of 4; + the no-op quad)
+  int epi_off;           // forward: staged bias slice; backward: mask bits (byte offset)
+  int order_off;         // staged order slice (byte offset)
+  int in_map;            // tensor map that reloads the operand into region A, -1: region D
+  int in_boxes;          // boxes of that reload
   int in_box_rows;
-  int wide;            // long rows: one row per warp, one column per lane
+  int wide;              // long rows: one row per warp, one column per lane
 };
 
 struct ChainParams {
@@ -128,17 +140,25 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ int lds_s32(const int32_t* p) {
-  int v;
-  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
-  return v;
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c, int r,
+                                            unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c), "r"(r), "r"(bar)
+      : "memory");
 }
-__device__ __forceinline__ float lds_f32(const float* p) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
-  return v;
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
+                                         unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
 }
-__device__ __forceinline__ float lds_f32x1(unsigned a) {
+// volatile shared loads: a batch of them stays a batch (ptxas otherwise sinks
+// each load next to its first use)
+__device__ __forceinline__ float lds_f32(unsigned a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
   return v;
@@ -150,255 +170,174 @@ __device__ __forceinline__ float4 lds_f32x4(unsigned a) {
                : "r"(a));
   return v;
 }
-__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c, int r,
-                                            unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(map), "r"(c), "r"(r), "r"(bar)
-      : "memory");
+__device__ __forceinline__ int4 lds_s32x4(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
 }
 
 enum ChainKind { kFwd = 0, kFwdLast = 1, kBwd = 2 };
 
-// What one warp needs to run its rows of one product.
+// What one warp needs to run its rows of one product (shared addresses).
 struct RowTask {
-  const int32_t* sp;  // staged pointers; row r at sp[r - pr0]
+  const int32_t* sp;     // staged padded pointers; row r at sp[r - pr0]
   int pr0;
-  int a0;             // staged nonzero s at si[s - a0] / sv[s - a0]
-  const int32_t* si;
-  const float* sv;
+  int a0;                // staged padded slot s at local index s - a0
+  unsigned si, sv;       // staged indices / values
+  int dummy;             // local index of the no-op quad
   const int32_t* order;  // the CTA's rows, longest segment first
   int nrows;
-  const float* X;     // operand [rows][32]
-  const float* sbias;  // forward: staged bias, row r at sbias[r - pr0]
+  unsigned X;            // operand [rows][32] (+ zero row)
+  const float* sbias;    // forward: staged bias, row r at sbias[r - pr0]
   const unsigned* mbits;  // backward: ReLU mask bits, row r at mbits[r - r0]
   int r0;
   int act;
   float* out;
   int64_t ld;
-  int n;              // batch width (valid columns)
-  int c0;             // first column of the cluster's group
-  unsigned lg;        // forward-last: shared address of the logits block
+  int n;                 // batch width (valid columns)
+  int c0;                // first column of the cluster's group
+  unsigned lg;           // forward-last: shared address of the logits block
   unsigned C;
-  unsigned long long* dbg;
 };
 
-// The CTA's rows of one product.  A warp runs up to 4 rows at a time, one
-// per 8-lane group; lane l8 of a group owns columns 4*l8 .. 4*l8+3 (16-byte
-// operand reads: the 8 lanes of a group read one 128-byte operand row, the
-// 4 groups 4 rows -- conflict-free).  Rows are taken longest first, so the
-// rows a warp runs together have about the same length.  Each element sums its
-// segment in ascending s from 0, multiply and add rounded separately; then
-// the epilogue (bias + ReLU, or the ReLU mask of the layer below) and one
-// 16-byte store per lane.
-template <int K>
-__device__ __forceinline__ void run_rows(const RowTask& w, int warp, int lane) {
-  const int g = lane >> 3, l8 = lane & 7;
-  const int cq = 4 * l8;  // first of this lane's 4 columns in the group
-  const float* Xl = w.X + cq;
-  int dk = 0;
-  auto dstamp = [&]() {
-    if (w.dbg != nullptr && lane == 0 && warp == 0 && dk < 12) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      w.dbg[dk] = t;
+template <int K, int W>
+__device__ __forceinline__ void epilogue(const RowTask& w, int r, int cq, float (&acc)[W]) {
+  if constexpr (K == kBwd) {
+    if (w.act) {
+      const unsigned bits = w.mbits[r - w.r0] >> cq;
+#pragma unroll
+      for (int u = 0; u < W; ++u) acc[u] = mul_rn(acc[u], ((bits >> u) & 1u) ? 1.f : 0.f);
     }
-    ++dk;
-  };
-  dstamp();
-  // slot (sorted row) warp + 16 g + 64 t: a CTA with at most 16 rows gives
-  // every warp its own row
-  for (int base = warp; base < w.nrows; base += 4 * kChainWarps) {
-    const int slot = base + kChainWarps * g;
-    const bool has = slot < w.nrows;
-    const int r = has ? w.order[slot] : -1;
-    int s = 0, e = 0;
-    if (has) {
-      s = w.sp[r - w.pr0] - w.a0;
-      e = w.sp[r + 1 - w.pr0] - w.a0;
+  } else {
+    if (w.sbias != nullptr) {
+      const float b = w.sbias[r - w.pr0];
+#pragma unroll
+      for (int u = 0; u < W; ++u) acc[u] = add_rn(acc[u], b);
     }
-    const int trip = __reduce_max_sync(0xffffffffu, e - s);
-    dstamp();
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    // software pipeline over rounds of 4 elements: the indices / values of
-    // round i+2 and the operands of round i+1 are in flight while round i is
-    // summed (volatile shared loads keep each batch together)
-    const int32_t* ci = w.si - w.a0;
-    const float* cv = w.sv - w.a0;
-    const unsigned xb = smem_u32(Xl);
-    const int eg = e + w.a0;  // global index of the row end
-    auto meta = [&](int jb, int (&c)[4], float (&v)[4]) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool p = jb + u < eg;
-        const int jj = p ? jb + u : w.a0;  // (staged word 0 when past the end)
-        c[u] = lds_s32(ci + jj);
-        v[u] = lds_f32(cv + jj);
-      }
-    };
-    auto operands = [&](int jb, const int (&c)[4], float4 (&x)[4]) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int cc = jb + u < eg ? c[u] : 0;  // row 0: in range whatever was read
-        x[u] = lds_f32x4(xb + (unsigned)cc * 128u);
-      }
-    };
-    int c0[4], c1[4];
-    float v0[4], v1[4];
-    float4 x0[4];
-    const int jg = s + w.a0;  // global nonzero index of the row start
-    meta(jg, c0, v0);
-    meta(jg + 4, c1, v1);
-    operands(jg, c0, x0);
-    for (int i = 0; i < trip; i += 4) {
-      const int j = jg + i;
-      float4 x1[4];
-      operands(j + 4, c1, x1);
-      int c2[4];
-      float v2[4];
-      meta(j + 8, c2, v2);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (j + u < eg) {
-          acc.x = add_rn(acc.x, mul_rn(v0[u], x0[u].x));
-          acc.y = add_rn(acc.y, mul_rn(v0[u], x0[u].y));
-          acc.z = add_rn(acc.z, mul_rn(v0[u], x0[u].z));
-          acc.w = add_rn(acc.w, mul_rn(v0[u], x0[u].w));
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        v0[u] = v1[u];
-        x0[u] = x1[u];
-        c1[u] = c2[u];
-        v1[u] = v2[u];
-      }
-    }
-    dstamp();
-    if (!has) continue;
-    if constexpr (K == kBwd) {
+    if constexpr (K == kFwd) {
       if (w.act) {
-        const unsigned bits = w.mbits[r - w.r0] >> cq;
-        acc.x = mul_rn(acc.x, (bits & 1u) ? 1.f : 0.f);
-        acc.y = mul_rn(acc.y, (bits & 2u) ? 1.f : 0.f);
-        acc.z = mul_rn(acc.z, (bits & 4u) ? 1.f : 0.f);
-        acc.w = mul_rn(acc.w, (bits & 8u) ? 1.f : 0.f);
-      }
-    } else {
-      if (w.sbias != nullptr) {
-        const float b = w.sbias[r - w.pr0];
-        acc.x = add_rn(acc.x, b);
-        acc.y = add_rn(acc.y, b);
-        acc.z = add_rn(acc.z, b);
-        acc.w = add_rn(acc.w, b);
-      }
-      if constexpr (K == kFwd) {
-        if (w.act) {
-          acc.x = relu_np(acc.x);
-          acc.y = relu_np(acc.y);
-          acc.z = relu_np(acc.z);
-          acc.w = relu_np(acc.w);
-        }
+#pragma unroll
+        for (int u = 0; u < W; ++u) acc[u] = relu_np(acc[u]);
       }
     }
-    const int col = w.c0 + cq;
-    float* o = w.out + (int64_t)r * w.ld + col;
+  }
+  const int col = w.c0 + cq;
+  float* o = w.out + (int64_t)r * w.ld + col;
+  if constexpr (W == 4) {
     if (col + 3 < w.n) {
-      *reinterpret_cast<float4*>(o) = acc;
+      *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
     } else {
-      if (col < w.n) o[0] = acc.x;
-      if (col + 1 < w.n) o[1] = acc.y;
-      if (col + 2 < w.n) o[2] = acc.z;
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (col + u < w.n) o[u] = acc[u];
     }
-    if constexpr (K == kFwdLast) {
-      // the logits of the cluster's columns into every CTA's logit block
-      const unsigned a = w.lg + (unsigned)(r * 32 + cq) * 4u;
-      for (unsigned t = 0; t < w.C; ++t) {
-        unsigned remote;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(a), "r"(t));
+  } else {
+    if (col < w.n) o[0] = acc[0];
+  }
+  if constexpr (K == kFwdLast) {
+    // the logits of the cluster's columns into every CTA's logit block
+    const unsigned a = w.lg + (unsigned)(r * 32 + cq) * 4u;
+    for (unsigned t = 0; t < w.C; ++t) {
+      unsigned remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(a), "r"(t));
+      if constexpr (W == 4) {
         asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote),
-                     "f"(acc.x), "f"(acc.y), "f"(acc.z), "f"(acc.w)
+                     "f"(acc[0]), "f"(acc[1]), "f"(acc[2]), "f"(acc[3])
                      : "memory");
+      } else {
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(acc[0]) : "memory");
       }
     }
   }
 }
 
-__device__ __forceinline__ int4 lds_s32x4(const int32_t* p) {
-  int4 v;
-  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(smem_u32(p)));
-  return v;
-}
-__device__ __forceinline__ float4 lds_f32v4(const float* p) {
-  return lds_f32x4(smem_u32(p));
+// The CTA's rows of one product, 4 rows per warp at a time (8-lane groups, 4
+// columns per lane).  Software pipeline over quads: the indices / values of
+// quad k+2 and the 4 operand rows of quad k+1 are in flight while quad k is
+// summed.  A group whose row has no quads left reads the no-op quad.
+template <int K>
+__device__ __forceinline__ void run_rows(const RowTask& w, int warp, int lane) {
+  const int g = lane >> 3, l8 = lane & 7;
+  const int cq = 4 * l8;
+  const unsigned xb = w.X + 4u * (unsigned)cq;
+  // slot (sorted row) warp + 16 g + 64 t: a CTA with at most 16 rows gives
+  // every warp its own row
+  for (int base = warp; base < w.nrows; base += 4 * kChainWarps) {
+    const int slot = base + kChainWarps * g;
+    const bool has = slot < w.nrows;
+    const int r = has ? w.order[slot] : 0;
+    const int qb = has ? w.sp[r - w.pr0] - w.a0 : w.dummy;
+    const int nq = has ? (w.sp[r + 1 - w.pr0] - w.a0 - qb) >> 2 : 0;
+    const int trip = __reduce_max_sync(0xffffffffu, nq);
+    auto qa = [&](int k) { return (unsigned)(k < nq ? qb + 4 * k : w.dummy) * 4u; };
+    auto opnd = [&](const int4 c, float4 (&x)[4]) {
+      x[0] = lds_f32x4(xb + (unsigned)c.x * 128u);
+      x[1] = lds_f32x4(xb + (unsigned)c.y * 128u);
+      x[2] = lds_f32x4(xb + (unsigned)c.z * 128u);
+      x[3] = lds_f32x4(xb + (unsigned)c.w * 128u);
+    };
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int4 c1 = lds_s32x4(w.si + qa(1));
+    float4 v0 = lds_f32x4(w.sv + qa(0)), v1 = lds_f32x4(w.sv + qa(1));
+    float4 x0[4];
+    opnd(lds_s32x4(w.si + qa(0)), x0);
+    for (int k = 0; k < trip; ++k) {
+      float4 x1[4];
+      opnd(c1, x1);
+      const int4 c2 = lds_s32x4(w.si + qa(k + 2));
+      const float4 v2 = lds_f32x4(w.sv + qa(k + 2));
+      const float vv[4] = {v0.x, v0.y, v0.z, v0.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[0] = add_rn(acc[0], mul_rn(vv[u], x0[u].x));
+        acc[1] = add_rn(acc[1], mul_rn(vv[u], x0[u].y));
+        acc[2] = add_rn(acc[2], mul_rn(vv[u], x0[u].z));
+        acc[3] = add_rn(acc[3], mul_rn(vv[u], x0[u].w));
+      }
+      v0 = v1;
+      v1 = v2;
+      c1 = c2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x0[u] = x1[u];
+    }
+    if (has) epilogue<K, 4>(w, r, cq, acc);
+  }
 }
 
 // Long rows (the output layer's ~300-nonzero rows at config 2): one row per
-// warp, one column per lane, so a lane's chain costs ~5 instructions per
-// element instead of ~15 (quads of (index, value) pairs by broadcast 16-byte
-// loads two quads ahead, the 4 operands of the next quad one quad ahead).
+// warp, one column per lane, ~5 instructions per element.
 template <int K>
 __device__ __forceinline__ void run_rows_wide(const RowTask& w, int warp, int lane) {
-  const int32_t* ci = w.si - w.a0;
-  const float* cv = w.sv - w.a0;
-  const unsigned xl = smem_u32(w.X) + 4u * (unsigned)lane;
+  const unsigned xl = w.X + 4u * (unsigned)lane;
   for (int slot = warp; slot < w.nrows; slot += kChainWarps) {
     const int r = w.order[slot];
-    int j = w.sp[r - w.pr0];
-    const int e = w.sp[r + 1 - w.pr0];
-    float acc = 0.f;
-    for (; j < e && (j & 3); ++j)
-      acc = add_rn(acc, mul_rn(lds_f32(cv + j), lds_f32x1(xl + 128u * (unsigned)lds_s32(ci + j))));
-    const int nq = (e - j) >> 2;
-    if (nq > 0) {
-      const int last = j + 4 * (nq - 1);
-      const int jb = j;
-      auto at = [&](int i) { return min(jb + 4 * i, last); };
-      auto xq = [&](const int4 c) {
-        return make_float4(lds_f32x1(xl + 128u * (unsigned)c.x), lds_f32x1(xl + 128u * (unsigned)c.y),
-                           lds_f32x1(xl + 128u * (unsigned)c.z), lds_f32x1(xl + 128u * (unsigned)c.w));
-      };
-      int4 c1 = lds_s32x4(ci + at(1));
-      float4 v0 = lds_f32v4(cv + at(0)), v1 = lds_f32v4(cv + at(1));
-      float4 x0 = xq(lds_s32x4(ci + at(0)));
-      for (int i = 0; i < nq; ++i) {
-        const float4 x1 = xq(c1);
-        const int4 c2 = lds_s32x4(ci + at(i + 2));
-        const float4 v2 = lds_f32v4(cv + at(i + 2));
-        acc = add_rn(acc, mul_rn(v0.x, x0.x));
-        acc = add_rn(acc, mul_rn(v0.y, x0.y));
-        acc = add_rn(acc, mul_rn(v0.z, x0.z));
-        acc = add_rn(acc, mul_rn(v0.w, x0.w));
-        v0 = v1;
-        x0 = x1;
-        v1 = v2;
-        c1 = c2;
-      }
-      j += 4 * nq;
+    const int qb = w.sp[r - w.pr0] - w.a0;
+    const int nq = (w.sp[r + 1 - w.pr0] - w.a0 - qb) >> 2;
+    auto qa = [&](int k) { return (unsigned)(k < nq ? qb + 4 * k : w.dummy) * 4u; };
+    auto opnd = [&](const int4 c) {
+      return make_float4(lds_f32(xl + (unsigned)c.x * 128u), lds_f32(xl + (unsigned)c.y * 128u),
+                         lds_f32(xl + (unsigned)c.z * 128u), lds_f32(xl + (unsigned)c.w * 128u));
+    };
+    float acc[1] = {0.f};
+    int4 c1 = lds_s32x4(w.si + qa(1));
+    float4 v0 = lds_f32x4(w.sv + qa(0)), v1 = lds_f32x4(w.sv + qa(1));
+    float4 x0 = opnd(lds_s32x4(w.si + qa(0)));
+    for (int k = 0; k < nq; ++k) {
+      const float4 x1 = opnd(c1);
+      const int4 c2 = lds_s32x4(w.si + qa(k + 2));
+      const float4 v2 = lds_f32x4(w.sv + qa(k + 2));
+      acc[0] = add_rn(acc[0], mul_rn(v0.x, x0.x));
+      acc[0] = add_rn(acc[0], mul_rn(v0.y, x0.y));
+      acc[0] = add_rn(acc[0], mul_rn(v0.z, x0.z));
+      acc[0] = add_rn(acc[0], mul_rn(v0.w, x0.w));
+      v0 = v1;
+      v1 = v2;
+      x0 = x1;
+      c1 = c2;
     }
-    for (; j < e; ++j)
-      acc = add_rn(acc, mul_rn(lds_f32(cv + j), lds_f32x1(xl + 128u * (unsigned)lds_s32(ci + j))));
-    if constexpr (K == kBwd) {
-      if (w.act) acc = mul_rn(acc, ((w.mbits[r - w.r0] >> lane) & 1u) ? 1.f : 0.f);
-    } else {
-      if (w.sbias != nullptr) acc = add_rn(acc, w.sbias[r - w.pr0]);
-      if constexpr (K == kFwd) {
-        if (w.act) acc = relu_np(acc);
-      }
-    }
-    const int col = w.c0 + lane;
-    if (col < w.n) w.out[(int64_t)r * w.ld + col] = acc;
-    if constexpr (K == kFwdLast) {
-      const unsigned a = w.lg + (unsigned)(r * 32 + lane) * 4u;
-      for (unsigned t = 0; t < w.C; ++t) {
-        unsigned remote;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(a), "r"(t));
-        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(acc) : "memory");
-      }
-    }
+    epilogue<K, 1>(w, r, lane, acc);
   }
 }
 
@@ -408,21 +347,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long s_bar[NPH + 1];  // + the staging barrier
   __shared__ int s_bnd[NPH][2];
-  // the phase descriptors in shared memory: read from the (3 KB) parameter
-  // block inside the loops, they miss the constant cache
+  // the phase descriptors in shared memory (indexed loads of the 3 KB
+  // parameter block miss the constant cache)
   __shared__ __align__(16) ChainPhase s_ph[NPH];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   static_assert(sizeof(ChainPhase) % 4 == 0, "phase descriptor words");
-  static_assert(NPH <= kChainWarps, "one warp per phase descriptor");
-  // (one address per load: lanes reading different parameter words would
-  // serialise in the constant cache)
-  if (lane == 0 && warp < NPH) {
-    constexpr int kW = (int)sizeof(ChainPhase) / 4;
-    const int* src = reinterpret_cast<const int*>(&P.ph[warp]);
-    int* dst = reinterpret_cast<int*>(&s_ph[warp]);
-#pragma unroll
-    for (int k = 0; k < kW; ++k) dst[k] = src[k];
-  }
+  static_assert(NPH < kChainWarps, "one warp per phase descriptor");
   const unsigned q = cluster_rank(), C = cluster_size();
   const int group = (int)(blockIdx.x / C);
   const int c0 = group * 32;
@@ -433,7 +363,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   float* A = reinterpret_cast<float*>(base + P.off_A);
   float* D = reinterpret_cast<float*>(base + P.off_D);
   float* LG = reinterpret_cast<float*>(base + P.off_LG);
+  float* E = LG + kChainMaxClasses * 32;  // exp(z) per class
+  float* S = E + kChainMaxClasses * 32;   // s per column
+  float* TT = S + 32;                     // targets
   const unsigned bar0 = smem_u32(&s_bar[0]);
+  const unsigned stage_bar = bar0 + 8 * NPH;
 
   unsigned long long* prof = P.prof ? P.prof + (size_t)blockIdx.x * 32 : nullptr;
   int nprof = 0;
@@ -446,65 +380,71 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
     ++nprof;
   };
   stamp();
+  // (one address per parameter load: lanes reading different words would
+  // serialise in the constant cache)
+  if (lane == 0 && warp < NPH) {
+    constexpr int kW = (int)sizeof(ChainPhase) / 4;
+    const int* src = reinterpret_cast<const int*>(&P.ph[warp]);
+    int* dst = reinterpret_cast<int*>(&s_ph[warp]);
+#pragma unroll
+    for (int k = 0; k < kW; ++k) dst[k] = src[k];
+  }
   if (tid == 0) {
 #pragma unroll
     for (int p = 0; p < NPH; ++p) mbar_init(bar0 + 8 * p, 1);
-    mbar_init(bar0 + 8 * NPH, NPH);  // one arrival per phase's staging thread
+    mbar_init(stage_bar, NPH);  // one arrival per phase's staging thread
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // the targets of the softmax columns (older than the previous kernel), one
+  // class per warp; the zero row of the first transposed product's operand
+  if (warp < P.classes) TT[warp * 32 + lane] = ok ? P.t[warp * P.ld_t + col] : 0.f;
+  if (warp == kChainWarps - 1) D[P.classes * 32 + lane] = 0.f;
   __syncthreads();
-  stamp();
-  // every phase's segment bounds for this CTA's rows, loaded in parallel
+  // every phase's padded segment bounds for this CTA's rows
   if (tid < 2 * NPH) {
     const ChainPhase& f = s_ph[tid >> 1];
     s_bnd[tid >> 1][tid & 1] = f.ptr[f.split[q + (tid & 1)]];
   }
-  // the targets of the softmax columns (older than the previous kernel)
-  float tr[kChainMaxClasses];
-  if (warp == 0) {
-#pragma unroll
-    for (int c = 0; c < kChainMaxClasses; ++c)
-      tr[c] = (c < P.classes && ok) ? P.t[c * P.ld_t + col] : 0.f;
-  }
   __syncthreads();
   stamp();
-  // stage every phase's pointer / index / value segment, row order and bias
-  // slice for this CTA's rows with 1-D bulk copies (thread p issues phase
-  // p's; the last < 4 words of a segment are copied by plain loads, so no
-  // copy reads past an array).  Static data and values older than the
-  // previous kernel: before the programmatic-dependency wait.
-  const unsigned stage_bar = bar0 + 8 * NPH;
+  // stage every phase's padded pointers / indices / values, row order and
+  // bias slice for this CTA's rows with 1-D bulk copies (thread p issues
+  // phase p's; a pointer / order / bias slice is rounded up to 16-byte chunks
+  // where the array allows, its last < 4 words otherwise copied by plain
+  // loads).  Static data and values older than the previous kernel: before
+  // the programmatic-dependency wait.
   if (tid < NPH) {
     const int p = tid;
     const ChainPhase& f = s_ph[p];
     const int r0 = f.split[q], r1 = f.split[q + 1];
     const int pr0 = r0 & ~3;
-    const int a0 = s_bnd[p][0] & ~3;
-    const int a1 = s_bnd[p][1];
+    const int a0 = s_bnd[p][0], a1 = s_bnd[p][1];
     int32_t* sp = reinterpret_cast<int32_t*>(base + f.meta_off);
     int32_t* si = sp + f.ptr_words;
     float* sv = reinterpret_cast<float*>(si + f.nz_words);
     unsigned bytes = 0;
-    auto seg = [&](void* dst, const void* src, int words) {
-      const int body = words & ~3;
+    auto seg = [&](void* dst, const void* src, int words, int avail) {
+      const int up = (words + 3) & ~3;
+      const int body = up <= avail ? up : (words & ~3);
       if (body > 0) {
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(smem_u32(dst)), "l"(src), "r"(4 * body), "r"(stage_bar)
-            : "memory");
+        bulk_g2s(smem_u32(dst), src, 4u * (unsigned)body, stage_bar);
         bytes += 4u * (unsigned)body;
       }
       for (int k = body; k < words; ++k)
         static_cast<int32_t*>(dst)[k] = static_cast<const int32_t*>(src)[k];
     };
-    seg(sp, f.ptr + pr0, r1 + 1 - pr0);
-    seg(si, f.idx + a0, a1 - a0);
-    seg(sv, f.val + a0, a1 - a0);
-    seg(base + f.order_off, f.order + pr0, r1 - pr0);
-    if (p < NF && f.bias != nullptr) seg(base + f.epi_off, f.bias + pr0, r1 - pr0);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(stage_bar),
-                 "r"(bytes)
-                 : "memory");
+    seg(sp, f.ptr + pr0, r1 + 1 - pr0, f.rows + 1 - pr0);
+    seg(si, f.idx + a0, a1 - a0, f.nnzp - a0);
+    seg(sv, f.val + a0, a1 - a0, f.nnzp - a0);
+    seg(base + f.order_off, f.order + pr0, r1 - pr0, ((f.rows + 3) & ~3) - pr0);
+    if (p < NF && f.bias != nullptr) seg(base + f.epi_off, f.bias + pr0, r1 - pr0, f.rows - pr0);
+    // the no-op quad after the segment: the zero row, -0.0
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      si[a1 - a0 + k] = f.zero_row;
+      sv[a1 - a0 + k] = -0.f;
+    }
+    mbar_expect_tx(stage_bar, bytes);
   }
   stamp();
 
@@ -523,7 +463,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   pdl_wait();
   reload(0);
   mbar_wait(stage_bar, 0);
-  __syncthreads();  // staged segments (and their plain-copied tails) visible
+  __syncthreads();  // staged segments (and their plain-copied parts) visible
   stamp();
 
   double loss_local = 0.0;
@@ -533,41 +473,43 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
     if (p == NF) {
       // softmax cross-entropy gradient of the cluster's 32 columns from the
       // logits every CTA received (so the first transposed product needs no
-      // exchange); the rank-0 CTA writes d_{L-1}.  softmax_step_kernel's
-      // column code (elementwise.cu).
+      // exchange), parallel over classes: warp c computes e_c = exp(z_c),
+      // warp 0 sums s and z.t in class order (the loss term), warp c forms
+      // d_c = (e_c / s - t_c) / divisor; the rank-0 CTA writes d_{L-1}
+      const int classes = P.classes;
+      if (warp < classes) {
+        float mx = LG[lane];
+        for (int c = 1; c < classes; ++c) {
+          const float v = LG[c * 32 + lane];
+          mx = (v > mx || v != v) ? v : mx;
+        }
+        E[warp * 32 + lane] = exp_full(sub_rn(LG[warp * 32 + lane], mx));
+      }
+      __syncthreads();
       if (warp == 0) {
-        const int classes = P.classes;
-        float er[kChainMaxClasses];
-#pragma unroll
-        for (int c = 0; c < kChainMaxClasses; ++c) er[c] = c < classes ? LG[c * 32 + lane] : 0.f;
-        float mx = er[0];
-#pragma unroll
-        for (int c = 1; c < kChainMaxClasses; ++c)
-          if (c < classes) mx = (er[c] > mx || er[c] != er[c]) ? er[c] : mx;
-        float s = 0.f, zt = 0.f;
-#pragma unroll
-        for (int c = 0; c < kChainMaxClasses; ++c) {
-          if (c < classes) {
-            const float z = sub_rn(er[c], mx);
-            er[c] = exp_full(z);
-            s = add_rn(s, er[c]);
-            zt = add_rn(zt, mul_rn(z, tr[c]));
-          }
+        float mx = LG[lane];
+        for (int c = 1; c < classes; ++c) {
+          const float v = LG[c * 32 + lane];
+          mx = (v > mx || v != v) ? v : mx;
         }
-#pragma unroll
-        for (int c = 0; c < kChainMaxClasses; ++c) {
-          if (c < classes) {
-            const float g = div_rn(sub_rn(div_rn(er[c], s), tr[c]), P.divisor);
-            D[c * 32 + lane] = ok ? g : 0.f;
-            if (q == 0 && ok) P.dy_top[c * P.ld + col] = g;
-          }
+        float sum = 0.f, zt = 0.f;
+        for (int c = 0; c < classes; ++c) {
+          sum = add_rn(sum, E[c * 32 + lane]);
+          zt = add_rn(zt, mul_rn(sub_rn(LG[c * 32 + lane], mx), TT[c * 32 + lane]));
         }
-        loss_local = ok ? static_cast<double>(sub_rn(log_full(s), zt)) : 0.0;
+        S[lane] = sum;
+        loss_local = ok ? static_cast<double>(sub_rn(log_full(sum), zt)) : 0.0;
+      }
+      __syncthreads();
+      if (warp < classes) {
+        const float g =
+            div_rn(sub_rn(div_rn(E[warp * 32 + lane], S[lane]), TT[warp * 32 + lane]), P.divisor);
+        D[warp * 32 + lane] = ok ? g : 0.f;
+        if (q == 0 && ok) P.dy_top[warp * P.ld + col] = g;
       }
       __syncthreads();
       stamp();
     }
-    const float* X = p == NF ? D : A;
     if (f.in_map >= 0) {
       mbar_wait(bar0 + 8 * p, 0);
       stamp();
@@ -581,23 +523,31 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
       if (b.act) {
         unsigned* mb = reinterpret_cast<unsigned*>(base + b.epi_off);
         const int b0 = b.split[q], b1 = b.split[q + 1];
-        for (int r = b0 + warp; r < b1; r += kChainWarps) {
-          const unsigned bits = __ballot_sync(0xffffffffu, A[r * 32 + lane] > 0.f);
-          if (lane == 0) mb[r - b0] = bits;
+        const unsigned ab = smem_u32(A) + 4u * (unsigned)lane;
+        for (int r = b0 + warp; r < b1; r += 4 * kChainWarps) {
+          float a[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            a[u] = lds_f32(ab + 128u * (unsigned)min(r + u * kChainWarps, b1 - 1));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned bits = __ballot_sync(0xffffffffu, a[u] > 0.f);
+            if (lane == 0 && r + u * kChainWarps < b1) mb[r + u * kChainWarps - b0] = bits;
+          }
         }
       }
     }
     stamp();
     RowTask w;
-    w.dbg = (prof != nullptr && p == NF - 1) ? prof + 20 : nullptr;
     w.sp = reinterpret_cast<const int32_t*>(base + f.meta_off);
     w.pr0 = r0 & ~3;
-    w.a0 = s_bnd[p][0] & ~3;
-    w.si = w.sp + f.ptr_words;
-    w.sv = reinterpret_cast<const float*>(w.si + f.nz_words);
+    w.a0 = s_bnd[p][0];
+    w.si = smem_u32(w.sp + f.ptr_words);
+    w.sv = w.si + 4u * (unsigned)f.nz_words;
+    w.dummy = s_bnd[p][1] - s_bnd[p][0];
     w.order = reinterpret_cast<const int32_t*>(base + f.order_off) + (r0 - (r0 & ~3));
     w.nrows = r1 - r0;
-    w.X = X;
+    w.X = p == NF ? smem_u32(D) : smem_u32(A);
     w.sbias = (p < NF && f.bias != nullptr) ? reinterpret_cast<const float*>(base + f.epi_off)
                                             : nullptr;
     w.mbits = reinterpret_cast<const unsigned*>(base + f.epi_off);
@@ -653,6 +603,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   }
 }
 
+// padded value copies: pval[s] = values[src[s]], or -0.0 for a pad
+__global__ void chain_refresh_kernel(const int32_t* __restrict__ src,
+                                     const float* __restrict__ values, float* __restrict__ pval,
+                                     int64_t n) {
+  pdl_wait();
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = src[s];
+    pval[s] = k >= 0 ? values[k] : -0.f;
+  }
+  pdl_trigger();
+}
+
 }  // namespace
 }  // namespace smb
 
@@ -661,12 +624,16 @@ struct smb_chain_plan {
   int64_t n = 0, ld = 0;
   int classes = 0;
   size_t smem = 0;
-  smb::ChainParams proto;  // everything but the per-step pointers and maps
-  std::vector<int64_t> rows;  // m of every layer
-  std::vector<int> relu;      // activation after every layer
-  int32_t* order_dev = nullptr;  // every phase's row order (owned)
+  smb::ChainParams proto;        // everything but the per-step pointers and maps
+  std::vector<int64_t> rows;     // m of every layer
+  std::vector<int> relu;         // activation after every layer
+  std::vector<int64_t> src_off;  // per layer: [fwd | bwd] padded slots in src / pval
+  std::vector<int64_t> src_len;
+  void* dev = nullptr;           // owned: pointers, indices, orders, src maps, values
+  int32_t* src = nullptr;
+  float* pval = nullptr;
   ~smb_chain_plan() {
-    if (order_dev) cudaFree(order_dev);
+    if (dev) cudaFree(dev);
   }
 };
 
@@ -676,6 +643,37 @@ using smb::ChainPhase;
 extern "C" size_t smb_chain_workspace_bytes(int64_t n) {
   return 256 + sizeof(double) * (size_t)smb::ceil_div(n > 0 ? n : 1, 32);
 }
+
+namespace {
+// A padded product: segment pointers (multiples of 4), operand rows (pads:
+// zero_row), the source value index of every slot (-1: pad).
+struct Padded {
+  std::vector<int32_t> ptr, idx, src, order;
+};
+
+Padded pad_segments(const std::vector<int32_t>& seg, const std::vector<int32_t>& idx,
+                    const int32_t* value_of, int zero_row) {
+  Padded out;
+  const int rows = (int)seg.size() - 1;
+  out.ptr.resize((size_t)rows + 1);
+  out.ptr[0] = 0;
+  for (int r = 0; r < rows; ++r) out.ptr[r + 1] = out.ptr[r] + ((seg[r + 1] - seg[r] + 3) & ~3);
+  out.idx.assign((size_t)out.ptr[rows], zero_row);
+  out.src.assign((size_t)out.ptr[rows], -1);
+  for (int r = 0; r < rows; ++r)
+    for (int s = seg[r]; s < seg[r + 1]; ++s) {
+      out.idx[out.ptr[r] + (s - seg[r])] = idx[s];
+      out.src[out.ptr[r] + (s - seg[r])] = value_of ? value_of[s] : s;
+    }
+  return out;
+}
+
+template <typename T>
+bool to_host(std::vector<T>& v, const T* d, int64_t n) {
+  v.resize((size_t)n);
+  return n == 0 || cudaMemcpy(v.data(), d, sizeof(T) * n, cudaMemcpyDeviceToHost) == cudaSuccess;
+}
+}  // namespace
 
 extern "C" int smb_chain_plan_create(int nlayers, const smb_pattern* const* patterns,
                                      const int* relu, int64_t n, int64_t ld,
@@ -695,7 +693,7 @@ extern "C" int smb_chain_plan_create(int nlayers, const smb_pattern* const* patt
     if (l > 0)
       SMB_REQUIRE(patterns[l]->k == patterns[l - 1]->m, "chain: layer %d input width mismatch", l);
     SMB_REQUIRE(patterns[l]->m < (1 << 24) && patterns[l]->k < (1 << 24) &&
-                    patterns[l]->nnz < (1ll << 31),
+                    patterns[l]->nnz < (1ll << 29),
                 "chain: unsupported layer size");
   }
   const int classes = (int)patterns[nlayers - 1]->m;
@@ -719,56 +717,81 @@ extern "C" int smb_chain_plan_create(int nlayers, const smb_pattern* const* patt
     plan->rows.push_back(patterns[l]->m);
     plan->relu.push_back(relu[l] != 0);
   }
-  cudaDeviceSynchronize();  // setup: host copies of the segment pointers
+  cudaDeviceSynchronize();  // setup: host copies of the structure
   ChainParams& P = plan->proto;
   memset(&P, 0, sizeof(P));
+  // padded products: forward phase l-1 (CSR of layer l), backward phase
+  // 2L-2-l (CSC of layer l)
+  std::vector<Padded> pads(2 * (L - 1));
+  bool okc = true;
+  for (int l = 1; l < L && okc; ++l) {
+    const smb_pattern* pat = patterns[l];
+    std::vector<int32_t> rp, ci, cp, ri, pm;
+    okc = to_host(rp, pat->row_ptr, pat->m + 1) && to_host(ci, pat->col_idx, pat->nnz) &&
+          to_host(cp, pat->col_ptr, pat->k + 1) && to_host(ri, pat->row_idx, pat->nnz) &&
+          to_host(pm, pat->perm, pat->nnz);
+    if (!okc) break;
+    pads[l - 1] = pad_segments(rp, ci, nullptr, (int)pat->k);
+    pads[2 * L - 2 - l] = pad_segments(cp, ri, pm.data(), (int)pat->m);
+  }
+  if (!okc) {
+    delete plan;
+    set_error("chain: reading the pattern structure failed");
+    return SMB_ERR_CUDA;
+  }
+  // one device block: per phase ptr | idx | order (int32, 16-byte aligned
+  // pieces), then per layer the src map, then the padded values
+  std::vector<int32_t> blob;
+  auto put = [&](const std::vector<int32_t>& v) {
+    const size_t at = blob.size();
+    blob.insert(blob.end(), v.begin(), v.end());
+    while (blob.size() % 4) blob.push_back(0);
+    return at;
+  };
+  std::vector<size_t> at_ptr(2 * (L - 1)), at_idx(2 * (L - 1)), at_order(2 * (L - 1));
   size_t off = 0;
   int max_in_rows = 0;
-  std::vector<int32_t> order_host;
-  std::vector<size_t> order_at(2 * kChainMaxL, 0);
-  auto fill = [&](int p, const smb_pattern* pat, bool fwd, int in_rows, int in_map) -> bool {
+  for (int p = 0; p < 2 * (L - 1); ++p) {
     ChainPhase& f = P.ph[p];
-    const int rows = (int)(fwd ? pat->m : pat->k);
-    std::vector<int32_t> ptr((size_t)rows + 1);
-    if (cudaMemcpy(ptr.data(), fwd ? pat->row_ptr : pat->col_ptr, sizeof(int32_t) * (rows + 1),
-                   cudaMemcpyDeviceToHost) != cudaSuccess)
-      return false;
-    // the CTAs' row ranges, balanced by nonzeros
-    const int64_t z = ptr[rows];
+    const bool fwd = p < L - 1;
+    const int l = fwd ? p + 1 : 2 * L - 2 - p;
+    const smb_pattern* pat = patterns[l];
+    Padded& pd = pads[p];
+    const int rows = (int)pd.ptr.size() - 1;
+    const int in_rows = (int)(fwd ? pat->k : pat->m);
+    // the CTAs' row ranges, balanced by (padded) nonzeros
+    const int64_t z = pd.ptr[rows];
     f.split[0] = 0;
     for (int q = 1; q < C; ++q) {
       const int64_t target = z * q / C;
-      const int r = (int)(std::lower_bound(ptr.begin(), ptr.end(), (int32_t)target) - ptr.begin());
+      const int r = (int)(std::lower_bound(pd.ptr.begin(), pd.ptr.end(), (int32_t)target) -
+                          pd.ptr.begin());
       f.split[q] = std::max(f.split[q - 1], std::min(r, rows));
     }
     f.split[C] = rows;
-    // each CTA's rows, longest segment first (a warp's 4 rows then take about
-    // the same number of steps)
-    order_at[p] = order_host.size();
+    // each CTA's rows, longest segment first
     for (int q = 0; q < C; ++q) {
       std::vector<int32_t> rr;
       for (int r = f.split[q]; r < f.split[q + 1]; ++r) rr.push_back(r);
       std::stable_sort(rr.begin(), rr.end(), [&](int32_t a, int32_t b) {
-        return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b];
+        return pd.ptr[a + 1] - pd.ptr[a] > pd.ptr[b + 1] - pd.ptr[b];
       });
-      order_host.insert(order_host.end(), rr.begin(), rr.end());
+      pd.order.insert(pd.order.end(), rr.begin(), rr.end());
     }
-    while (order_host.size() % 4) order_host.push_back(0);  // 16-byte aligned phases
     int pw = 0, nw = 0, ew = 0, ow = 0;
     for (int q = 0; q < C; ++q) {
       const int r0 = f.split[q], r1 = f.split[q + 1], pr0 = r0 & ~3;
       pw = std::max(pw, ((r1 + 1 - pr0) + 3) & ~3);
-      nw = std::max(nw, ((ptr[r1] - (ptr[r0] & ~3)) + 3) & ~3);
+      nw = std::max(nw, pd.ptr[r1] - pd.ptr[r0] + 4);  // + the no-op quad
       // forward: the bias slice from pr0; backward: one mask word per row
       ew = std::max(ew, fwd ? (((r1 - pr0) + 3) & ~3) : (((r1 - r0) + 3) & ~3));
       ow = std::max(ow, ((r1 - pr0) + 3) & ~3);
     }
     f.rows = rows;
-    f.nnz = (int)pat->nnz;
-    // rows of >= 48 nonzeros on average run one per warp (lane = column)
-    f.wide = rows > 0 && z >= (int64_t)48 * rows;
-    f.ptr = fwd ? pat->row_ptr : pat->col_ptr;
-    f.idx = fwd ? pat->col_idx : pat->row_idx;
+    f.nnzp = (int)z;
+    f.act = fwd ? (relu[l] != 0) : (relu[l - 1] != 0);
+    f.zero_row = in_rows;
+    f.wide = rows > 0 && z >= (int64_t)48 * rows;  // long rows: one per warp
     f.meta_off = (int)off;
     f.ptr_words = pw;
     f.nz_words = nw;
@@ -777,45 +800,70 @@ extern "C" int smb_chain_plan_create(int nlayers, const smb_pattern* const* patt
     off += (size_t)4 * ew;
     f.order_off = (int)off;
     off += (size_t)4 * ow;
-    f.in_map = in_map;
-    f.in_box_rows = std::min(kBoxRows, std::max(in_rows, 1));
-    f.in_boxes = (int)ceil_div(in_rows, f.in_box_rows);
-    if (in_map >= 0) max_in_rows = std::max(max_in_rows, f.in_boxes * f.in_box_rows);
-    return true;
-  };
-  bool okc = true;
-  // forward phases p = l - 1 for layers l = 1..L-1: operand a_{l-1} (map l-1)
+    // operand reload: boxes of <= 256 rows covering the rows AND the zero
+    // row after them (out-of-bounds rows of a box are zero-filled)
+    f.in_map = fwd ? l - 1 : (p == L - 1 ? -1 : (L - 1) + (l - 1));
+    const int need = in_rows + 1;
+    f.in_boxes = (int)ceil_div(need, 256);
+    f.in_box_rows = (int)ceil_div(need, f.in_boxes);
+    if (f.in_map >= 0) max_in_rows = std::max(max_in_rows, f.in_boxes * f.in_box_rows);
+    at_ptr[p] = put(pd.ptr);
+    at_idx[p] = put(pd.idx);
+    at_order[p] = put(pd.order);
+  }
+  // per layer: the src map of [forward | backward] padded slots
+  plan->src_off.assign(L, 0);
+  plan->src_len.assign(L, 0);
+  const size_t src_at = blob.size();
+  std::vector<size_t> at_pval_f(L, 0), at_pval_b(L, 0);
+  size_t src_words = 0;
   for (int l = 1; l < L; ++l) {
-    okc = okc && fill(l - 1, patterns[l], true, (int)patterns[l]->k, l - 1);
-    P.ph[l - 1].act = relu[l] != 0;
+    const Padded& pf = pads[l - 1];
+    const Padded& pb = pads[2 * L - 2 - l];
+    plan->src_off[l] = (int64_t)src_words;
+    at_pval_f[l] = src_words;
+    blob.insert(blob.end(), pf.src.begin(), pf.src.end());
+    src_words += pf.src.size();
+    while (src_words % 4) {
+      blob.push_back(-1);
+      ++src_words;
+    }
+    at_pval_b[l] = src_words;
+    blob.insert(blob.end(), pb.src.begin(), pb.src.end());
+    src_words += pb.src.size();
+    while (src_words % 4) {
+      blob.push_back(-1);
+      ++src_words;
+    }
+    plan->src_len[l] = (int64_t)src_words - plan->src_off[l];
   }
-  // backward phases p = L-1+j for layers l = L-1-j: operand d_l (region D
-  // for the top layer, else map (L-1) + (l-1)); mask = relu of layer l-1
-  for (int j = 0; j < L - 1; ++j) {
-    const int l = L - 1 - j;
-    okc = okc && fill(L - 1 + j, patterns[l], false, (int)patterns[l]->m,
-                      j == 0 ? -1 : (L - 1) + (l - 1));
-    P.ph[L - 1 + j].act = relu[l - 1] != 0;
-  }
-  if (okc && cudaMalloc(&plan->order_dev, sizeof(int32_t) * order_host.size()) == cudaSuccess &&
-      cudaMemcpy(plan->order_dev, order_host.data(), sizeof(int32_t) * order_host.size(),
-                 cudaMemcpyHostToDevice) == cudaSuccess) {
-    for (int p = 0; p < 2 * (L - 1); ++p) P.ph[p].order = plan->order_dev + order_at[p];
-  } else {
-    okc = false;
-  }
-  if (!okc) {
+  const size_t total_words = blob.size() + src_words;  // + the padded values
+  if (cudaMalloc(&plan->dev, 4 * std::max<size_t>(total_words, 4)) != cudaSuccess ||
+      cudaMemcpy(plan->dev, blob.data(), 4 * blob.size(), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
     delete plan;
-    set_error("chain: setting up the segment tables failed");
+    set_error("chain: allocating the padded structure failed");
     return SMB_ERR_CUDA;
+  }
+  int32_t* d = static_cast<int32_t*>(plan->dev);
+  plan->src = d + src_at;
+  plan->pval = reinterpret_cast<float*>(d + blob.size());
+  for (int p = 0; p < 2 * (L - 1); ++p) {
+    ChainPhase& f = P.ph[p];
+    const bool fwd = p < L - 1;
+    const int l = fwd ? p + 1 : 2 * L - 2 - p;
+    f.ptr = d + at_ptr[p];
+    f.idx = d + at_idx[p];
+    f.order = d + at_order[p];
+    f.val = plan->pval + (fwd ? at_pval_f[l] : at_pval_b[l]);
   }
   off = (off + 1023) & ~size_t(1023);
   P.off_A = (int)off;
   off += (size_t)max_in_rows * 128;
   P.off_D = (int)off;
-  off += (size_t)kChainMaxClasses * 128;
-  P.off_LG = (int)off;
-  off += (size_t)kChainMaxClasses * 128;
+  off += (size_t)(kChainMaxClasses + 1) * 128;  // + the zero row
+  P.off_LG = (int)off;                          // logits, exp(z), s, targets
+  off += (size_t)(3 * kChainMaxClasses + 1) * 128;
   plan->smem = off + 1024;  // alignment slack
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
@@ -858,6 +906,22 @@ extern "C" int smb_chain_plan_info(const smb_chain_plan* plan, int64_t* info4) {
   return SMB_OK;
 }
 
+extern "C" int smb_chain_refresh(const smb_chain_plan* plan, int layer, const void* values,
+                                 void* stream) {
+  using namespace smb;
+  clear_error();
+  SMB_REQUIRE(plan != nullptr && values != nullptr, "smb_chain_refresh: null argument");
+  SMB_REQUIRE(layer >= 1 && layer < plan->L, "smb_chain_refresh: layer %d out of 1..%d", layer,
+              plan->L - 1);
+  const int64_t nslots = plan->src_len[layer];
+  if (nslots == 0) return SMB_OK;
+  const int64_t o = plan->src_off[layer];
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nslots, 256), 4 * 148);
+  launch_k(chain_refresh_kernel, dim3(grid), dim3(256), 0, as_stream(stream), plan->src + o,
+           static_cast<const float*>(values), plan->pval + o, nslots);
+  return check_launch("smb_chain_refresh");
+}
+
 namespace {
 bool map_rows32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t n, int64_t ld,
                 int box_rows) {
@@ -893,14 +957,13 @@ void launch_chain(const smb_chain_plan* plan, const ChainParams& P, cudaStream_t
 }
 }  // namespace
 
-extern "C" int smb_chain_run(const smb_chain_plan* plan, const void* const* values,
-                             const void* const* values_csc, const void* const* bias,
+extern "C" int smb_chain_run(const smb_chain_plan* plan, const void* const* bias,
                              void* const* acts, void* const* dys, const void* t, int64_t ld_t,
                              double divisor, double* loss_out, void* workspace, void* stream) {
   using namespace smb;
   clear_error();
-  SMB_REQUIRE(plan != nullptr && values != nullptr && values_csc != nullptr && bias != nullptr &&
-                  acts != nullptr && dys != nullptr && t != nullptr,
+  SMB_REQUIRE(plan != nullptr && bias != nullptr && acts != nullptr && dys != nullptr &&
+                  t != nullptr,
               "smb_chain_run: null argument");
   SMB_REQUIRE(ld_t >= plan->n, "smb_chain_run: leading dimension of t smaller than n");
   SMB_REQUIRE(divisor != 0.0, "smb_chain_run: zero divisor");
@@ -911,14 +974,12 @@ extern "C" int smb_chain_run(const smb_chain_plan* plan, const void* const* valu
     SMB_REQUIRE(acts[l] != nullptr && dys[l] != nullptr && aligned16(acts[l]) && aligned16(dys[l]),
                 "smb_chain_run: activation / gradient buffers must be 16-byte aligned");
     if (l > 0)
-      SMB_REQUIRE(values[l] != nullptr && values_csc[l] != nullptr && aligned16(values[l]) &&
-                      aligned16(values_csc[l]) && aligned16(bias[l]),
-                  "smb_chain_run: value / bias buffers must be 16-byte aligned");
+      SMB_REQUIRE(bias[l] == nullptr || aligned16(bias[l]),
+                  "smb_chain_run: bias buffers must be 16-byte aligned");
   }
   ChainParams P = plan->proto;
   for (int l = 1; l < L; ++l) {
     ChainPhase& f = P.ph[l - 1];
-    f.val = static_cast<const float*>(values[l]);
     f.bias = static_cast<const float*>(bias[l]);
     f.out = static_cast<float*>(acts[l]);
     if (!map_rows32(&P.maps[l - 1], acts[l - 1], plan->rows[l - 1], plan->n, plan->ld,
@@ -930,7 +991,6 @@ extern "C" int smb_chain_run(const smb_chain_plan* plan, const void* const* valu
   for (int j = 0; j < L - 1; ++j) {
     const int l = L - 1 - j;
     ChainPhase& f = P.ph[L - 1 + j];
-    f.val = static_cast<const float*>(values_csc[l]);
     f.bias = nullptr;
     f.out = static_cast<float*>(dys[l - 1]);
     if (f.in_map >= 0 &&

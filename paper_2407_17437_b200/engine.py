@@ -122,6 +122,7 @@ class KernelTimer:
         torch.cuda.synchronize()
         for t, saved_t in snapshot:
             t.copy_(saved_t)
+        step.sync_weights()  # derived copies (CSC / padded) of the restored values
         torch.cuda.synchronize()
         return out
 
@@ -329,8 +330,6 @@ class FusedTrainStep:
             return None
         if not all(u.relu for u in us[:-1]) or us[-1].relu:
             return None
-        if any(u.vals_csc is None for u in us[1:]):
-            return None
         lib = _lib.load()
         L = len(us)
         pats = (C.c_void_p * L)(*[u.layer.weights.pattern.handle for u in us])
@@ -344,6 +343,10 @@ class FusedTrainStep:
             _lib.check(rc, "smb_chain_plan_create")
         self._chain_ws = torch.zeros(int(lib.smb_chain_workspace_bytes(self.B)), dtype=torch.uint8,
                                      device=self.dev)
+        # the chain reads the plan's padded value copies (refreshed after
+        # every update), not the CSC-ordered copies of the separate kernels
+        for u in us:
+            u.vals_csc = None
         return _ChainPlan(out.value)
 
     def chain_info(self):
@@ -380,11 +383,14 @@ class FusedTrainStep:
         if u.vals_csc is not None:
             _lib.call("smb_values_to_csc", _lib.SMB_F32, u.layer.weights.pattern.handle,
                       ptr(self._vals(u)), ptr(u.vals_csc[self._parity]), stream_ptr())
+        if self._chain is not None and u.index > 0:
+            _lib.call("smb_chain_refresh", self._chain.h, u.index, ptr(self._vals(u)),
+                      stream_ptr())
 
     def _adopt_external_changes(self) -> None:
         """Re-sync any layer whose values changed outside the step."""
         for u in self.units:
-            if u.vals is None and u.vals_csc is None:
+            if u.vals is None and u.vals_csc is None and self._chain is None:
                 continue
             v = u.layer.weights.values
             if v._version != u.seen or (
@@ -721,14 +727,11 @@ class FusedTrainStep:
                    ptr(self._vals(u0)), ptr(x_in), ld, B, ptr(u0.layer.bias),
                    _lib.SMB_EPI_RELU if u0.relu else _lib.SMB_EPI_NONE, ptr(self.acts[0]), ld, st)
         arr = C.c_void_p * L
-        vals = arr(*[ptr(self._vals(u)) for u in us])
-        vcsc = arr(*[ptr(u.vals_csc[self._parity]) if u.vals_csc is not None else None
-                     for u in us])
         bias = arr(*[ptr(u.layer.bias) for u in us])
         acts = arr(*[ptr(a) for a in self.acts])
         dys = arr(*[ptr(d) for d in self.dys])
-        self._call("chain", "smb_chain_run", self._chain.h, vals, vcsc, bias, acts, dys,
-                   ptr(t_in), ld, float(self.B_global), ptr(self.loss), ptr(self._chain_ws), st)
+        self._call("chain", "smb_chain_run", self._chain.h, bias, acts, dys, ptr(t_in), ld,
+                   float(self.B_global), ptr(self.loss), ptr(self._chain_ws), st)
         for li in [0] + list(range(L - 1, 0, -1)):
             u = us[li]
             x_prev = self.acts[li - 1] if li > 0 else x_in
@@ -784,6 +787,9 @@ class FusedTrainStep:
                 self._call(f"to_csc[{u.index}]", "smb_values_to_csc", F32,
                            lay.weights.pattern.handle, ptr(w_out),
                            ptr(u.vals_csc[self._parity ^ 1]), st)
+            if self._chain is not None and fuse_update and u.index > 0:
+                self._call(f"chain_refresh[{u.index}]", "smb_chain_refresh", self._chain.h,
+                           u.index, ptr(w_out), st)
             return
         if u.m <= DENSE_T_MAX_ROWS and lay.mask is None:
             # ER-saturated output layer: gradient chains + update in one
