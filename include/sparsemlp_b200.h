@@ -396,7 +396,7 @@ SMB_API int smb_chain_plan_create(int nlayers, const smb_pattern* const* pattern
                                   const int* relu, int64_t n, int64_t ld, smb_chain_plan** out);
 SMB_API int smb_chain_plan_destroy(smb_chain_plan* plan);
 SMB_API int smb_chain_plan_info(const smb_chain_plan* plan, int64_t* info4);
-/* Diagnostics: later runs of the plan record %globaltimer stamps of their
+/* Diagnostics: later runs of the plan record SM clock (clock64) stamps of their
  * phases (thread 0 of every CTA, 32 slots per CTA) into `stamps` (device,
  * uint64[CTAs x 32]); NULL turns it off. */
 SMB_API int smb_chain_plan_profile(smb_chain_plan* plan, void* stamps);

@@ -73,6 +73,7 @@ struct ChainPhase {
   int rows;              // output rows
   int nnzp;              // padded segment total
   int split[kChainMaxC + 1];  // the cluster's CTAs' row ranges (balanced by nonzeros)
+  int segb[kChainMaxC + 1];   // their padded segment bounds
   int act;               // forward: np.maximum(., 0); backward: ReLU mask of the layer below
   int zero_row;          // the operand's all-zero row
   int meta_off;          // shared-memory byte offset of the staged segment
@@ -373,21 +374,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   int nprof = 0;
   auto stamp = [&]() {
     if (prof != nullptr && tid == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      prof[nprof] = t;
+      // SM cycles (globaltimer ticks too coarsely for sub-microsecond phases)
+      prof[nprof] = clock64();
     }
     ++nprof;
   };
   stamp();
-  // (one address per parameter load: lanes reading different words would
-  // serialise in the constant cache)
-  if (lane == 0 && warp < NPH) {
+  if (warp < NPH) {
     constexpr int kW = (int)sizeof(ChainPhase) / 4;
     const int* src = reinterpret_cast<const int*>(&P.ph[warp]);
     int* dst = reinterpret_cast<int*>(&s_ph[warp]);
-#pragma unroll
-    for (int k = 0; k < kW; ++k) dst[k] = src[k];
+    for (int k = lane; k < kW; k += 32) dst[k] = src[k];
   }
   if (tid == 0) {
 #pragma unroll
@@ -401,10 +398,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   if (warp == kChainWarps - 1) D[P.classes * 32 + lane] = 0.f;
   __syncthreads();
   // every phase's padded segment bounds for this CTA's rows
-  if (tid < 2 * NPH) {
-    const ChainPhase& f = s_ph[tid >> 1];
-    s_bnd[tid >> 1][tid & 1] = f.ptr[f.split[q + (tid & 1)]];
-  }
+  if (tid < 2 * NPH) s_bnd[tid >> 1][tid & 1] = s_ph[tid >> 1].segb[q + (tid & 1)];
   __syncthreads();
   stamp();
   // stage every phase's padded pointers / indices / values, row order and
@@ -769,6 +763,7 @@ extern "C" int smb_chain_plan_create(int nlayers, const smb_pattern* const* patt
       f.split[q] = std::max(f.split[q - 1], std::min(r, rows));
     }
     f.split[C] = rows;
+    for (int q = 0; q <= C; ++q) f.segb[q] = pd.ptr[f.split[q]];
     // each CTA's rows, longest segment first
     for (int q = 0; q < C; ++q) {
       std::vector<int32_t> rr;

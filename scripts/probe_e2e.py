@@ -12,7 +12,8 @@ import paper_2407_17437_b200 as smb
 
 B, L = 1024, [3072, 1024, 512, 10]
 model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=L, density=0.01, batch_size=B))
-st = smb.FusedTrainStep(model, B)
+import os
+st = smb.FusedTrainStep(model, B, chain=os.environ.get("E2E_CHAIN", "1") == "1")
 rng = np.random.default_rng(0)
 xs = [torch.from_numpy(rng.standard_normal((L[0], B), dtype=np.float32)).pin_memory() for _ in range(4)]
 t = np.zeros((10, B), np.float32)
