@@ -46,6 +46,7 @@
 // 128-column CTAs are 4 of this kernel's column groups.
 #include "async_copy.cuh"
 #include "pattern.cuh"
+#include "padded.cuh"
 #include "tma.cuh"
 
 #include <algorithm>
@@ -597,10 +598,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
   }
 }
 
-// padded value copies: pval[s] = values[src[s]], or -0.0 for a pad
-__global__ void chain_refresh_kernel(const int32_t* __restrict__ src,
-                                     const float* __restrict__ values, float* __restrict__ pval,
-                                     int64_t n) {
+}  // namespace
+
+__global__ void padded_refresh_kernel(const int32_t* __restrict__ src,
+                                      const float* __restrict__ values, float* __restrict__ pval,
+                                      int64_t n) {
   pdl_wait();
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
@@ -609,8 +611,6 @@ __global__ void chain_refresh_kernel(const int32_t* __restrict__ src,
   }
   pdl_trigger();
 }
-
-}  // namespace
 }  // namespace smb
 
 struct smb_chain_plan {
@@ -637,37 +637,6 @@ using smb::ChainPhase;
 extern "C" size_t smb_chain_workspace_bytes(int64_t n) {
   return 256 + sizeof(double) * (size_t)smb::ceil_div(n > 0 ? n : 1, 32);
 }
-
-namespace {
-// A padded product: segment pointers (multiples of 4), operand rows (pads:
-// zero_row), the source value index of every slot (-1: pad).
-struct Padded {
-  std::vector<int32_t> ptr, idx, src, order;
-};
-
-Padded pad_segments(const std::vector<int32_t>& seg, const std::vector<int32_t>& idx,
-                    const int32_t* value_of, int zero_row) {
-  Padded out;
-  const int rows = (int)seg.size() - 1;
-  out.ptr.resize((size_t)rows + 1);
-  out.ptr[0] = 0;
-  for (int r = 0; r < rows; ++r) out.ptr[r + 1] = out.ptr[r] + ((seg[r + 1] - seg[r] + 3) & ~3);
-  out.idx.assign((size_t)out.ptr[rows], zero_row);
-  out.src.assign((size_t)out.ptr[rows], -1);
-  for (int r = 0; r < rows; ++r)
-    for (int s = seg[r]; s < seg[r + 1]; ++s) {
-      out.idx[out.ptr[r] + (s - seg[r])] = idx[s];
-      out.src[out.ptr[r] + (s - seg[r])] = value_of ? value_of[s] : s;
-    }
-  return out;
-}
-
-template <typename T>
-bool to_host(std::vector<T>& v, const T* d, int64_t n) {
-  v.resize((size_t)n);
-  return n == 0 || cudaMemcpy(v.data(), d, sizeof(T) * n, cudaMemcpyDeviceToHost) == cudaSuccess;
-}
-}  // namespace
 
 extern "C" int smb_chain_plan_create(int nlayers, const smb_pattern* const* patterns,
                                      const int* relu, int64_t n, int64_t ld,
@@ -912,7 +881,7 @@ extern "C" int smb_chain_refresh(const smb_chain_plan* plan, int layer, const vo
   if (nslots == 0) return SMB_OK;
   const int64_t o = plan->src_off[layer];
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(nslots, 256), 4 * 148);
-  launch_k(chain_refresh_kernel, dim3(grid), dim3(256), 0, as_stream(stream), plan->src + o,
+  launch_k(padded_refresh_kernel, dim3(grid), dim3(256), 0, as_stream(stream), plan->src + o,
            static_cast<const float*>(values), plan->pval + o, nslots);
   return check_launch("smb_chain_refresh");
 }
