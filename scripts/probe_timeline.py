@@ -11,7 +11,7 @@ layers = [int(x) for x in os.environ.get("TL_LAYERS", "3072,1024,512,10").split(
 d = float(os.environ.get("TL_D", "0.01"))
 data = smb.synthetic_dataset(seed=0, n_samples=8 * B, features=layers[0], classes=layers[-1])
 model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=layers, density=d, batch_size=B, lr=0.01))
-st = smb.FusedTrainStep(model, B, pipeline=os.environ.get("TL_PIPE", "0") == "1")
+st = smb.FusedTrainStep(model, B)
 st.attach_dataset(smb.DeviceDataset(data))
 st.set_epoch(np.arange(8 * B))
 for _ in range(6):
