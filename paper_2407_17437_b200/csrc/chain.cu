@@ -381,39 +381,29 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
     ++nprof;
   };
   stamp();
-  if (warp < NPH) {
-    constexpr int kW = (int)sizeof(ChainPhase) / 4;
-    const int* src = reinterpret_cast<const int*>(&P.ph[warp]);
-    int* dst = reinterpret_cast<int*>(&s_ph[warp]);
-    for (int k = lane; k < kW; k += 32) dst[k] = src[k];
-  }
   if (tid == 0) {
 #pragma unroll
     for (int p = 0; p < NPH; ++p) mbar_init(bar0 + 8 * p, 1);
     mbar_init(stage_bar, NPH);  // one arrival per phase's staging thread
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // the targets of the softmax columns (older than the previous kernel), one
-  // class per warp; the zero row of the first transposed product's operand
-  if (warp < P.classes) TT[warp * 32 + lane] = ok ? P.t[warp * P.ld_t + col] : 0.f;
-  if (warp == kChainWarps - 1) D[P.classes * 32 + lane] = 0.f;
-  __syncthreads();
-  // every phase's padded segment bounds for this CTA's rows
-  if (tid < 2 * NPH) s_bnd[tid >> 1][tid & 1] = s_ph[tid >> 1].segb[q + (tid & 1)];
-  __syncthreads();
-  stamp();
-  // stage every phase's padded pointers / indices / values, row order and
-  // bias slice for this CTA's rows with 1-D bulk copies (thread p issues
-  // phase p's; a pointer / order / bias slice is rounded up to 16-byte chunks
-  // where the array allows, its last < 4 words otherwise copied by plain
-  // loads).  Static data and values older than the previous kernel: before
-  // the programmatic-dependency wait.
-  if (tid < NPH) {
-    const int p = tid;
-    const ChainPhase& f = s_ph[p];
+  __syncthreads();  // barriers initialised
+  // Stage every phase's padded pointers / indices / values, row order and
+  // bias slice for this CTA's rows with 1-D bulk copies: lane 0 of warp p
+  // issues phase p's, reading the phase's descriptor from the parameters at
+  // warp-uniform addresses (one constant-cache broadcast per field); a
+  // pointer / order / bias slice is rounded up to 16-byte chunks where the
+  // array allows, its last < 4 words otherwise copied by plain loads.  Static
+  // data and values older than the previous kernel: before the
+  // programmatic-dependency wait.
+  if (warp < NPH && lane == 0) {
+    const int p = warp;
+    const ChainPhase& f = P.ph[p];
     const int r0 = f.split[q], r1 = f.split[q + 1];
     const int pr0 = r0 & ~3;
-    const int a0 = s_bnd[p][0], a1 = s_bnd[p][1];
+    const int a0 = f.segb[q], a1 = f.segb[q + 1];
+    s_bnd[p][0] = a0;
+    s_bnd[p][1] = a1;
     int32_t* sp = reinterpret_cast<int32_t*>(base + f.meta_off);
     int32_t* si = sp + f.ptr_words;
     float* sv = reinterpret_cast<float*>(si + f.nz_words);
@@ -441,6 +431,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(const __grid_co
     }
     mbar_expect_tx(stage_bar, bytes);
   }
+  // the descriptors the main loop reads (lane-parallel copy)
+  if (warp < NPH) {
+    constexpr int kW = (int)sizeof(ChainPhase) / 4;
+    const int* src = reinterpret_cast<const int*>(&P.ph[warp]);
+    int* dst = reinterpret_cast<int*>(&s_ph[warp]);
+    for (int k = lane; k < kW; k += 32) dst[k] = src[k];
+  }
+  // the targets of the softmax columns (older than the previous kernel), one
+  // class per warp; the zero row of the first transposed product's operand
+  if (warp < P.classes) TT[warp * 32 + lane] = ok ? P.t[warp * P.ld_t + col] : 0.f;
+  if (warp == kChainWarps - 1) D[P.classes * 32 + lane] = 0.f;
   stamp();
 
   auto reload = [&](int p) {

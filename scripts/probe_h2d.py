@@ -6,9 +6,16 @@ import time
 sys.path.insert(0, ".")
 import torch
 
+import os
+try:  # the GPU's NUMA-local cores, as bench.py binds them
+    import pynvml
+    pynvml.nvmlInit()
+    pynvml.nvmlDeviceSetCpuAffinity(pynvml.nvmlDeviceGetHandleByIndex(0))
+except Exception as exc:  # (affinity is an optimisation)
+    print("no NVML affinity:", exc)
 x = torch.randn(3072, 1024).pin_memory()
 d = torch.empty(3072, 1024, device="cuda")
-for nst in (1, 2, 4):
+for nst in (1, 2, 3, 4, 8):
     sts = [torch.cuda.Stream() for _ in range(nst)]
     rows = 3072 // nst
     for _ in range(3):
