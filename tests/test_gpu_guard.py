@@ -18,7 +18,8 @@ allocation with a canary band on each side.
 Covered: the row-split SpMM (all lane widths incl. the L2-sliced form), the
 transposed SpMM (CSR and CSC values), the SDDMM + update kernels (small-layer
 pipe, mid-size, many-wave warp kernel), the dense output-layer kernels, the
-batch gather and the fused training step.
+batch gather, the column-chain kernel (TMA reloads, cluster barriers,
+distributed shared memory, bulk-copy staging) and the fused training step.
 """
 
 import numpy as np
@@ -71,6 +72,10 @@ class Guarded:
 
     def bands_intact(self):
         return np.array_equal(self.bands(), self.band_before)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
 
 
 def _run_twice_each(fn, make):
@@ -188,3 +193,81 @@ def test_gather_stays_in_bounds():
 
     out = _run_twice_each(fn, make)
     assert bits_equal(out["dst"], src[perm[1000:1000 + B]].T)
+
+
+@pytest.mark.parametrize("B", [1024, 100])
+def test_chain_kernel_stays_in_bounds_and_reproduces(B):
+    """The column-chain launch (smb_chain_run) with every activation /
+    gradient / target / loss / workspace buffer inside canary bands: no band
+    written, NaN vs zero bands identical, repeated runs identical, and the
+    results equal the separate kernels' (smb_spmm_p, smb_softmax_ce_grad,
+    smb_spmm_t_csc)."""
+    import ctypes as C
+
+    dims = [3072, 1024, 512, 10]
+    model, _ = smb.build_model(smb.ExperimentConfig(layer_dims=dims, density=0.01, seed=7,
+                                                    batch_size=B))
+    layers = [l for l in model.layers if isinstance(l, smb.SparseLinearLayer)]
+    L = len(layers)
+    ld = (B + 3) // 4 * 4
+    rng = np.random.default_rng(B)
+    a0 = np.zeros((dims[1], ld), np.float32)
+    a0[:, :B] = np.maximum(rng.standard_normal((dims[1], B)), 0).astype(np.float32)
+    t = np.zeros((dims[-1], ld), np.float32)
+    t[rng.integers(0, dims[-1], B), np.arange(B)] = 1
+    lib = _lib.load()
+    pats = (C.c_void_p * L)(*[l.weights.pattern.handle for l in layers])
+    relu = (C.c_int * L)(1, 1, 0)
+    h = C.c_void_p()
+    _lib.check(lib.smb_chain_plan_create(L, pats, relu, B, ld, C.byref(h)))
+    st = stream_ptr()
+    try:
+        for li in range(1, L):
+            _lib.call("smb_chain_refresh", h.value, li, ptr(layers[li].weights.values), st)
+        ws_words = int(lib.smb_chain_workspace_bytes(B)) // 4 + 1
+
+        def make(nan):
+            b = {"a0": Guarded(a0, nan), "t": Guarded(t, nan),
+                 "loss": Guarded(np.zeros(2, np.float32), nan),
+                 "ws": Guarded(np.zeros(ws_words, np.float32), False)}
+            for li in range(1, L):
+                b[f"a{li}"] = Guarded(np.zeros((dims[li + 1], ld), np.float32), nan)
+            for li in range(L):
+                b[f"d{li}"] = Guarded(np.zeros((dims[li + 1], ld), np.float32), nan)
+            return b
+
+        def fn(b):
+            arr = C.c_void_p * L
+            acts = arr(*[b[f"a{li}"].p for li in range(L)])
+            dys = arr(*[b[f"d{li}"].p for li in range(L)])
+            bias = arr(*[ptr(l.bias) for l in layers])
+            _lib.call("smb_chain_run", h.value, bias, acts, dys, b["t"].p, ld, float(B),
+                      b["loss"].p, b["ws"].p, st)
+
+        out = _run_twice_each(fn, make)
+    finally:
+        lib.smb_chain_plan_destroy(h.value)
+    # the separate kernels on plain buffers
+    F32 = _lib.SMB_F32
+    a = [torch.from_numpy(a0).cuda()] + [torch.zeros((d, ld), device="cuda") for d in dims[2:]]
+    dy = [torch.zeros((d, ld), device="cuda") for d in dims[1:]]
+    tt = torch.from_numpy(t).cuda()
+    for li in range(1, L):
+        lay = layers[li]
+        _lib.call("smb_spmm_p", F32, lay.weights.pattern.handle, ptr(lay.weights.values),
+                  ptr(a[li - 1]), ld, B, ptr(lay.bias),
+                  _lib.SMB_EPI_RELU if li < L - 1 else _lib.SMB_EPI_NONE, ptr(a[li]), ld, st)
+    _lib.call("smb_softmax_ce_grad", F32, ptr(a[L - 1]), ld, ptr(tt), ld, dims[-1], B, float(B),
+              ptr(dy[L - 1]), ld, None, st)
+    for li in range(L - 1, 0, -1):
+        lay = layers[li]
+        vcsc = torch.empty_like(lay.weights.values)
+        _lib.call("smb_values_to_csc", F32, lay.weights.pattern.handle, ptr(lay.weights.values),
+                  ptr(vcsc), st)
+        _lib.call("smb_spmm_t_csc", F32, lay.weights.pattern.handle, ptr(vcsc), ptr(dy[li]), ld,
+                  B, ptr(a[li - 1]), ld, ptr(dy[li - 1]), ld, st)
+    torch.cuda.synchronize()
+    for li in range(1, L):
+        assert bits_equal(out[f"a{li}"][:, :B], host(a[li])[:, :B]), f"a{li}"
+    for li in range(L):
+        assert bits_equal(out[f"d{li}"][:, :B], host(dy[li])[:, :B]), f"d{li}"
