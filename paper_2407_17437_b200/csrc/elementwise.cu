@@ -711,9 +711,10 @@ struct DenseFwdPlan {
 inline DenseFwdPlan dense_fwd_plan(int64_t k, int64_t n, int cw = 4) {
   DenseFwdPlan p;
   p.col_blocks = ceil_div(n > 0 ? n : 1, kDfCols * cw);
-  // ~256 CTAs (16 x loads of 16 bytes in flight per thread keep HBM busy),
+  // ~1024 CTAs (7 resident per SM, 16 x loads of 16 bytes in flight per
+  // thread keep HBM busy; 256 CTAs left config 5's 134 MB x at 25% of HBM),
   // slices of >= 64 rows so the partial sums stay small next to x
-  int64_t s = ceil_div(256, p.col_blocks);
+  int64_t s = ceil_div(1024, p.col_blocks);
   s = imax(1, imin(s, ceil_div(k > 0 ? k : 1, cw > 1 ? 64 : 32)));
   p.ks = ceil_div(ceil_div(k > 0 ? k : 1, s), 32) * 32;
   // the W^T slice lives in shared memory (ks x 32 padded rows x 8 bytes at
@@ -804,26 +805,44 @@ __global__ void __launch_bounds__(kDfCols)
     }
 }
 
+// y[i, t] = bias[i] + sum of the slices' partials: a CTA = 32 consecutive
+// outputs x 32 slice groups; group g sums slices g, g + 32, ... in order
+// (coalesced over the outputs), then the 32 group sums are added in a fixed
+// pairwise tree (deterministic).
+constexpr int kDfSumG = 32;
+
 template <typename T>
-__global__ void dense_fwd_sum_kernel(const T* __restrict__ part, int64_t slices, int64_t m,
-                                     int64_t n, const T* __restrict__ bias, T* __restrict__ y,
-                                     int64_t ld_y) {
+__global__ void __launch_bounds__(32 * kDfSumG)
+    dense_fwd_sum_kernel(const T* __restrict__ part, int64_t slices, int64_t m, int64_t n,
+                         const T* __restrict__ bias, T* __restrict__ y, int64_t ld_y) {
+  __shared__ T s_acc[kDfSumG][33];
   pdl_wait();
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m * n) return;
-  const int64_t i = e / n, t = e - i * n;
+  const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + c;
   const int64_t mn = m * n;
-  T acc = part[e];
-  int64_t s = 1;
-  for (; s + 16 <= slices; s += 16) {  // 16 loads in flight, summed in slice order
-    T v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = part[(s + u) * mn + e];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) acc += v[u];
+  T acc = T(0);
+  if (e < mn) {
+    int64_t s = g;
+    for (; s + 3 * kDfSumG < slices; s += 4 * kDfSumG) {  // 4 loads in flight
+      const T v0 = part[s * mn + e], v1 = part[(s + kDfSumG) * mn + e],
+              v2 = part[(s + 2 * kDfSumG) * mn + e], v3 = part[(s + 3 * kDfSumG) * mn + e];
+      acc += v0;
+      acc += v1;
+      acc += v2;
+      acc += v3;
+    }
+    for (; s < slices; s += kDfSumG) acc += part[s * mn + e];
   }
-  for (; s < slices; ++s) acc += part[s * mn + e];
-  y[i * ld_y + t] = (bias ? bias[i] : T(0)) + acc;
+  s_acc[g][c] = acc;
+  __syncthreads();
+  for (int h = kDfSumG / 2; h >= 1; h >>= 1) {
+    if (g < h) s_acc[g][c] += s_acc[g + h][c];
+    __syncthreads();
+  }
+  if (g == 0 && e < mn) {
+    const int64_t i = e / n, t = e - i * n;
+    y[i * ld_y + t] = (bias ? bias[i] : T(0)) + s_acc[0][c];
+  }
 }
 }  // namespace
 }  // namespace smb
@@ -879,7 +898,7 @@ extern "C" int smb_dense_forward_small(int dtype, const void* w, int64_t ld_w, i
       else
         go(dense_fwd_part_kernel<T, 0, 1>);
     }
-    launch_k(dense_fwd_sum_kernel<T>, dim3((unsigned)ceil_div(m * n, 256)), dim3(256), 0,
+    launch_k(dense_fwd_sum_kernel<T>, dim3((unsigned)ceil_div(m * n, 32)), dim3(32 * kDfSumG), 0,
              as_stream(stream), static_cast<const T*>(part), k == 0 ? int64_t(1) : p.slices,
              m, n, static_cast<const T*>(bias), static_cast<T*>(y), ld_y);
     return check_launch("smb_dense_forward_small");
