@@ -9,7 +9,7 @@ timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/
 timeout 1200 python bench.py --layers 3072,8192,8192,8192,10 --density 0.01 --batch 1024 --steps 200 --cpu-seconds 20 > gpurun_out/bench_cfg4.log 2>&1; echo "exit $?" >> gpurun_out/bench_cfg4.log
 timeout 1500 python bench.py --layers 3072,65536,65536,10 --density 0.001 --batch 512 --steps 100 --cpu-seconds 20 > gpurun_out/bench_cfg5.log 2>&1; echo "exit $?" >> gpurun_out/bench_cfg5.log
 timeout 900 python scripts/kernel_bench.py > gpurun_out/kernel_bench.log 2>&1; echo "exit $?" >> gpurun_out/kernel_bench.log
-bash scripts/gpu_profile_step.sh r02c_cfg2 3072,1024,512,10 0.01 1024 > gpurun_out/prof.log 2>&1
+bash scripts/gpu_profile_step.sh r02d_cfg2 3072,1024,512,10 0.01 1024 > gpurun_out/prof.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log
 for f in bench bench_cfg4 bench_cfg5; do grep "^{" gpurun_out/$f.log | python -c "
 import sys, json
