@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(THREADS)
                int ld, float* __restrict__ y, int rs) {
   constexpr int Q = BS / 4;             // quads per row
   constexpr int RPP = THREADS / Q;      // rows per pass
-  constexpr int LDX = BS + (BS == 32 ? 0 : 4) ;  // padding breaks row-bank aliasing
+  constexpr int LDX = BS + ((BS == 32 || BS == 4) ? 0 : 4);  // padding breaks row-bank aliasing
   extern __shared__ __align__(16) float xs[];
   const int slice = blockIdx.x / rs, split = blockIdx.x % rs;
   const int c0 = slice * BS;
@@ -95,8 +95,30 @@ __global__ void spmm_ref(const int* row_ptr, const int* col_idx, const float* va
   y[(size_t)i * ld + t] = acc;
 }
 
+static float* g_flush = nullptr;
+static bool g_flushed = false;
 template <typename F>
 float time_us(F f, int reps = 50) {
+  if (g_flushed) {  // L2 flushed before every launch, each launch timed alone
+    if (!g_flush) CK(cudaMalloc(&g_flush, 512u << 20));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    for (int i = 0; i < 3; ++i) f();
+    float tot = 0.f;
+    for (int i = 0; i < 20; ++i) {
+      CK(cudaMemsetAsync(g_flush, i, 512u << 20));
+      CK(cudaEventRecord(a));
+      f();
+      CK(cudaEventRecord(b));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      tot += ms;
+    }
+    CK(cudaGetLastError());
+    return tot * 1e3f / 20;
+  }
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
@@ -120,7 +142,7 @@ struct Shape {
 template <int BS, int TH>
 void run(const Shape& s, const int* rp, const int* ci, const float* v, const float* x, float* y,
          const float* yref, int n, int rs) {
-  constexpr int LDX = BS + (BS == 32 ? 0 : 4);
+  constexpr int LDX = BS + ((BS == 32 || BS == 4) ? 0 : 4);
   const size_t smem = (size_t)s.k * LDX * 4;
   if (smem > 227 * 1024) return;
   auto kern = spmm_slice<BS, TH>;
@@ -138,13 +160,20 @@ void run(const Shape& s, const int* rp, const int* ci, const float* v, const flo
          rs, grid, smem / 1024, us, bad);
 }
 
-int main() {
-  const int n = 1024;
-  Shape shapes[] = {{"c2.L0 1024x3072 r24", 1024, 3072, 24},
+int main(int argc, char** argv) {
+  // optional: m k r n [flushed]  (e.g. the config-3 point 8192 8192 8 512 1)
+  const int n = argc >= 5 ? atoi(argv[4]) : 1024;
+  g_flushed = argc >= 6 && atoi(argv[5]) != 0;
+  std::vector<Shape> shapes;
+  if (argc >= 5) {
+    shapes.push_back({"argv", atoi(argv[1]), atoi(argv[2]), atoi(argv[3])});
+  } else {
+    shapes = {{"c2.L0 1024x3072 r24", 1024, 3072, 24},
                     {"c2.L1 512x1024 r18", 512, 1024, 18},
                     {"c2.L2 10x512 r312", 10, 512, 312},
                     {"c4.L1 8192x8192 r69", 8192, 8192, 69},
                     {"c4.L0 8192x3072 r47", 8192, 3072, 47}};
+  }
   std::mt19937 rng(1);
   std::normal_distribution<float> nd;
   for (const Shape& s : shapes) {
@@ -179,6 +208,8 @@ int main() {
     CK(cudaDeviceSynchronize());
     printf("%s nnz=%d (x-gather %.1f MB)\n", s.name, nnz, nnz * 4.0 * n / 1e6);
     for (int rs : {1, 2, 4}) {
+      run<4, 512>(s, d_rp, d_ci, d_v, d_x, d_y, d_yref, n, rs);
+      run<4, 1024>(s, d_rp, d_ci, d_v, d_x, d_y, d_yref, n, rs);
       run<4, 256>(s, d_rp, d_ci, d_v, d_x, d_y, d_yref, n, rs);
       run<8, 256>(s, d_rp, d_ci, d_v, d_x, d_y, d_yref, n, rs);
       run<16, 256>(s, d_rp, d_ci, d_v, d_x, d_y, d_yref, n, rs);
