@@ -371,7 +371,8 @@ def test_sddmm_many_waves_long_rows_bit_exact(oracle, n):
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("m,k,n", [(10, 512, 1024), (10, 8192, 100), (1, 7, 3), (32, 300, 257),
-                                   (17, 1000, 1)])
+                                   (17, 1000, 1), (10, 4099, 512), (32, 1000, 64), (5, 77, 12),
+                                   (10, 20000, 4)])
 @pytest.mark.parametrize("with_mask", [True, False])
 def test_dense_backward_input_sequential_sum(dtype, m, k, n, with_mask):
     """smb_dense_backward_input: W^T d summed over ascending rows with
