@@ -34,6 +34,8 @@
 // (sddmm_tma_supported); the caller falls back to sddmm.cu otherwise.
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "pattern.cuh"
 #include "tma.cuh"
 
@@ -179,20 +181,31 @@ __global__ void __launch_bounds__(32 * WPC)
   const bool upd = active && opt.kind != SMB_OPT_NONE;
   float w_pre = upd ? values[p] : 0.f;
   float v_pre = (upd && velocity) ? velocity[p] : 0.f;
+  // two copy sites so that each one's tensor map is a uniform operand (the
+  // row coordinates are data: ptxas moves them to uniform registers in an
+  // ELECT / R2UR loop, one pass per copying lane)
   auto issue = [&](int ch) {
     const int s = ch % S;
     const unsigned bar = smem_addr(&s_full[warp][s]);
     if (lane == 0) mbar_arrive_expect_tx(bar, tx_bytes);
     __syncwarp();
-    if (copier)
-      tma_gather4(lane < 8 ? base + (unsigned)(s * kTmaXBytes + lane * 512)
-                           : dbase + (unsigned)(s * kTmaDBytes + (lane - 8) * 512),
-                  lane < 8 ? &xmap : &dmap, ch * 32, gr[0], gr[1], gr[2], gr[3], bar);
+    if (lane < 8)
+      tma_gather4(base + (unsigned)(s * kTmaXBytes + lane * 512), &xmap, ch * 32, gr[0], gr[1],
+                  gr[2], gr[3], bar);
+    else if (copier)
+      tma_gather4(dbase + (unsigned)(s * kTmaDBytes + (lane - 8) * 512), &dmap, ch * 32, gr[0],
+                  gr[1], gr[2], gr[3], bar);
   };
   for (int c = 0; c < S && c < n_chunks; ++c) issue(c);
   float acc = -0.0f;  // exact additive identity (sddmm.cu)
   const float* drow = d_out + row * ld_d;
   const int xsw = lane & 7;  // swizzle of this lane's x row (1024-aligned x blocks)
+  // the chunk loop is instantiated per staging mode (warp-uniform): as one
+  // loop with `staged` tested inside, ptxas predicated the 32 global d_out
+  // loads of the fallback into the staged path (issue slots spent on
+  // masked-off instructions)
+  auto run = [&](auto staged_c) {
+  constexpr bool kStaged = decltype(staged_c)::value;
   for (int ch = 0; ch < n_chunks; ++ch) {
     const int s = ch % S;
     mbar_wait(smem_addr(&s_full[warp][s]), (unsigned)((ch / S) & 1));
@@ -207,7 +220,7 @@ __global__ void __launch_bounds__(32 * WPC)
       for (int u = 0; u < 8; ++u) {
         const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * (u ^ xsw));
         float4 dv;
-        if (staged) {
+        if constexpr (kStaged) {
           dv = *reinterpret_cast<const float4*>(dr + 4 * (u ^ dsw));
         } else {
           dv = make_float4(drow[t0 + 4 * u], drow[t0 + 4 * u + 1], drow[t0 + 4 * u + 2],
@@ -222,13 +235,18 @@ __global__ void __launch_bounds__(32 * WPC)
       for (int j = 0; j < cnt; ++j) {
         const int u = j >> 2, e = j & 3;
         const float xv = xr[4 * (u ^ xsw) + e];
-        const float dv = staged ? dr[4 * (u ^ dsw) + e] : drow[t0 + j];
+        const float dv = kStaged ? dr[4 * (u ^ dsw) + e] : drow[t0 + j];
         acc = add_rn(acc, mul_rn(dv, xv));
       }
     }
     __syncwarp();  // every lane has read stage s: refill it
     if (ch + S < n_chunks) issue(ch + S);
   }
+  };
+  if (staged)
+    run(std::true_type{});
+  else
+    run(std::false_type{});
   pdl_trigger();
   if (!active) return;
   const float g = (n == 0) ? 0.f : acc;  // tensor_core.py:283-284: zero batch -> zeros
