@@ -6,9 +6,10 @@
 // nn.py:187-197), with the staging done by the Tensor Memory Accelerator
 // instead of per-thread cp.async:
 //
-//   * each warp owns 32 consecutive nonzeros (CSR order) and a private ring
-//     of S stages; a stage holds the 32 gathered x-row segments of one
-//     32-column batch chunk plus up to 4 d_out rows the warp's nonzeros span;
+//   * one warp per CTA owns 32 consecutive nonzeros (CSR order, or the
+//     pattern's L2-blocked order) and a private ring of 2 stages; a stage holds
+//     the 32 gathered x-row segments of one 32-column batch chunk plus the
+//     (up to DS) d_out rows the warp's nonzeros span;
 //   * 9 lanes fill a stage with ONE `cp.async.bulk.tensor.2d.tile::gather4`
 //     each (4 arbitrary rows x 128 bytes per instruction, SASS
 //     UTMALDG.2D.GATHER4) and the stage's mbarrier counts the bytes in
@@ -21,14 +22,26 @@
 //     without padding, unlike the 144-byte padded rows of cp.async staging
 //     that split sectors on the global side).
 //
-// Measured (ncu, config-4 hidden layer): the chains now leave the SM issue
-// bound (78% of peak instruction throughput), and 30% of the issued
-// instructions are the copy issue itself: the gather4 row coordinates are
-// data (col_idx), so ptxas moves them into uniform registers through an
-// ELECT / R2UR.BROADCAST loop per instruction.  Issuing all 9 copies from one
-// lane with the same coordinates is slower (232 vs 211 us: one thread then
-// serialises the 9 loops); one warp per CTA with a 2-stage ring (22 resident
-// warps per SM) beat 2-4 warps per CTA and 3-8 stages.
+// The kernel is bound by instruction issue and by how many warps (rings) an
+// SM holds, so both were trimmed (config-4 hidden layer, graph-timed):
+//   215 us  first version: one chunk loop with `staged` tested inside (ptxas
+//           predicated the fallback's 32 global d_out loads into the staged
+//           path: issue slots spent on masked-off instructions), one copy site
+//           choosing its tensor map per lane;
+//   178 us  the chunk loop instantiated per staging mode, one copy site per
+//           tensor map (uniform map operand);
+//   161 us  the chunk loop unrolled over the ring stages (every shared-memory
+//           address a register plus an immediate);
+//   149 us  no static shared memory and no alignment slack: 9.4 KB per CTA,
+//           21 resident warps per SM instead of 18.
+// The copy issue is still ~90 of the ~200 instructions per chunk: the gather4
+// row coordinates are data (col_idx), so ptxas moves them into uniform
+// registers through an ELECT / R2UR.BROADCAST loop, ~10 issue slots per copy
+// (a single elected lane holding every coordinate needs as many: the R2URs
+// and the UMOVs that line up the operand registers).  Measured and dropped:
+// two chains per lane sharing each staged d_out chunk (K = 2: half the warps
+// per SM, 221 us), 8 staged d_out rows (DS = 8: 162 us), 3 stages (204 us),
+// 2-4 warps per CTA.
 //
 // Valid for fp32 with 16-byte aligned operands and leading dimensions
 // (sddmm_tma_supported); the caller falls back to sddmm.cu otherwise.
@@ -41,17 +54,6 @@
 
 namespace smb {
 namespace {
-
-constexpr int kTmaXBytes = 32 * 128;  // x rows of one stage (1024-byte aligned blocks)
-// d_out rows staged per stage: 4 (one gather4) in CSR order, 8 (two) in the
-// blocked order, where a warp's 32 nonzeros span more rows
-// shared memory of one warp's ring: S x-blocks, then S d-blocks, rounded to
-// the 1024-byte swizzle atom (the hardware swizzle follows address bits
-// 7-9, so 512-byte aligned gather4 destinations are fine)
-template <int S, int DS>
-__host__ __device__ constexpr int warp_ring_bytes() {
-  return (S * (kTmaXBytes + DS * 128) + 1023) / 1024 * 1024;
-}
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -84,177 +86,272 @@ __device__ __forceinline__ void tma_gather4(unsigned dst, const CUtensorMap* map
       : "memory");
 }
 
-// ORD: the warps walk the pattern's L2-blocked nonzero order (ord_p /
-// ord_row, pattern.cu) instead of CSR order: a wave of resident warps then
-// gathers the x and d_out rows of one (row band, column band) block, so each
-// row segment is fetched from HBM about once per block instead of once per
-// wave (config 5 at B = 4096: x and d_out are 1 GB each).  The chains, their
-// order over the batch and the update are unchanged; results land at the
-// nonzero's CSR index.
-template <int S, int WPC, bool ORD, int DS = ORD ? 8 : 4>
-__global__ void __launch_bounds__(32 * WPC)
-    sddmm_tma_kernel(const __grid_constant__ CUtensorMap xmap,
-                     const __grid_constant__ CUtensorMap dmap, const int32_t* __restrict__ row_ptr,
-                     const int32_t* __restrict__ col_idx, const int32_t* __restrict__ tile_row0,
-                     const int32_t* __restrict__ ord_p, const int32_t* __restrict__ ord_row,
-                     int64_t m, int64_t nnz, const float* __restrict__ d_out, int64_t ld_d, int n,
-                     const float* values, float* values_out, float* velocity, float* grad_out,
-                     OptConsts<float> opt) {
-  constexpr int kTile = 32 * WPC;  // nonzeros per CTA (a multiple of the tile_row0 grain)
+// K chains per lane (K = 1, 2): lane l owns the K consecutive nonzeros
+// K*l .. K*l+K-1 of the warp's 32*K, which mostly lie in one row of the
+// pattern, so the lane reads each staged d_out chunk once for all of them
+// (per pair: 4 bytes of x written by the TMA + 4 read + 4/K of d_out read from
+// shared memory, the resource the one-chain kernel saturates together with
+// the issue slots).  Nonzero K*l+e is staged at shared-memory row 32*e + l:
+// every quarter-warp still reads 8 consecutive 128-byte rows, conflict-free
+// under the 128-byte swizzle.  The chunk loop is unrolled over the S ring
+// stages, so every shared-memory address is a register plus an immediate.
+template <int S, bool ORD, int K, int DS>
+__global__ void __launch_bounds__(32)
+    sddmm_tmak_kernel(const __grid_constant__ CUtensorMap xmap,
+                      const __grid_constant__ CUtensorMap dmap,
+                      const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                      const int32_t* __restrict__ tile_row0, const int32_t* __restrict__ ord_p,
+                      const int32_t* __restrict__ ord_row, int64_t m, int64_t nnz,
+                      const float* __restrict__ d_out, int64_t ld_d, int n, const float* values,
+                      float* values_out, float* velocity, float* grad_out, OptConsts<float> opt) {
+  constexpr int kTile = 32 * K;
+  constexpr int kXBytes = kTile * 128;
+  constexpr int kDBytes = DS * 128;
+  static_assert(kTile % kTileGrain == 0 && DS % 4 == 0 && DS <= 8 && 4 * K + DS / 4 <= 32, "");
+  // No static shared memory: the dynamic block then starts at the CTA's
+  // 1024-byte aligned window base (checked), so the ring needs no alignment
+  // slack and the barriers / row window live behind it -- 9.5 KB per CTA at
+  // K = 1, 21 resident warps per SM instead of 18.
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ int32_t s_rp[kTile + 1];
-  __shared__ __align__(8) unsigned long long s_full[WPC][S];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // dynamic smem rounded up to 1024 bytes (the 128-byte swizzle atom)
-  const unsigned raw = smem_addr(smem_raw);
-  const unsigned base = ((raw + 1023u) & ~1023u) + (unsigned)(warp * warp_ring_bytes<S, DS>());
-  const unsigned dbase = base + S * kTmaXBytes;
-  const unsigned char* gbase = smem_raw + (base - raw);
-  const int64_t p0 = (int64_t)blockIdx.x * kTile;
-  const int64_t pw = p0 + warp * 32;
-  const int nw = (int)imax(0, imin(32, nnz - pw));
-  const bool active = lane < nw;
-  // p: the CSR index of this lane's nonzero
-  const int64_t p = ORD ? (active ? (int64_t)ord_p[pw + lane] : 0) : pw + lane;
+  constexpr int kRing = S * (kXBytes + kDBytes);
+  unsigned long long* s_full = reinterpret_cast<unsigned long long*>(smem_raw + kRing);
+  int64_t* s_slot_row = reinterpret_cast<int64_t*>(smem_raw + kRing + 8 * S);
+  int32_t* s_rp = reinterpret_cast<int32_t*>(smem_raw + kRing + 8 * S + 8 * DS);
+  const int lane = threadIdx.x;
+  const unsigned base = smem_addr(smem_raw);  // x blocks, then d blocks
+  if (base & 1023u) __trap();
+  const unsigned dbase = base + S * kXBytes;
+  const unsigned char* gbase = smem_raw;
+  const unsigned bar0 = smem_addr(s_full);
+  const int64_t pw = (int64_t)blockIdx.x * kTile;
+  const int nw = (int)imax(0, imin(kTile, nnz - pw));
+  bool act[K];
+  int64_t p[K];
+  int32_t col[K];
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    act[e] = K * lane + e < nw;
+    p[e] = ORD ? (act[e] ? (int64_t)ord_p[pw + K * lane + e] : 0) : pw + K * lane + e;
+  }
   int32_t r0 = 0;
   if constexpr (!ORD) {
     r0 = tile_row0[(int64_t)blockIdx.x * (kTile / kTileGrain)];
-    s_rp[tid] = (r0 + tid <= m) ? row_ptr[r0 + tid] : INT32_MAX;
-    if (tid == 0) s_rp[kTile] = (r0 + kTile <= m) ? row_ptr[r0 + kTile] : INT32_MAX;
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      const int i = lane + 32 * e;
+      s_rp[i] = (r0 + i <= m) ? row_ptr[r0 + i] : INT32_MAX;
+    }
+    if (lane == 0) s_rp[kTile] = (r0 + kTile <= m) ? row_ptr[r0 + kTile] : INT32_MAX;
   }
-  const int32_t my_col = active ? col_idx[p] : 0;
+#pragma unroll
+  for (int e = 0; e < K; ++e) col[e] = act[e] ? col_idx[p[e]] : 0;
   if (lane == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(smem_addr(&s_full[warp][s]), 1);
+    for (int s = 0; s < S; ++s) mbar_init(bar0 + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();  // the only CTA-wide barrier (row window + barrier init)
+  __syncthreads();
   if (nw == 0) return;
-  int64_t row;
-  int slot, n_slots;
-  constexpr int kTmaDSlots = DS;
-  constexpr int kTmaDBytes = DS * 128;
-  int64_t slot_row[kTmaDSlots];
+  int64_t row[K];
+  int slot[K];
+  int n_slots;
+  int64_t slot_row[DS];
   if constexpr (ORD) {
-    // d_out slots = runs of equal rows among the warp's nonzeros (rows are
-    // non-decreasing inside a block)
-    row = active ? (int64_t)ord_row[pw + lane] : (int64_t)ord_row[pw];
-    const int64_t prev = __shfl_up_sync(0xffffffffu, row, 1);
-    const unsigned runs = __ballot_sync(0xffffffffu, active && (lane == 0 || row != prev));
-    slot = __popc(runs & (0xffffffffu >> (31 - lane))) - 1;
-    n_slots = __popc(runs);
-    unsigned rest = runs;
+    // d_out slots = runs of equal rows in the warp's nonzero order
+    bool head[K];
+    unsigned heads[K];
 #pragma unroll
-    for (int q = 0; q < kTmaDSlots; ++q) {
-      const int src = rest ? __ffs(rest) - 1 : 0;
-      const int64_t r = __shfl_sync(0xffffffffu, row, src);
-      slot_row[q] = rest ? r : (q > 0 ? slot_row[q - 1] : r);
-      rest &= rest - 1;
+    for (int e = 0; e < K; ++e)
+      row[e] = act[e] ? (int64_t)ord_row[pw + K * lane + e] : (int64_t)ord_row[pw];
+    const int64_t prev_lane = __shfl_up_sync(0xffffffffu, row[K - 1], 1);
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      const int64_t prev = e == 0 ? prev_lane : row[e - 1];
+      head[e] = act[e] && ((lane == 0 && e == 0) || row[e] != prev);
+      heads[e] = __ballot_sync(0xffffffffu, head[e]);
     }
-  } else {
-    row = tile_row_of<kTile>(active ? p : pw, r0, s_rp, row_ptr, m);
-    const int64_t row_first = __shfl_sync(0xffffffffu, row, 0);
-    const int64_t row_last = __shfl_sync(0xffffffffu, row, nw - 1);
-    n_slots = (int)(row_last - row_first + 1);
-    slot = (int)(row - row_first);
+    // runs started before this lane, then inside it
+    int before = 0;
+    n_slots = 0;
 #pragma unroll
-    for (int q = 0; q < kTmaDSlots; ++q) slot_row[q] = imin(row_first + imin(q, n_slots - 1), m - 1);
+    for (int e = 0; e < K; ++e) {
+      before += __popc(heads[e] & ((1u << lane) - 1u));
+      n_slots += __popc(heads[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      before += head[e] ? 1 : 0;
+      slot[e] = before - 1;
+    }
+    if (lane < DS) s_slot_row[lane] = row[0];  // filler: any valid row
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < K; ++e)
+      if (head[e] && slot[e] < DS) s_slot_row[slot[e]] = row[e];
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < DS; ++q) slot_row[q] = s_slot_row[q];
+  } else {
+#pragma unroll
+    for (int e = 0; e < K; ++e)
+      row[e] = tile_row_of<kTile>(act[e] ? p[e] : pw, r0, s_rp, row_ptr, m);
+    const int64_t row_first = __shfl_sync(0xffffffffu, row[0], 0);
+    int64_t row_last = row_first;
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      const int64_t r = __shfl_sync(0xffffffffu, row[e], (nw - 1) / K);
+      if ((nw - 1) % K == e) row_last = r;
+    }
+    n_slots = (int)(row_last - row_first + 1);
+#pragma unroll
+    for (int e = 0; e < K; ++e) slot[e] = (int)(row[e] - row_first);
+#pragma unroll
+    for (int q = 0; q < DS; ++q) slot_row[q] = imin(row_first + imin(q, n_slots - 1), m - 1);
   }
-  const bool staged = n_slots <= kTmaDSlots;  // warp-uniform
+  const bool staged = n_slots <= DS;  // warp-uniform
   const int n_chunks = (n + 31) / 32;
-  // copy roles: lane g < 8 gathers x rows 4g..4g+3, lane 8 the d_out rows
+  // copy roles: lane g < 8K gathers the shared-memory rows 4g..4g+3 (nonzero
+  // K*l+e sits at row 32e + l), lanes 8K.. the staged d_out rows
   int gr[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int src = (lane < 8) ? 4 * lane + q : 0;
-    gr[q] = __shfl_sync(0xffffffffu, my_col, src);
+    const int src = 4 * (lane & 7) + q;
+    int v = 0;
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      const int c = __shfl_sync(0xffffffffu, col[e], src);
+      if ((lane >> 3) == e) v = c;
+    }
+    gr[q] = v;
   }
-  // lanes 8 (and 9) gather the staged d_out rows 0-3 (4-7)
 #pragma unroll
   for (int g = 0; g < DS / 4; ++g)
-    if (lane == 8 + g) {
+    if (lane == 8 * K + g) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) gr[q] = (int)slot_row[4 * g + q];
     }
-  const bool copier = lane < 8 || (staged && lane < 8 + DS / 4);
-  const unsigned tx_bytes = 32 * 128 + (staged ? kTmaDSlots * 128 : 0);
+  const bool dcopier = staged && lane >= 8 * K && lane < 8 * K + DS / 4;
+  const unsigned tx_bytes = kXBytes + (staged ? kDBytes : 0);
   pdl_wait();  // d_out / x are earlier kernels' outputs
-  const bool upd = active && opt.kind != SMB_OPT_NONE;
-  float w_pre = upd ? values[p] : 0.f;
-  float v_pre = (upd && velocity) ? velocity[p] : 0.f;
-  // two copy sites so that each one's tensor map is a uniform operand (the
-  // row coordinates are data: ptxas moves them to uniform registers in an
-  // ELECT / R2UR loop, one pass per copying lane)
-  auto issue = [&](int ch) {
-    const int s = ch % S;
-    const unsigned bar = smem_addr(&s_full[warp][s]);
+  const bool has_opt = opt.kind != SMB_OPT_NONE;
+  float w_pre[K], v_pre[K], acc[K];
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    const bool upd = act[e] && has_opt;
+    w_pre[e] = upd ? values[p[e]] : 0.f;
+    v_pre[e] = (upd && velocity) ? velocity[p[e]] : 0.f;
+    acc[e] = -0.0f;  // exact additive identity (sddmm.cu)
+  }
+  auto issue = [&](int ch, int s) {
+    const unsigned bar = bar0 + 8 * s;
     if (lane == 0) mbar_arrive_expect_tx(bar, tx_bytes);
     __syncwarp();
-    if (lane < 8)
-      tma_gather4(base + (unsigned)(s * kTmaXBytes + lane * 512), &xmap, ch * 32, gr[0], gr[1],
+    if (lane < 8 * K)
+      tma_gather4(base + (unsigned)(s * kXBytes + lane * 512), &xmap, ch * 32, gr[0], gr[1],
                   gr[2], gr[3], bar);
-    else if (copier)
-      tma_gather4(dbase + (unsigned)(s * kTmaDBytes + (lane - 8) * 512), &dmap, ch * 32, gr[0],
+    else if (dcopier)
+      tma_gather4(dbase + (unsigned)(s * kDBytes + (lane - 8 * K) * 512), &dmap, ch * 32, gr[0],
                   gr[1], gr[2], gr[3], bar);
   };
-  for (int c = 0; c < S && c < n_chunks; ++c) issue(c);
-  float acc = -0.0f;  // exact additive identity (sddmm.cu)
-  const float* drow = d_out + row * ld_d;
-  const int xsw = lane & 7;  // swizzle of this lane's x row (1024-aligned x blocks)
-  // the chunk loop is instantiated per staging mode (warp-uniform): as one
-  // loop with `staged` tested inside, ptxas predicated the 32 global d_out
-  // loads of the fallback into the staged path (issue slots spent on
-  // masked-off instructions)
-  auto run = [&](auto staged_c) {
-  constexpr bool kStaged = decltype(staged_c)::value;
-  for (int ch = 0; ch < n_chunks; ++ch) {
-    const int s = ch % S;
-    mbar_wait(smem_addr(&s_full[warp][s]), (unsigned)((ch / S) & 1));
-    const float* xr = reinterpret_cast<const float*>(gbase + s * kTmaXBytes + lane * 128);
-    const unsigned doff = S * kTmaXBytes + s * kTmaDBytes + slot * 128;
-    const float* dr = reinterpret_cast<const float*>(gbase + doff);
-    const int dsw = (int)(((base + doff) >> 7) & 7);  // swizzle of this lane's d_out row
-    const int t0 = ch * 32;
-    const int cnt = min(32, n - t0);
-    if (cnt == 32) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * (u ^ xsw));
-        float4 dv;
-        if constexpr (kStaged) {
-          dv = *reinterpret_cast<const float4*>(dr + 4 * (u ^ dsw));
+  for (int s = 0; s < S; ++s)
+    if (s < n_chunks) issue(s, s);
+  const int xsw = lane & 7;  // swizzle of this lane's x rows (row 32e + l, 1024-aligned blocks)
+  const unsigned char* xl = gbase + lane * 128;
+  // kSame (warp-uniform): every lane's K nonzeros lie in one row, so the lane
+  // reads one d_out chunk for all of them with no per-lane test
+  auto run = [&](auto staged_c, auto same_c) {
+    constexpr bool kStaged = decltype(staged_c)::value;
+    constexpr bool kSame = decltype(same_c)::value;
+    // staged d_out rows: row `slot` of the stage's d block; the block starts
+    // at a multiple of DS rows, so the swizzle of a row (address bits 7-9) is
+    // slot ^ (s * DS mod 8) for slot < DS.  Unstaged: the rows in global memory
+    auto dst_sw = [](int s) { return (s * DS) & 7; };
+    const unsigned char* dl[K];
+    const float* drow[K];
+    int dsw[K];
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      dl[e] = gbase + S * kXBytes + (kStaged ? slot[e] : 0) * 128;
+      dsw[e] = slot[e] & 7;
+      drow[e] = d_out + row[e] * ld_d;
+    }
+    for (int ch0 = 0; ch0 < n_chunks; ch0 += S) {
+      const unsigned parity = (unsigned)((ch0 / S) & 1);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int ch = ch0 + s;
+        if (ch >= n_chunks) break;
+        mbar_wait(bar0 + 8 * s, parity);
+        const int t0 = ch * 32;
+        const int cnt = min(32, n - t0);
+        if (cnt == 32) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            float4 xv[K], dv[K];
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+              xv[e] = *reinterpret_cast<const float4*>(xl + s * kXBytes + e * 4096 +
+                                                       16 * (u ^ xsw));
+              if constexpr (kStaged) {
+                if (e == 0 || (!kSame && slot[e] != slot[e - 1]))
+                  dv[e] = *reinterpret_cast<const float4*>(dl[e] + s * kDBytes +
+                                                           16 * (u ^ dsw[e] ^ dst_sw(s)));
+                else
+                  dv[e] = dv[e - 1];
+              } else {
+                // 16-byte aligned: sddmm_tma_supported
+                dv[e] = *reinterpret_cast<const float4*>(drow[e] + t0 + 4 * u);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+              acc[e] = add_rn(acc[e], mul_rn(dv[e].x, xv[e].x));
+              acc[e] = add_rn(acc[e], mul_rn(dv[e].y, xv[e].y));
+              acc[e] = add_rn(acc[e], mul_rn(dv[e].z, xv[e].z));
+              acc[e] = add_rn(acc[e], mul_rn(dv[e].w, xv[e].w));
+            }
+          }
         } else {
-          dv = make_float4(drow[t0 + 4 * u], drow[t0 + 4 * u + 1], drow[t0 + 4 * u + 2],
-                           drow[t0 + 4 * u + 3]);
+          for (int j = 0; j < cnt; ++j) {
+            const int u = j >> 2, q = j & 3;
+#pragma unroll
+            for (int e = 0; e < K; ++e) {
+              const float xv = reinterpret_cast<const float*>(xl + s * kXBytes + e * 4096 +
+                                                              16 * (u ^ xsw))[q];
+              const float dv =
+                  kStaged ? reinterpret_cast<const float*>(dl[e] + s * kDBytes +
+                                                           16 * (u ^ dsw[e] ^ dst_sw(s)))[q]
+                          : drow[e][t0 + j];
+              acc[e] = add_rn(acc[e], mul_rn(dv, xv));
+            }
+          }
         }
-        acc = add_rn(acc, mul_rn(dv.x, xv.x));
-        acc = add_rn(acc, mul_rn(dv.y, xv.y));
-        acc = add_rn(acc, mul_rn(dv.z, xv.z));
-        acc = add_rn(acc, mul_rn(dv.w, xv.w));
-      }
-    } else {
-      for (int j = 0; j < cnt; ++j) {
-        const int u = j >> 2, e = j & 3;
-        const float xv = xr[4 * (u ^ xsw) + e];
-        const float dv = kStaged ? dr[4 * (u ^ dsw) + e] : drow[t0 + j];
-        acc = add_rn(acc, mul_rn(dv, xv));
+        __syncwarp();  // every lane has read stage s: refill it
+        if (ch + S < n_chunks) issue(ch + S, s);
       }
     }
-    __syncwarp();  // every lane has read stage s: refill it
-    if (ch + S < n_chunks) issue(ch + S);
-  }
   };
-  if (staged)
-    run(std::true_type{});
+  bool same = true;
+#pragma unroll
+  for (int e = 1; e < K; ++e) same = same && slot[e] == slot[0];
+  same = K > 1 && __all_sync(0xffffffffu, same);
+  if (!staged)
+    run(std::false_type{}, std::false_type{});
+  else if (same)
+    run(std::true_type{}, std::true_type{});
   else
-    run(std::false_type{});
+    run(std::true_type{}, std::false_type{});
   pdl_trigger();
-  if (!active) return;
-  const float g = (n == 0) ? 0.f : acc;  // tensor_core.py:283-284: zero batch -> zeros
-  if (grad_out) grad_out[p] = g;
-  if (upd) {
-    apply_update(opt, g, &w_pre, &v_pre);
-    values_out[p] = w_pre;
-    if (velocity) velocity[p] = v_pre;
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    if (!act[e]) continue;
+    const float g = (n == 0) ? 0.f : acc[e];  // tensor_core.py:283-284: zero batch -> zeros
+    if (grad_out) grad_out[p[e]] = g;
+    if (has_opt) {
+      apply_update(opt, g, &w_pre[e], &v_pre[e]);
+      values_out[p[e]] = w_pre[e];
+      if (velocity) velocity[p[e]] = v_pre[e];
+    }
   }
 }
 
@@ -313,17 +410,33 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
     set_error("sddmm (TMA): tensor map encoding failed");
     return SMB_ERR_CUDA;
   }
-  auto go = [&](auto kernel, int s, int wpc, int ring) {
-    const size_t smem = (size_t)wpc * ring + 1024;
+// lab knobs (scripts/build_variant.sh): chains per lane, ring stages, staged
+// d_out rows in CSR order / in the blocked order (a warp spans more rows there)
+#ifndef SMB_TMA_DS_ORD
+#define SMB_TMA_DS_ORD 8
+#endif
+#ifndef SMB_TMA_K
+#define SMB_TMA_K 1
+#endif
+#ifndef SMB_TMA_S
+#define SMB_TMA_S 2
+#endif
+#ifndef SMB_TMA_DS
+#define SMB_TMA_DS 4
+#endif
+  constexpr int K = SMB_TMA_K, S = SMB_TMA_S, DS = SMB_TMA_DS;
+  auto gok = [&](auto kernel, int ds) {
+    // ring + barriers + slot rows + row window (sddmm_tmak_kernel)
+    const size_t smem = (size_t)S * (32 * K * 128 + ds * 128) + 8 * S + 8 * ds + 4 * (32 * K + 1);
     ensure_smem(kernel, smem);
-    launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, 32 * wpc)), dim3(32 * wpc), smem, st,
-             xmap, dmap, pat->row_ptr, pat->col_idx, pat->tile_row0, pat->ord_p, pat->ord_row,
-             pat->m, pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity, grad_out, opt);
+    launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, 32 * K)), dim3(32), smem, st, xmap, dmap,
+             pat->row_ptr, pat->col_idx, pat->tile_row0, pat->ord_p, pat->ord_row, pat->m,
+             pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity, grad_out, opt);
   };
   if (sddmm_use_blocked_order(pat, n))
-    go(sddmm_tma_kernel<2, 1, true>, 2, 1, warp_ring_bytes<2, 8>());
+    gok(sddmm_tmak_kernel<S, true, K, SMB_TMA_DS_ORD>, SMB_TMA_DS_ORD);
   else
-    go(sddmm_tma_kernel<2, 1, false>, 2, 1, warp_ring_bytes<2, 4>());
+    gok(sddmm_tmak_kernel<S, false, K, DS>, DS);
   return check_launch("smb_sddmm_update (TMA)");
 }
 
