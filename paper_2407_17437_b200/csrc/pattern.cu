@@ -139,6 +139,7 @@ void free_pattern(smb_pattern* p) {
   cudaFree(p->tile_row0);
   cudaFree(p->ord_p);
   cudaFree(p->ord_row);
+  cudaFree(p->acc_ws);
   delete p;
 }
 
@@ -285,6 +286,7 @@ extern "C" int smb_pattern_create(const int32_t* row_ptr, const int32_t* col_idx
       }
     if (cudaMalloc(&p->ord_p, sizeof(int32_t) * nnz) != cudaSuccess ||
         cudaMalloc(&p->ord_row, sizeof(int32_t) * nnz) != cudaSuccess ||
+        cudaMalloc(&p->acc_ws, sizeof(float) * nnz) != cudaSuccess ||
         cudaMemcpy(p->ord_p, op.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice) !=
             cudaSuccess ||
         cudaMemcpy(p->ord_row, orow.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice) !=

@@ -23,6 +23,7 @@ struct smb_pattern {
   // the CSR index of the q-th nonzero in that order, ord_row[q] its row.
   int32_t* ord_p = nullptr;    // owned, [nnz] or null
   int32_t* ord_row = nullptr;  // owned, [nnz] or null
+  float* acc_ws = nullptr;     // owned, [nnz] or null: chain sums carried between batch phases
   int bands = 0;
 };
 

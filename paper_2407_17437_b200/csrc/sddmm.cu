@@ -508,7 +508,9 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       // 677 -> 485 us, config 3 d=0.1 1364 -> 1236 us; more stages or warps
       // per CTA lower the resident warps and run slower.  Few-wave layers keep
       // the cp.async kernels: one warp's TMA chunks do not overlap well
-      // (config-2 layers 10-15 us -> 21-24 us with any ring depth).
+      // (config-2 layers 10-15 us -> 21-24 us with any ring depth; the
+      // rewritten kernel with 4-8 stages: 9-13 us -> 18-20 us, the serial
+      // ELECT / R2UR copy issue of each chunk is exposed at 1-5 warps per SM).
       // (rows of >= 16 nonzeros on average: a warp's 32 nonzeros then span
       // <= 4 rows and read d_out from the ring; very sparse rows -- config 3
       // d = 0.001, 8 per row -- keep the cp.async pipe with a d_out row per

@@ -103,7 +103,12 @@ __global__ void __launch_bounds__(32)
                       const int32_t* __restrict__ tile_row0, const int32_t* __restrict__ ord_p,
                       const int32_t* __restrict__ ord_row, int64_t m, int64_t nnz,
                       const float* __restrict__ d_out, int64_t ld_d, int n, const float* values,
-                      float* values_out, float* velocity, float* grad_out, OptConsts<float> opt) {
+                      float* values_out, float* velocity, float* grad_out, OptConsts<float> opt,
+                      int tb, int te, float* acc_io) {
+  // This launch sums the batch columns [tb, te) of every chain (a phase);
+  // phases run in column order, the partial sums carried in acc_io (indexed
+  // like the values) between them, so each chain's order over the batch is
+  // unchanged.  tb == 0 starts the chains, te == n finishes them (update).
   constexpr int kTile = 32 * K;
   constexpr int kXBytes = kTile * 128;
   constexpr int kDBytes = DS * 128;
@@ -208,7 +213,7 @@ __global__ void __launch_bounds__(32)
     for (int q = 0; q < DS; ++q) slot_row[q] = imin(row_first + imin(q, n_slots - 1), m - 1);
   }
   const bool staged = n_slots <= DS;  // warp-uniform
-  const int n_chunks = (n + 31) / 32;
+  const int n_chunks = (te - tb + 31) / 32;
   // copy roles: lane g < 8K gathers the shared-memory rows 4g..4g+3 (nonzero
   // K*l+e sits at row 32e + l), lanes 8K.. the staged d_out rows
   int gr[4];
@@ -236,21 +241,22 @@ __global__ void __launch_bounds__(32)
   float w_pre[K], v_pre[K], acc[K];
 #pragma unroll
   for (int e = 0; e < K; ++e) {
-    const bool upd = act[e] && has_opt;
+    const bool upd = act[e] && has_opt && te >= n;
     w_pre[e] = upd ? values[p[e]] : 0.f;
     v_pre[e] = (upd && velocity) ? velocity[p[e]] : 0.f;
-    acc[e] = -0.0f;  // exact additive identity (sddmm.cu)
+    // -0.0f: exact additive identity (sddmm.cu)
+    acc[e] = (tb > 0 && act[e]) ? acc_io[p[e]] : -0.0f;
   }
   auto issue = [&](int ch, int s) {
     const unsigned bar = bar0 + 8 * s;
     if (lane == 0) mbar_arrive_expect_tx(bar, tx_bytes);
     __syncwarp();
     if (lane < 8 * K)
-      tma_gather4(base + (unsigned)(s * kXBytes + lane * 512), &xmap, ch * 32, gr[0], gr[1],
+      tma_gather4(base + (unsigned)(s * kXBytes + lane * 512), &xmap, tb + ch * 32, gr[0], gr[1],
                   gr[2], gr[3], bar);
     else if (dcopier)
-      tma_gather4(dbase + (unsigned)(s * kDBytes + (lane - 8 * K) * 512), &dmap, ch * 32, gr[0],
-                  gr[1], gr[2], gr[3], bar);
+      tma_gather4(dbase + (unsigned)(s * kDBytes + (lane - 8 * K) * 512), &dmap, tb + ch * 32,
+                  gr[0], gr[1], gr[2], gr[3], bar);
   };
 #pragma unroll
   for (int s = 0; s < S; ++s)
@@ -282,8 +288,8 @@ __global__ void __launch_bounds__(32)
         const int ch = ch0 + s;
         if (ch >= n_chunks) break;
         mbar_wait(bar0 + 8 * s, parity);
-        const int t0 = ch * 32;
-        const int cnt = min(32, n - t0);
+        const int t0 = tb + ch * 32;
+        const int cnt = min(32, te - t0);
         if (cnt == 32) {
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
@@ -345,6 +351,10 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
   for (int e = 0; e < K; ++e) {
     if (!act[e]) continue;
+    if (te < n) {  // more phases follow
+      acc_io[p[e]] = acc[e];
+      continue;
+    }
     const float g = (n == 0) ? 0.f : acc[e];  // tensor_core.py:283-284: zero batch -> zeros
     if (grad_out) grad_out[p[e]] = g;
     if (has_opt) {
@@ -412,6 +422,9 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
   }
 // lab knobs (scripts/build_variant.sh): chains per lane, ring stages, staged
 // d_out rows in CSR order / in the blocked order (a warp spans more rows there)
+#ifndef SMB_TMA_PHASE_COLS
+#define SMB_TMA_PHASE_COLS 256
+#endif
 #ifndef SMB_TMA_DS_ORD
 #define SMB_TMA_DS_ORD 8
 #endif
@@ -425,17 +438,30 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
 #define SMB_TMA_DS 4
 #endif
   constexpr int K = SMB_TMA_K, S = SMB_TMA_S, DS = SMB_TMA_DS;
-  auto gok = [&](auto kernel, int ds) {
+  int tb = 0, te = (int)n;
+  auto gok = [&](auto kernel, int ds, int stages = SMB_TMA_S) {
     // ring + barriers + slot rows + row window (sddmm_tmak_kernel)
-    const size_t smem = (size_t)S * (32 * K * 128 + ds * 128) + 8 * S + 8 * ds + 4 * (32 * K + 1);
+    const size_t smem =
+        (size_t)stages * (32 * K * 128 + ds * 128) + 8 * stages + 8 * ds + 4 * (32 * K + 1);
     ensure_smem(kernel, smem);
     launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, 32 * K)), dim3(32), smem, st, xmap, dmap,
              pat->row_ptr, pat->col_idx, pat->tile_row0, pat->ord_p, pat->ord_row, pat->m,
-             pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity, grad_out, opt);
+             pat->nnz, d_out, ld_d, (int)n, values, values_out, velocity, grad_out, opt, tb, te,
+             pat->acc_ws);
   };
-  if (sddmm_use_blocked_order(pat, n))
-    gok(sddmm_tmak_kernel<S, true, K, SMB_TMA_DS_ORD>, SMB_TMA_DS_ORD);
-  else
+  if (sddmm_use_blocked_order(pat, n)) {
+    // x and d_out overflow L2 many times over (config 5 at B = 4096: 1 GB
+    // each).  One launch over the whole batch kept 27% of its gathers in L2
+    // and read 30 GB from HBM for 2.2 GB of operands (ncu): resident warps
+    // are at every stage of their chains, so a block's working set is its
+    // band rows x the whole batch.  Phases of kPhaseCols columns bound it to
+    // band rows x kPhaseCols x 4 bytes x 2 (27 MB at 13,300-row bands).
+    constexpr int kPhaseCols = SMB_TMA_PHASE_COLS;
+    for (tb = 0; tb < (int)n; tb = te) {
+      te = (kPhaseCols > 0 && pat->acc_ws) ? (int)imin(n, tb + kPhaseCols) : (int)n;
+      gok(sddmm_tmak_kernel<S, true, K, SMB_TMA_DS_ORD>, SMB_TMA_DS_ORD);
+    }
+  } else
     gok(sddmm_tmak_kernel<S, false, K, DS>, DS);
   return check_launch("smb_sddmm_update (TMA)");
 }

@@ -254,7 +254,9 @@ def test_blocked_order_sddmm_bit_exact(orc):
     times at the batch width walk their nonzeros in the pattern's L2-blocked
     order (row band x column band blocks, CSR order inside); each chain and
     the update are unchanged and land at the CSR index: bit-exact with the
-    oracle, ragged batch width included."""
+    oracle, ragged batch width included.  The batch is walked in phases of
+    256 columns (9 launches here, the last one ragged), the chain sums carried
+    between them in the pattern's workspace."""
     m = k = 30000
     n = 2300  # (m + k) * n * 4 bytes > 512 MB -> blocked order
     nnz = int(0.0005 * m * k)
