@@ -511,11 +511,12 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
       // (config-2 layers 10-15 us -> 21-24 us with any ring depth; the
       // rewritten kernel with 4-8 stages: 9-13 us -> 18-20 us, the serial
       // ELECT / R2UR copy issue of each chunk is exposed at 1-5 warps per SM).
-      // (rows of >= 16 nonzeros on average: a warp's 32 nonzeros then span
-      // <= 4 rows and read d_out from the ring; very sparse rows -- config 3
-      // d = 0.001, 8 per row -- keep the cp.async pipe with a d_out row per
-      // nonzero: 20 vs 27 us there)
-      if (!small32 && !small64 && !mid32 && pat->nnz >= 16 * pat->m &&
+      // (rows of >= 8 nonzeros on average: with 16 or more a warp's 32
+      // nonzeros span <= 4 rows, with 8-16 -- config 3 d = 0.001 -- the kernel
+      // stages 8 d_out rows per chunk: 17.2 -> 15.2 us at B = 512 and 106 ->
+      // 51 us at B = 2048 against the cp.async pipe with a d_out row per
+      // nonzero; sparser rows are not measured and keep the pipe)
+      if (!small32 && !small64 && !mid32 && pat->nnz >= 8 * pat->m &&
           sddmm_tma_supported(pat, d_out, ld_d, x, ld_x, n)) {
         const int rc = launch_sddmm_tma(pat, static_cast<const float*>(d_out), ld_d,
                                         static_cast<const float*>(x), ld_x, n,

@@ -461,7 +461,10 @@ int launch_sddmm_tma(const smb_pattern* pat, const float* d_out, int64_t ld_d, c
       te = (kPhaseCols > 0 && pat->acc_ws) ? (int)imin(n, tb + kPhaseCols) : (int)n;
       gok(sddmm_tmak_kernel<S, true, K, SMB_TMA_DS_ORD>, SMB_TMA_DS_ORD);
     }
-  } else
+  } else if (pat->nnz < 16 * pat->m)
+    // short rows: a warp's 32 nonzeros span more than 4 rows
+    gok(sddmm_tmak_kernel<S, false, K, 8>, 8);
+  else
     gok(sddmm_tmak_kernel<S, false, K, DS>, DS);
   return check_launch("smb_sddmm_update (TMA)");
 }
