@@ -108,4 +108,5 @@ def main(densities=(0.001, 0.01, 0.1), batches=(128, 512, 2048), iters=10):
 
 
 if __name__ == "__main__":
-    main()
+    # optional: densities to run, e.g. `python scripts/kernel_bench.py 0.001`
+    main(tuple(float(a) for a in sys.argv[1:]) or (0.001, 0.01, 0.1))
