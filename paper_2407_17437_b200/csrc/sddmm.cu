@@ -414,6 +414,160 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Lean one-warp tile kernel for few-wave fp32 layers (config 2: 1-5 warps per
+// SM).  With so few warps an SM's issue slots are idle and each warp runs at
+// its own instruction rate, so the time of a chain is the instruction count
+// of its chunk loop: sddmm_pipe_kernel spends ~270 instructions per 32-column
+// chunk (dynamic ring-stage arithmetic, 64-bit source address adds, full /
+// ragged issue branches, a CTA barrier) for 64 multiplies and adds.  Here the
+// chunk loop is unrolled over the S ring stages, so stage addresses and the
+// copies' column offsets are immediates, the source pointers advance once per
+// S chunks, and the warp synchronises with __syncwarp.  Same chains, order
+// and rounding; tiles must span <= DS rows (host check) and operands be
+// 16-byte aligned.
+template <int S, int DS>
+__global__ void __launch_bounds__(32)
+    sddmm_lean_kernel(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                      const int32_t* __restrict__ tile_row0, int64_t m, int64_t nnz,
+                      const float* __restrict__ d_out, int64_t ld_d, const float* __restrict__ x,
+                      int64_t ld_x, int n, const float* values, float* values_out,
+                      float* velocity, float* grad_out, OptConsts<float> opt) {
+  static_assert(S % 2 == 0 && DS % 4 == 0, "two register sets alternate over the stages");
+  constexpr int kStageFloats = (32 + DS) * 32;
+  constexpr unsigned kStageBytes = kStageFloats * 4;
+  constexpr int DC = DS / 4;  // d_out copies per lane and chunk
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* smem = reinterpret_cast<float*>(align128(smem_raw));
+  __shared__ int32_t s_col[32];
+  __shared__ int32_t s_rp[33];
+  const int lane = threadIdx.x;
+  const int64_t p0 = (int64_t)blockIdx.x * 32;
+  const int64_t p = p0 + lane;
+  const int n_active = (int)imin(32, nnz - p0);
+  const bool active = lane < n_active;
+  const int32_t r0 = tile_row0[blockIdx.x];
+  s_col[lane] = active ? col_idx[p] : 0;
+  s_rp[lane] = (r0 + lane <= m) ? row_ptr[r0 + lane] : INT32_MAX;
+  if (lane == 0) s_rp[32] = (r0 + 32 <= m) ? row_ptr[r0 + 32] : INT32_MAX;
+  __syncwarp();
+  const int64_t row = tile_row_of<32>(active ? p : p0, r0, s_rp, row_ptr, m);
+  const int slot = (int)(row - r0);  // < DS (host check)
+  const int64_t last_row = tile_row_of<32>(p0 + n_active - 1, r0, s_rp, row_ptr, m);
+  const int n_staged = (int)imin(DS, last_row - r0 + 1);
+  // copy slots of this lane: vector v of x rows lane/8 + 4k and of d_out rows lane/8 + 4c
+  const int v = lane & 7, rq = lane >> 3;
+  const float* xp[8];
+  unsigned xdst[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int r = rq + 4 * k;
+    xp[k] = x + (int64_t)s_col[r] * ld_x + v * 4;
+    xdst[k] = (unsigned)(swz<32, 4>(r, v) * 4);
+  }
+  bool dcopy[DC];
+  const float* dp[DC];
+  unsigned ddst[DC];
+#pragma unroll
+  for (int c = 0; c < DC; ++c) {
+    const int r = rq + 4 * c;
+    dcopy[c] = r < n_staged;
+    dp[c] = d_out + (int64_t)(r0 + (dcopy[c] ? r : 0)) * ld_d + v * 4;
+    ddst[c] = (unsigned)(swz<32, 4>(32 + r, v) * 4);
+  }
+  const unsigned sbase = smem_u32(smem);
+  pdl_wait();  // d_out / x are earlier kernels' outputs
+  const bool upd = active && opt.kind != SMB_OPT_NONE;
+  float w_pre = upd ? values[p] : 0.f;
+  float v_pre = (upd && velocity) ? velocity[p] : 0.f;
+  const int n_full = n / 32;
+  const int n_chunks = (n + 31) / 32;
+  // chunk `ch` into ring stage `stage`; `off` = its first column relative to
+  // the advancing source pointers (an immediate at every call site)
+  auto issue = [&](int ch, int stage, int off) {
+    const unsigned st = sbase + (unsigned)stage * kStageBytes;
+    if (ch < n_full) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cp_async16(st + xdst[k], xp[k] + off);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        if (dcopy[c]) cp_async16(st + ddst[c], dp[c] + off);
+    } else if (ch < n_chunks) {  // the ragged last chunk: zero-filled past n
+      const int valid = max(0, min(4, n - (ch * 32 + v * 4)));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cp_async16(st + xdst[k], xp[k] + off, valid * 4);
+#pragma unroll
+      for (int c = 0; c < DC; ++c)
+        if (dcopy[c]) cp_async16(st + ddst[c], dp[c] + off, valid * 4);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(s, s, s * 32);
+  // this lane's x row / d_out row vectors inside a stage
+  int xo[8], dof[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    xo[w] = swz<32, 4>(lane, w);
+    dof[w] = swz<32, 4>(32 + slot, w);
+  }
+  float acc = -0.0f;  // exact additive identity (sddmm_pipe_kernel)
+  float4 xr[2][8], dr[2][8];
+  auto sum8 = [&](const float4* xv, const float4* dv) {
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      acc = add_rn(acc, mul_rn(dv[w].x, xv[w].x));
+      acc = add_rn(acc, mul_rn(dv[w].y, xv[w].y));
+      acc = add_rn(acc, mul_rn(dv[w].z, xv[w].z));
+      acc = add_rn(acc, mul_rn(dv[w].w, xv[w].w));
+    }
+  };
+  // Chunk ch's shared-memory reads are issued before chunk ch-1's chain runs
+  // (two register sets; chunk parity == stage parity because S is even).
+  for (int ch0 = 0; ch0 < n_full; ch0 += S) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int ch = ch0 + s;
+      if (ch >= n_full) break;
+      cp_async_wait<S - 2>();
+      __syncwarp();  // chunk ch landed for every lane; stage (s - 1) % S is free
+      issue(ch + S - 1, (s + S - 1) % S, (s + S - 1) * 32);
+      const float* xs = smem + s * kStageFloats;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        xr[s & 1][w] = lds16(xs + xo[w]);
+        dr[s & 1][w] = lds16(xs + dof[w]);
+      }
+      if (ch > 0) sum8(xr[(s & 1) ^ 1], dr[(s & 1) ^ 1]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xp[k] += S * 32;
+#pragma unroll
+    for (int c = 0; c < DC; ++c) dp[c] += S * 32;
+  }
+  if (n_full > 0) {
+    if ((n_full - 1) & 1) sum8(xr[1], dr[1]);
+    else sum8(xr[0], dr[0]);
+  }
+  cp_async_wait<0>();
+  if (n_full < n_chunks) {  // ragged last chunk
+    __syncwarp();
+    const float* xs = smem + (n_full % S) * kStageFloats;
+    const int cnt = n - n_full * 32;
+    for (int j = 0; j < cnt; ++j)
+      acc = add_rn(acc, mul_rn(xs[swz<32, 4>(32 + slot, j / 4) + j % 4],
+                               xs[swz<32, 4>(lane, j / 4) + j % 4]));
+  }
+  pdl_trigger();
+  if (!active) return;
+  const float g = (n == 0) ? 0.f : acc;  // tensor_core.py:283-284: zero batch -> zeros
+  if (grad_out) grad_out[p] = g;
+  if (upd) {
+    apply_update(opt, g, &w_pre, &v_pre);
+    values_out[p] = w_pre;
+    if (velocity) velocity[p] = v_pre;
+  }
+}
+
 }  // namespace
 
 template <typename T>
@@ -528,6 +682,62 @@ int sddmm_update_impl(const smb_pattern* pat, const void* d_out, int64_t ld_d, c
         warp_done = true;
       } else if (!small32 && !small64 && !mid32 && warp_kernel) {
         go(sddmm_warp_kernel<T, 32, 2>, 128, SddmmWarpCfg<T, 32, 2>::smem_bytes);
+        warp_done = true;
+      }
+    }
+#ifndef SMB_LEAN
+#define SMB_LEAN 1
+#endif
+#ifndef SMB_LEAN_MID_S
+#define SMB_LEAN_MID_S 6
+#endif
+#ifndef SMB_LEAN_MID_DS
+#define SMB_LEAN_MID_DS 4
+#endif
+#ifndef SMB_LEAN_SMALL_S
+#define SMB_LEAN_SMALL_S 6
+#endif
+#ifndef SMB_LEAN_SMALL_DS
+#define SMB_LEAN_SMALL_DS 4
+#endif
+    if constexpr (sizeof(T) == 4 && SMB_LEAN != 0) {
+      // few-wave layers whose 32-nonzero tiles span <= 8 rows: the lean
+      // one-warp kernel (sddmm_lean_kernel).  Measured on B200 at config 2
+      // (scripts/gpu_ab_bench2.sh; kernel alone graph-timed / step with the L2
+      // flush / step back to back):
+      //   layer 0 (1024 x 3072, 5.2 tiles per SM) alone: pipe 13.05 us, lean
+      //     6 stages 11.1-11.3 us, 4 stages 10.9 us, 8 stages x 8 d_out rows
+      //     14.8 us (41 KB per CTA: the SMs that get 6 tiles run two waves);
+      //   layers 1 / 2 (1-2 tiles per SM) alone: pipe 8.6 / 8.4 us, lean 8
+      //     stages 7.7 / 7.4 us, 6 stages 8.0 / 7.8 us;
+      //   the step, where the three kernels share the SMs' shared memory with
+      //     each other and the next batch's gather, follows the footprints
+      //     rather than the kernels' own times -- pipe kernels 66.5 / 59.7 us;
+      //     (layer 0 stages x rows, layers 1-2 stages x rows): 6x4 + 6x4 62.4 /
+      //     55.9 us (kept), 8x8 + 8x8 63.5 / 56.7, 6x4 + 4x4 64.4 / 57.6, 6x8 +
+      //     6x8 65.4 / 58.1, 4x4 + 8x8 65.6 / 58.3, 6x4 + 8x8 65.9 / 59.3, 6x8 +
+      //     6x4 66.3 / 59.8, 6x4 + 8x4 66.4 / 60.0, 6x4 + 6x8 66.6 / 59.9, 4x4 +
+      //     6x4 67.3 / 59.8, 8x8 + 8x4 72.4 / 58.0.
+      if (!warp_done && vec && (mid32 || small32) && pat->span32 <= 8 && n < (int64_t(1) << 30)) {
+        auto lean = [&](auto kernel, int stages, int ds) {
+          const size_t bytes = (size_t)stages * (32 + ds) * 128 + 128;
+          ensure_smem(kernel, bytes);
+          launch_k(kernel, dim3((unsigned)ceil_div(pat->nnz, 32)), dim3(32), bytes, st,
+                   pat->row_ptr, pat->col_idx, pat->tile_row0, pat->m, pat->nnz,
+                   static_cast<const float*>(d_out), ld_d, static_cast<const float*>(x), ld_x,
+                   (int)n, static_cast<const float*>(values), static_cast<float*>(values_out),
+                   static_cast<float*>(velocity), static_cast<float*>(grad_out), opt);
+        };
+        if (small32 && pat->span32 <= SMB_LEAN_SMALL_DS)
+          lean(sddmm_lean_kernel<SMB_LEAN_SMALL_S, SMB_LEAN_SMALL_DS>, SMB_LEAN_SMALL_S,
+               SMB_LEAN_SMALL_DS);
+        else if (small32)
+          lean(sddmm_lean_kernel<SMB_LEAN_SMALL_S, 8>, SMB_LEAN_SMALL_S, 8);
+        else if (pat->span32 <= SMB_LEAN_MID_DS)
+          lean(sddmm_lean_kernel<SMB_LEAN_MID_S, SMB_LEAN_MID_DS>, SMB_LEAN_MID_S,
+               SMB_LEAN_MID_DS);
+        else
+          lean(sddmm_lean_kernel<SMB_LEAN_MID_S, 8>, SMB_LEAN_MID_S, 8);
         warp_done = true;
       }
     }
