@@ -287,6 +287,11 @@ class FusedTrainStep:
                   for u in self.units if not u.sparse and u.m <= DENSE_T_MAX_ROWS] or [0])
         self._dense_ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev) if nb else None
         self.overlap = True
+        # where the next batch is gathered in the chain-kernel step: beside the
+        # chain kernel (True) or beside the weight sides at the end (False)
+        # (config 2: 56.5 -> 53.6 us back to back once the lean SDDMMs left the
+        # gather as the tail of the step; before them it was within 1 us)
+        self.prefetch_beside_chain = True
         self._parity = 0
         self._sides = {}
         for u in self.units:
@@ -585,8 +590,9 @@ class FusedTrainStep:
                 self._gather_into(1 - self._slot, stream_ptr(), ahead=True)
 
         if self._chain is not None and fuse_update and overlap:
-            self._launch_chain_step(eta, x_in, t_in, fork, main)
-            if gather:
+            early = gather and self.prefetch_beside_chain
+            self._launch_chain_step(eta, x_in, t_in, fork, main, prefetch if early else None)
+            if gather and not early:
                 prefetch()
             for s_ in forked:
                 main.wait_stream(s_)
@@ -710,7 +716,7 @@ class FusedTrainStep:
         for s_ in forked:
             main.wait_stream(s_)  # join: the step ends when every update has
 
-    def _launch_chain_step(self, eta, x_in, t_in, fork, main) -> None:
+    def _launch_chain_step(self, eta, x_in, t_in, fork, main, prefetch=None) -> None:
         """Single-GPU step through the column-chain kernel: layer 0's forward
         SpMM, then ONE cluster launch for layers 1..L-1 forward, the softmax
         step and every input gradient (csrc/chain.cu), then every layer's
@@ -726,6 +732,8 @@ class FusedTrainStep:
         self._call("spmm[0]", "smb_spmm_p", F32, u0.layer.weights.pattern.handle,
                    ptr(self._vals(u0)), ptr(x_in), ld, B, ptr(u0.layer.bias),
                    _lib.SMB_EPI_RELU if u0.relu else _lib.SMB_EPI_NONE, ptr(self.acts[0]), ld, st)
+        if prefetch is not None:
+            prefetch()  # the next batch's gather beside the chain kernel
         arr = C.c_void_p * L
         bias = arr(*[ptr(u.layer.bias) for u in us])
         acts = arr(*[ptr(a) for a in self.acts])
