@@ -4,7 +4,7 @@
 # usage: bash scripts/gpu_profile_step.sh NAME LAYERS DENSITY BATCH [keep_rep]
 NAME=$1; L=$2; D=$3; B=$4; KEEP=$5
 mkdir -p gpurun_out
-RX='regex:row_spmm|sddmm_pipe|sddmm_warp|sddmm_tma|softmax_step|gather_columns|bias_rows|deep_kernel|spmv|values_to_csc|dense_|chain_kernel|padded_refresh'
+RX='regex:row_spmm|sddmm_pipe|sddmm_warp|sddmm_tma|sddmm_lean|softmax_step|gather_columns|bias_rows|deep_kernel|spmv|values_to_csc|dense_|chain_kernel|padded_refresh'
 CMD="python scripts/ncu_step.py $L $D $B 3 gpurun_out/${NAME}_tags.txt"
 timeout 300 $CMD > gpurun_out/${NAME}_plain.log 2>&1 || { echo "plain failed"; cat gpurun_out/${NAME}_plain.log; exit 1; }
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k "$RX" \
