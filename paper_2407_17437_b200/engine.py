@@ -323,7 +323,7 @@ class FusedTrainStep:
         # most 16 classes, operands within shared memory)
         self._chain = None
         self._chain_ws = None
-        if chain and self.overlap and not self.dp:
+        if chain and self.overlap:
             self._chain = self._make_chain_plan()
         self.sync_weights()
 
@@ -589,9 +589,10 @@ class FusedTrainStep:
             with torch.cuda.stream(fork("prefetch")) if overlap else _nullctx():
                 self._gather_into(1 - self._slot, stream_ptr(), ahead=True)
 
-        if self._chain is not None and fuse_update and overlap:
+        if self._chain is not None and overlap and (fuse_update or comm):
             early = gather and self.prefetch_beside_chain
-            self._launch_chain_step(eta, x_in, t_in, fork, main, prefetch if early else None)
+            self._launch_chain_step(eta, x_in, t_in, fork, main, prefetch if early else None,
+                                    comm=comm)
             if gather and not early:
                 prefetch()
             for s_ in forked:
@@ -716,12 +717,17 @@ class FusedTrainStep:
         for s_ in forked:
             main.wait_stream(s_)  # join: the step ends when every update has
 
-    def _launch_chain_step(self, eta, x_in, t_in, fork, main, prefetch=None) -> None:
-        """Single-GPU step through the column-chain kernel: layer 0's forward
-        SpMM, then ONE cluster launch for layers 1..L-1 forward, the softmax
-        step and every input gradient (csrc/chain.cu), then every layer's
-        weight side (bias row sums + update, SDDMM + update) concurrently on
-        the layers' side streams, the first layer's (the longest SDDMM) first."""
+    def _launch_chain_step(self, eta, x_in, t_in, fork, main, prefetch=None,
+                           comm: bool = False) -> None:
+        """Step through the column-chain kernel: layer 0's forward SpMM, then
+        ONE cluster launch for layers 1..L-1 forward, the softmax step and
+        every input gradient (csrc/chain.cu), then every layer's weight side
+        concurrently on the layers' side streams, the first layer's (the
+        longest SDDMM) first.  Single GPU: SDDMM + update and bias row sums +
+        update fused.  Data parallel (comm): the gradients go to the layer's
+        flat bucket, which is summed over the ranks and applied on that
+        stream (same bucket order on every rank), then the chain's padded
+        value copies are refreshed."""
         import ctypes as C
 
         st = stream_ptr()
@@ -743,11 +749,17 @@ class FusedTrainStep:
         for li in [0] + list(range(L - 1, 0, -1)):
             u = us[li]
             x_prev = self.acts[li - 1] if li > 0 else x_in
-            b, vb, gb, kind, mu = self._bias_target(u, True)
+            b, vb, gb, kind, mu = self._bias_target(u, not comm)
             with torch.cuda.stream(fork(("weights", li))):
-                self._weight_side(u, self.dys[li], x_prev, eta, True, stream_ptr())
+                self._weight_side(u, self.dys[li], x_prev, eta, not comm, stream_ptr())
                 self._call(f"bias[{li}]", "smb_bias_grad_update", F32, ptr(self.dys[li]), ld,
                            u.m, B, b, vb, gb, kind, mu, float(eta), stream_ptr())
+                if comm:
+                    self._allreduce_bucket(u)
+                    self._update_unit_from_flat(u, eta, stream_ptr())
+                    if li > 0:
+                        self._call(f"chain_refresh[{li}]", "smb_chain_refresh", self._chain.h,
+                                   li, ptr(self._vals(u)), stream_ptr())
 
     def _side_stream(self, key):
         s_ = self._sides.get(key)
