@@ -197,8 +197,10 @@ SMB_API int smb_sddmm_update(int dtype, const smb_pattern* pattern, const void* 
  * layer (which must see the pre-update weights, train.py:400-401) can run
  * concurrently with the update on another stream.
  * opt_kind may carry SMB_HINT_CONCURRENT (OR-ed in): the launch shares the
- * GPU with other kernels, so small layers take the staging ring with the
- * smallest shared-memory footprint (same results bit for bit). */
+ * GPU with other kernels, so small layers on the general cp.async kernel take
+ * the staging ring with the smallest shared-memory footprint (same results
+ * bit for bit; the lean one-warp kernel's ring was chosen inside the step and
+ * ignores the hint). */
 #define SMB_HINT_CONCURRENT 0x100
 SMB_API int smb_sddmm_update_into(int dtype, const smb_pattern* pattern, const void* d_out,
                                   int64_t ld_dout, const void* x, int64_t ld_x, int64_t n,
