@@ -1199,8 +1199,19 @@ static int gather_launch(int dtype, const void* src, int64_t n_samples, int64_t 
     using T = decltype(tag);
     dim3 grid((unsigned)ceil_div(batch, 32), (unsigned)ceil_div(features, 128));
     const bool vec = aligned16(src) && (features * (int64_t)sizeof(T)) % 16 == 0;
+#ifndef SMB_GATHER_PAD
+#define SMB_GATHER_PAD 24576
+#endif
+    // The gather AHEAD runs beside the training step's kernels; in the
+    // chain-kernel step beside the chain, whose CTAs fill 128 SMs with 204 KB
+    // of shared memory each.  A 24 KB shared-memory reservation (unused) keeps
+    // the gather's CTAs off those SMs, on the 20 the chain leaves free: the
+    // chain is no longer slowed by them (config 2: 60.8 -> 58.4 us per step
+    // with the L2 flush, 19.0 -> 19.2 M samples/s back to back; 6 / 12 / 16 /
+    // 28 KB: 59.4 / 59.4 / 59.5 / 58.5 us).
+    const size_t pad = step_counter != nullptr ? SMB_GATHER_PAD : 0;
     if (vec)
-      launch_k(gather_columns_kernel<T, true>, grid, dim3(256), 0, as_stream(stream),
+      launch_k(gather_columns_kernel<T, true>, grid, dim3(256), pad, as_stream(stream),
                static_cast<const T*>(src), features, perm, step_counter, base, step_offset,
                modulo, batch, static_cast<T*>(dst), ld_dst);
     else
